@@ -1,0 +1,309 @@
+"""Benchmark: trace intervals/s -> full host + device TALP metric tree.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl engine|reference]
+
+One step = one pass of the hot path (validate + summarize_host +
+summarize_device + both metric trees, i.e. ``compute_report``) over the
+config-shaped synthetic trace.  ``value`` is whole-job intervals/s with the
+SoA already resident in HBM (generated there by the engine's generator);
+``e2e`` is the same metric through the C ABI from pinned HOST buffers, H2D
+copies and the result D2H inside the timed region.  Weak scaling: at N GPUs
+every rank owns a C-sized rank block of an N-times larger trace.
+
+``--impl reference`` times the CPU reference path (the C oracle port of the
+reference algorithm, all host threads) on a bounded sample of the same
+workload; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BYTES_PER_INTERVAL = 21      # start u64 + end u64 + res i32 + kind u8
+METRIC = "trace intervals/sec -> full TALP metric tree (1/2/4/8 B200, % HBM roofline)"
+UNIT = "intervals/s"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def _traffic():
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except Exception:
+            return None
+    return None
+
+
+class Clocks:
+    """nvidia-smi sampling of SM clocks / throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        try:
+            rows = [ln.split(",") for ln in Path(self.path).read_text().splitlines() if ln.strip()]
+        except Exception:
+            rows = []
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 5 + i and "Active" in r[5 + i]
+                          and "Not" not in r[5 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _global_config(name: str, world: int):
+    from paper_2603_26576_b200.configs import CONFIGS, Config
+    c = CONFIGS[name]
+    if world == 1:
+        return c
+    return Config(f"{c.name}x{world}", c.description, c.n_ranks * world, c.gpus_per_rank,
+                  c.host_records * world, c.dev_records * world, c.overlap, c.serialized_dev, c.dur_scale0,
+                  c.seed, c.kernel_pct)
+
+
+# ---------------------------------------------------------------------------
+# reference arm: CPU oracle port on a bounded sample
+# ---------------------------------------------------------------------------
+def _cpu_sample(cfg, target_intervals: int):
+    from oracle import gen as ogen
+    per_rank = cfg.intervals / cfg.n_ranks
+    ranks = max(1, min(cfg.n_ranks, int(target_intervals // per_rank)))
+    (h, d) = ogen.generate(cfg, 0, ranks)
+    return h, d, ranks, ranks * cfg.gpus_per_rank, h[0].size + d[0].size
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    cfg = _global_config(args.config, world)
+    h, d, n, m, k = _cpu_sample(cfg, args.cpu_sample)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        O.analyze(h, d, n, m, nthreads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        r = O.analyze(h, d, n, m, nthreads=threads)
+        times.append(time.perf_counter() - t0)
+        assert r.status == 0
+    sec = sum(times) / len(times)
+    value = k / sec
+    sample = f"first {n} of {cfg.n_ranks} ranks of {cfg.name} ({k} intervals), numpy-generated"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": cfg.name, "intervals": cfg.intervals, "ranks": cfg.n_ranks,
+                   "devices": cfg.n_devices, "parallelism": f"dp{world}"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# engine arm
+# ---------------------------------------------------------------------------
+def run_engine(args, world, rank, local):
+    import numpy as np
+    import torch
+
+    from paper_2603_26576_b200 import _native as N
+    from paper_2603_26576_b200.engine import DeviceTrace, analyze_device, analyze_host_columns
+    from paper_2603_26576_b200.synth import generate
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = _global_config(args.config, world)
+    per = cfg.n_ranks // world
+    r0, r1 = rank * per, (rank + 1) * per
+    dt = generate(cfg, r0, r1, device=local)
+    intervals_local = dt.host_count + dt.dev_count
+    intervals_total = intervals_local * world
+    stream = torch.cuda.current_stream(local)
+
+    def sync():
+        torch.cuda.synchronize(local)
+        if dist:
+            dist.barrier()
+
+    from paper_2603_26576_b200.sharded import combine_shards
+
+    def step():
+        f = analyze_device(dt, N.MODE_REPORT, stream=stream.cuda_stream, device=local)
+        if dist:
+            f = combine_shards(f, dt, dist, local, stream.cuda_stream)
+        return f
+
+    for _ in range(max(args.warmup, 3)):
+        f = step()
+    assert f.status == N.OK, f.status
+    kernel_ms = []
+    sync()
+    with Clocks(local) as clk:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            f = step()
+            kernel_ms.append(f.kernel_ms)
+        ev1.record(stream)
+        sync()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = intervals_total / (ms / 1e3)
+
+    # e2e: same call from pinned host buffers (H2D + result D2H inside the timed region)
+    pinned = DeviceTrace(*(x.cpu().pin_memory() for x in (dt.h_start, dt.h_end, dt.h_res, dt.h_kind,
+                                                          dt.d_start, dt.d_end, dt.d_res, dt.d_kind)),
+                         dt.n, dt.m)
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    analyze_host_columns(pinned, stream=stream.cuda_stream, device=local)
+    sync()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        fe = analyze_host_columns(pinned, stream=stream.cuda_stream, device=local)
+        if dist:
+            fe = combine_shards(fe, dt, dist, local, stream.cuda_stream)
+    sync()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+    if dist:
+        t = torch.tensor([e2e_ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    assert fe.status == N.OK and fe.elapsed == f.elapsed
+    h2d = intervals_local * BYTES_PER_INTERVAL
+    d2h = 160 + (dt.n + dt.m) * 32
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    peak, peak_kind = _peaks()
+    kms = statistics.mean(kernel_ms)
+    achieved = intervals_local * BYTES_PER_INTERVAL / (kms / 1e3) / 1e9
+    traffic = _traffic()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic (generated in HBM by the engine's K0 generator)",
+        "config": {"workload": cfg.name, "intervals": intervals_total, "intervals_per_gpu": intervals_local,
+                   "ranks": cfg.n_ranks, "devices": cfg.n_devices, "parallelism": f"dp{world} (rank-sharded)",
+                   "l2": "inputs larger than L2 (21 B x intervals >> 126 MB)"},
+        "e2e": {"value": intervals_total / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+        "gpu_launches": args.steps * (1 if world == 1 else 3),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_source": peak_kind,
+                     "traffic": (traffic or {}).get("bytes_per_launch") if traffic and
+                     traffic.get("workload") == cfg.name else None,
+                     "kernel": "hb::analyze_kernel", "kernel_ms": kms,
+                     "algorithmic_bytes_per_launch": intervals_local * BYTES_PER_INTERVAL},
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+        h, d, n, m, k = _cpu_sample(cfg, args.cpu_sample)
+        threads = os.cpu_count() or 1
+        O.analyze(h, d, n, m, nthreads=threads)
+        t0 = time.perf_counter()
+        reps = 0
+        while True:
+            O.analyze(h, d, n, m, nthreads=threads)
+            reps += 1
+            if time.perf_counter() - t0 > args.cpu_seconds:
+                break
+        sec = (time.perf_counter() - t0) / reps
+        line["cpu_baseline"] = {"value": k / sec, "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": f"C oracle on first {n} of {cfg.n_ranks} ranks of {cfg.name} "
+                                          f"({k} intervals), {reps} reps"}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-sample", type=float, default=2e7)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = _dist()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_engine(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,189 @@
+/*
+ * heteff_b200.h -- C ABI of the B200 engine for the heteff hot path
+ *                  (state-interval trace -> host + device POP/TALP metric tree).
+ *
+ * The reference (`heteff`, pure Python) has no native FFI; its drop-in
+ * surface is the Python API of pkg/src/heteff/__init__.py:3-51.  Each entry
+ * point below is what a ctypes/cffi binding of that API binds, one per
+ * reference stage function:
+ *
+ *   heteff_analyze(mode=REPORT)            <- compute_report   metrics.py:125-154
+ *   heteff_analyze(mode=VALIDATE)          <- validate         model.py:160-230
+ *   heteff_analyze(mode=SUMMARIZE_HOST)    <- summarize_host   summarize.py:57-92
+ *   heteff_analyze(mode=SUMMARIZE_DEVICE)  <- summarize_device summarize.py:95-138
+ *   heteff_host_metrics                    <- host_metrics     metrics.py:66-93
+ *   heteff_device_metrics                  <- device_metrics   metrics.py:96-122
+ *   heteff_analyze_host                    <- same, from HOST buffers (copies inside)
+ *   heteff_generate                        <- (no reference counterpart) synthetic
+ *                                             config-shaped traces written in HBM
+ *
+ * Conventions: plain pointers and sizes only, no torch types.  Record
+ * columns are device pointers for heteff_analyze / heteff_generate and host
+ * pointers for heteff_analyze_host.  All outputs (heteff_result and
+ * heteff_outputs) are HOST memory; every call is stream-ordered on the
+ * given stream and returns after the results are on the host.  A context
+ * is not thread-safe; use one per thread / stream.  Status codes map 1:1
+ * onto the reference's exceptions (see heteff_status).
+ *
+ * Packed SoA record layout (one set for host records, one for device):
+ *   start u64[count], end u64[count]      half-open [start, end) ns (model.py:39-48)
+ *   res   i32[count]                      dense resource id in [0, ids)
+ *   kind  u8 [count]                      host: 0 useful 1 offload 2 mpi
+ *                                         dev : 0 kernel 1 memory   (model.py:24-36)
+ * Records must be grouped by res in ascending order and start-sorted
+ * within a group -- the reference's canonical order (model.py:74-80,
+ * 99-107) once dense ids follow the reference id order.  Violations are
+ * detected per record and reported as HETEFF_CONTRACT (never silently
+ * mis-summarized).  The stream column of the reference is never read
+ * (summaries are stream-oblivious) and is not part of the ABI.
+ */
+#ifndef HETEFF_B200_H
+#define HETEFF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HETEFF_ABI_VERSION 1
+
+typedef enum {
+    HETEFF_OK = 0,
+    HETEFF_INVALID_TRACE = 1,   /* -> InvalidTraceError   (model.py:130-137)  */
+    HETEFF_ANALYSIS_ERROR = 2,  /* -> AnalysisError       (metrics.py:136-137) */
+    HETEFF_VALUE_ERROR = 3,     /* -> ValueError          (summarize.py:103-104, metrics.py:75-78) */
+    HETEFF_CONTRACT = 4,        /* input not in canonical order / bad kind code */
+    HETEFF_CUDA_ERROR = 5,
+    HETEFF_NOMEM = 6,
+    HETEFF_BAD_ARG = 7
+} heteff_status;
+
+typedef enum {
+    HETEFF_MODE_REPORT = 0,
+    HETEFF_MODE_SUMMARIZE_DEVICE = 1,
+    HETEFF_MODE_VALIDATE = 2,
+    HETEFF_MODE_SUMMARIZE_HOST = 3
+} heteff_mode;
+
+/* index-list classes of heteff_result.counts / heteff_outputs.lists */
+enum {
+    HETEFF_HOST_MALFORMED = 0,  /* start > end                 model.py:152-153 */
+    HETEFF_HOST_ZERO = 1,       /* zero-length (warning)       model.py:155-156 */
+    HETEFF_HOST_UNDECLARED = 2, /* rank not declared           model.py:195-196 */
+    HETEFF_HOST_OVERLAP = 3,    /* overlap with earlier record model.py:203-215 */
+    HETEFF_DEV_MALFORMED = 4,
+    HETEFF_DEV_ZERO = 5,
+    HETEFF_DEV_UNDECLARED = 6,  /* device not declared         model.py:222-223 */
+    HETEFF_DEV_LATE = 7,        /* ends after host elapsed     model.py:224-228 */
+    HETEFF_NUM_LISTS = 8
+};
+
+/* contract_flags bits */
+enum {
+    HETEFF_CONTRACT_HOST_ORDER = 1,
+    HETEFF_CONTRACT_DEV_ORDER = 2,
+    HETEFF_CONTRACT_HOST_KIND = 4,
+    HETEFF_CONTRACT_DEV_KIND = 8
+};
+
+typedef struct {
+    const uint64_t *start;
+    const uint64_t *end;
+    const int32_t *res;
+    const uint8_t *kind;
+    int64_t count;
+} heteff_records;
+
+typedef struct {
+    heteff_records host;
+    heteff_records dev;
+    int32_t host_ids;           /* size of the dense host id space */
+    int32_t dev_ids;
+    const int32_t *host_decl;   /* [host_ids] declaration position or -1; NULL = identity */
+    const int32_t *dev_decl;    /* (same memory space as the record columns)             */
+    int32_t n;                  /* number of distinct declared ranks   */
+    int32_t m;                  /* number of distinct declared devices */
+    uint64_t host_elapsed_floor;/* max end of host records kept out of the SoA (0 if none) */
+} heteff_trace;
+
+typedef struct {
+    int32_t mode;               /* heteff_mode */
+    int32_t reserved;
+    uint64_t elapsed;           /* SUMMARIZE_DEVICE: the explicit elapsed window */
+    int64_t list_capacity;      /* capacity of each heteff_outputs list (0 = counts only) */
+} heteff_options;
+
+typedef struct {
+    int32_t status;             /* heteff_status */
+    int32_t contract_flags;
+    int64_t contract_index;     /* first offending record (min over violations) */
+    uint64_t host_elapsed;      /* max end over all host records (model.py:217) */
+    uint64_t elapsed;           /* E (summarize.py:88-91) or the explicit window */
+    uint64_t dev_max_end;       /* max end over all device records */
+    int32_t host_present;       /* n >= 1 */
+    int32_t device_present;     /* m >= 1 */
+    double host_metrics[5];     /* PE, MPI PE, MPI CE, MPI LB, device offload eff. */
+    uint32_t host_mask;         /* bit i set: host_metrics[i] defined (else None) */
+    uint32_t device_mask;
+    double device_metrics[4];   /* PE, LB, CE, orchestration eff. */
+    int64_t counts[HETEFF_NUM_LISTS];
+    double kernel_ms;           /* device time of the analysis kernel (CUDA events) */
+} heteff_result;
+
+typedef struct {
+    uint64_t *host_summaries;   /* [n][4] useful, offload, mpi, span_end (declaration order) */
+    uint64_t *device_summaries; /* [m][4] kernel, memory, idle, clamped  (declaration order) */
+    int64_t *lists[HETEFF_NUM_LISTS]; /* record indices, unordered, list_capacity each */
+} heteff_outputs;
+
+typedef struct heteff_ctx heteff_ctx;
+
+int heteff_abi_version(void);
+heteff_ctx *heteff_create(int device);
+void heteff_destroy(heteff_ctx *ctx);
+const char *heteff_last_error(const heteff_ctx *ctx);
+
+/* trace columns in device memory */
+int heteff_analyze(heteff_ctx *ctx, const heteff_trace *trace, const heteff_options *opt,
+                   heteff_result *result, const heteff_outputs *out, void *stream);
+
+/* trace columns in host memory (pinned for full PCIe rate); H2D inside */
+int heteff_analyze_host(heteff_ctx *ctx, const heteff_trace *trace, const heteff_options *opt,
+                        heteff_result *result, const heteff_outputs *out, void *stream);
+
+/* overlap errors: cover index of each listed record (model.py:208-215), host memory */
+int heteff_overlap_covers(heteff_ctx *ctx, const heteff_trace *trace, int host_columns_on_host,
+                          const int64_t *error_idx, int64_t count, int64_t *cover_idx, void *stream);
+
+/* metric trees from summaries (host memory [k][4] as laid out in heteff_outputs) */
+int heteff_host_metrics(heteff_ctx *ctx, const uint64_t *summaries, int32_t n, uint64_t elapsed,
+                        double metrics[5], uint32_t *mask, void *stream);
+int heteff_device_metrics(heteff_ctx *ctx, const uint64_t *summaries, int32_t m, uint64_t elapsed,
+                          double metrics[4], uint32_t *mask, void *stream);
+
+/* ---- synthetic config-shaped traces (counter-based RNG, bit-identical to oracle/gen.py) ---- */
+typedef struct {
+    uint64_t seed;
+    int32_t n_res;              /* resources generated by this call (local ids 0..n_res-1) */
+    int32_t res_base;           /* global id of local resource 0 (rank sharding); RNG keys use global ids */
+    int64_t per_res;            /* records per resource ...                                   */
+    int32_t extra_below;        /* ... plus one for global ids < extra_below                  */
+    int32_t serialized;         /* 1: start_j = sum(gap+dur) like a host chain, 0: arrival process */
+    int64_t count;              /* total records of this call (must match per_res/extra_below) */
+    uint32_t gap_max;           /* gap / inter-arrival ~ U[0, gap_max] */
+    uint32_t dur_max;           /* duration ~ U[1, dur_max] */
+    uint32_t dur_scale0;        /* duration multiplier for resource 0 (imbalance), >= 1 */
+    uint32_t kernel_pct;        /* device side: P(kind == kernel) in percent */
+    int32_t is_host;            /* 1: kind = state U{0,1,2}; 0: kind per kernel_pct */
+    int32_t reserved;
+} heteff_gen_side;
+
+int heteff_generate(heteff_ctx *ctx, const heteff_gen_side *side, uint64_t *start, uint64_t *end,
+                    int32_t *res, uint8_t *kind, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HETEFF_B200_H */

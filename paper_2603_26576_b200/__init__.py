@@ -1,0 +1,46 @@
+"""B200-native engine for the heteff hot path: state-interval traces -> the
+host + device POP/TALP efficiency trees (arXiv 2603.26576).
+
+Drop-in for the reference package's hot-path API (``heteff/__init__.py:3-51``):
+the trace model types plus ``validate``, ``summarize_host``,
+``summarize_device``, ``host_metrics``, ``device_metrics`` and
+``compute_report``, all computed by hand-written sm_100a CUDA kernels behind
+the C ABI in ``include/heteff_b200.h``.  Large traces use the columnar path
+(:mod:`.engine` ``analyze_device``) with the SoA already in HBM.
+"""
+
+from .api import (
+    AnalysisError,
+    DeviceMetrics,
+    DeviceSummary,
+    HostMetrics,
+    HostSummary,
+    MetricsReport,
+    compute_report,
+    device_metrics,
+    host_metrics,
+    summarize_device,
+    summarize_host,
+    validate,
+)
+from .model import (
+    U64_MAX,
+    DeviceActivityKind,
+    DeviceDecl,
+    DeviceRecord,
+    HostRecord,
+    HostState,
+    Interval,
+    InvalidTraceError,
+    Trace,
+    ValidationReport,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "AnalysisError", "DeviceMetrics", "DeviceSummary", "HostMetrics", "HostSummary", "MetricsReport",
+    "compute_report", "device_metrics", "host_metrics", "summarize_device", "summarize_host", "validate",
+    "U64_MAX", "DeviceActivityKind", "DeviceDecl", "DeviceRecord", "HostRecord", "HostState", "Interval",
+    "InvalidTraceError", "Trace", "ValidationReport",
+]

@@ -1,0 +1,136 @@
+"""ctypes binding of the C ABI in ``include/heteff_b200.h``.
+
+The shared library ``libheteff_b200.so`` is built in-tree by
+``__graft_entry__.build()`` (nvcc, ``-gencode arch=compute_100a,code=sm_100a``).
+There is no fallback: if the library is missing or no CUDA device is
+visible, every engine call raises -- the product path never computes on the
+CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libheteff_b200.so"
+
+# status codes (heteff_status)
+OK, INVALID_TRACE, ANALYSIS_ERROR, VALUE_ERROR, CONTRACT, CUDA_ERROR, NOMEM, BAD_ARG = range(8)
+# modes (heteff_mode)
+MODE_REPORT, MODE_SUMMARIZE_DEVICE, MODE_VALIDATE, MODE_SUMMARIZE_HOST = range(4)
+# list classes
+HOST_MALFORMED, HOST_ZERO, HOST_UNDECLARED, HOST_OVERLAP = range(4)
+DEV_MALFORMED, DEV_ZERO, DEV_UNDECLARED, DEV_LATE = range(4, 8)
+NUM_LISTS = 8
+
+_p = C.c_void_p
+
+
+class Records(C.Structure):
+    _fields_ = [("start", _p), ("end", _p), ("res", _p), ("kind", _p), ("count", C.c_int64)]
+
+
+class TraceABI(C.Structure):
+    _fields_ = [
+        ("host", Records), ("dev", Records),
+        ("host_ids", C.c_int32), ("dev_ids", C.c_int32),
+        ("host_decl", _p), ("dev_decl", _p),
+        ("n", C.c_int32), ("m", C.c_int32),
+        ("host_elapsed_floor", C.c_uint64),
+    ]
+
+
+class Options(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("reserved", C.c_int32), ("elapsed", C.c_uint64),
+                ("list_capacity", C.c_int64)]
+
+
+class Result(C.Structure):
+    _fields_ = [
+        ("status", C.c_int32), ("contract_flags", C.c_int32), ("contract_index", C.c_int64),
+        ("host_elapsed", C.c_uint64), ("elapsed", C.c_uint64), ("dev_max_end", C.c_uint64),
+        ("host_present", C.c_int32), ("device_present", C.c_int32),
+        ("host_metrics", C.c_double * 5), ("host_mask", C.c_uint32), ("device_mask", C.c_uint32),
+        ("device_metrics", C.c_double * 4), ("counts", C.c_int64 * NUM_LISTS), ("kernel_ms", C.c_double),
+    ]
+
+
+class Outputs(C.Structure):
+    _fields_ = [("host_summaries", _p), ("device_summaries", _p), ("lists", _p * NUM_LISTS)]
+
+
+class GenSide(C.Structure):
+    _fields_ = [
+        ("seed", C.c_uint64), ("n_res", C.c_int32), ("res_base", C.c_int32),
+        ("per_res", C.c_int64), ("extra_below", C.c_int32), ("serialized", C.c_int32),
+        ("count", C.c_int64), ("gap_max", C.c_uint32), ("dur_max", C.c_uint32),
+        ("dur_scale0", C.c_uint32), ("kernel_pct", C.c_uint32), ("is_host", C.c_int32),
+        ("reserved", C.c_int32),
+    ]
+
+
+#: every symbol include/heteff_b200.h declares
+EXPORTED = (
+    "heteff_abi_version", "heteff_create", "heteff_destroy", "heteff_last_error",
+    "heteff_analyze", "heteff_analyze_host", "heteff_overlap_covers",
+    "heteff_host_metrics", "heteff_device_metrics", "heteff_generate",
+)
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load the engine library (no GPU needed to load; compute calls need one)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"native engine {LIB_PATH.name} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(str(LIB_PATH))
+    lib.heteff_abi_version.restype = C.c_int
+    lib.heteff_create.restype = _p
+    lib.heteff_create.argtypes = [C.c_int]
+    lib.heteff_destroy.argtypes = [_p]
+    lib.heteff_last_error.restype = C.c_char_p
+    lib.heteff_last_error.argtypes = [_p]
+    for name in ("heteff_analyze", "heteff_analyze_host"):
+        f = getattr(lib, name)
+        f.restype = C.c_int
+        f.argtypes = [_p, C.POINTER(TraceABI), C.POINTER(Options), C.POINTER(Result), C.POINTER(Outputs), _p]
+    lib.heteff_overlap_covers.restype = C.c_int
+    lib.heteff_overlap_covers.argtypes = [_p, C.POINTER(TraceABI), C.c_int, _p, C.c_int64, _p, _p]
+    for name in ("heteff_host_metrics", "heteff_device_metrics"):
+        f = getattr(lib, name)
+        f.restype = C.c_int
+        f.argtypes = [_p, _p, C.c_int32, C.c_uint64, _p, C.POINTER(C.c_uint32), _p]
+    lib.heteff_generate.restype = C.c_int
+    lib.heteff_generate.argtypes = [_p, C.POINTER(GenSide), _p, _p, _p, _p, _p]
+    _lib = lib
+    return lib
+
+
+class NativeError(RuntimeError):
+    """The engine reported a CUDA / argument failure (not a trace property)."""
+
+
+_ctx: dict[int, int] = {}
+
+
+def context(device: int | None = None) -> int:
+    """Per-process engine context for ``device`` (default: $HETEFF_DEVICE or 0)."""
+    if device is None:
+        device = int(os.environ.get("HETEFF_DEVICE", "0"))
+    if device not in _ctx:
+        lib = load()
+        h = lib.heteff_create(device)
+        if not h:
+            raise NativeError(f"heteff_create({device}) failed: no usable CUDA device")
+        _ctx[device] = h
+    return _ctx[device]
+
+
+def last_error(ctx: int) -> str:
+    msg = load().heteff_last_error(ctx)
+    return msg.decode() if msg else ""

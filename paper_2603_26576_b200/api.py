@@ -1,0 +1,194 @@
+"""The drop-in hot-path API: same names, arguments, results and exceptions as
+the reference's ``heteff`` stage functions, computed by the B200 engine.
+
+=====================  ==========================================
+this module            reference
+=====================  ==========================================
+``validate``           ``model.py:160-230``
+``summarize_host``     ``summarize.py:57-92``
+``summarize_device``   ``summarize.py:95-138``
+``host_metrics``       ``metrics.py:66-93``
+``device_metrics``     ``metrics.py:96-122``
+``compute_report``     ``metrics.py:125-154``
+=====================  ==========================================
+
+Every function packs the trace (host-side ingest, :mod:`.packing`) and runs
+the fused analysis kernel; there is no CPU compute path.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .engine import Findings, analyze_packed, metrics_from_summaries
+from .messages import clamp_warnings, declaration_messages, validation_report
+from .model import U64_MAX, InvalidTraceError, Trace, ValidationReport
+from .packing import PackedTrace, pack_trace
+
+
+class AnalysisError(Exception):
+    """The trace is structurally fine but cannot be analyzed (e.g. zero elapsed)."""
+
+
+@dataclass(frozen=True)
+class HostSummary:
+    """Per-rank state totals, gaps and lead-in counted as useful."""
+
+    rank: int
+    d_useful: int
+    d_offload: int
+    d_mpi: int
+    span_end: int
+
+
+@dataclass(frozen=True)
+class DeviceSummary:
+    """Per-device activity totals; kernel + memory + idle == elapsed."""
+
+    device_id: int
+    d_kernel: int
+    d_memory: int
+    d_idle: int
+
+
+@dataclass(frozen=True)
+class HostMetrics:
+    parallel_efficiency: float
+    mpi_parallel_efficiency: float | None
+    mpi_communication_efficiency: float | None
+    mpi_load_balance: float | None
+    device_offload_efficiency: float | None
+
+
+@dataclass(frozen=True)
+class DeviceMetrics:
+    parallel_efficiency: float
+    load_balance: float | None
+    communication_efficiency: float | None
+    orchestration_efficiency: float | None
+
+
+@dataclass(frozen=True)
+class MetricsReport:
+    elapsed_ns: int
+    n: int
+    m: int
+    host: HostMetrics | None
+    device: DeviceMetrics | None
+    host_summaries: tuple[HostSummary, ...]
+    device_summaries: tuple[DeviceSummary, ...]
+    warnings: tuple[str, ...]
+
+
+def _run(trace: Trace, mode: int, elapsed: int = 0, want_lists: bool = True):
+    packed = pack_trace(trace)
+    f = analyze_packed(packed, mode, elapsed, want_lists=want_lists)
+    if f.status == N.CONTRACT:  # packing always produces canonical order
+        raise N.NativeError(f"packed trace violates the canonical-order contract at record {f.contract_index}")
+    return packed, f
+
+
+def _invalid(trace: Trace, f: Findings) -> bool:
+    decl_errors, _ = declaration_messages(trace)
+    return bool(decl_errors) or f.status == N.INVALID_TRACE
+
+
+def _raise_invalid(trace: Trace, packed: PackedTrace, f: Findings, report: ValidationReport | None = None):
+    if report is None:
+        report = validation_report(trace, packed, f)
+    raise InvalidTraceError(report)
+
+
+def _host_summaries(trace: Trace, f: Findings) -> list[HostSummary]:
+    out = []
+    for pos, rank in enumerate(trace.host_processes):
+        u, w, p, s = (int(x) for x in f.host_sum[pos])
+        out.append(HostSummary(rank, u, w, p, s))
+    return out
+
+
+def _device_summaries(trace: Trace, f: Findings, elapsed: int) -> list[DeviceSummary]:
+    out = []
+    for pos, d in enumerate(trace.devices):
+        k, mem, idle, _ = (int(x) for x in f.dev_sum[pos])
+        if elapsed > U64_MAX:   # window beyond the u64 domain: idle is the exact remainder
+            idle = elapsed - k - mem
+        out.append(DeviceSummary(d.device_id, k, mem, idle))
+    return out
+
+
+def validate(trace: Trace) -> ValidationReport:
+    """Every trace invariant, as data (never raises); ``model.py:160-230``."""
+    packed, f = _run(trace, N.MODE_VALIDATE)
+    return validation_report(trace, packed, f)
+
+
+def summarize_host(trace: Trace) -> tuple[list[HostSummary], int]:
+    """Per-rank totals and the elapsed time E; ``summarize.py:57-92``."""
+    packed, f = _run(trace, N.MODE_SUMMARIZE_HOST, want_lists=False)
+    if _invalid(trace, f):
+        _, f = _run(trace, N.MODE_VALIDATE)
+        _raise_invalid(trace, packed, f)
+    return _host_summaries(trace, f), f.elapsed
+
+
+def summarize_device(trace: Trace, elapsed: int) -> tuple[list[DeviceSummary], list[str]]:
+    """Per-device kernel / memory / idle inside ``[0, elapsed)``; ``summarize.py:95-138``."""
+    if elapsed <= 0:
+        raise ValueError(f"elapsed must be positive, got {elapsed}")
+    packed, f = _run(trace, N.MODE_SUMMARIZE_DEVICE, min(elapsed, U64_MAX), want_lists=False)
+    if _invalid(trace, f):
+        _, f = _run(trace, N.MODE_VALIDATE)
+        _raise_invalid(trace, packed, f)
+    return _device_summaries(trace, f, elapsed), clamp_warnings(trace, f, elapsed)
+
+
+def _u64_rows(rows) -> np.ndarray:
+    try:
+        return np.array(rows, dtype=np.uint64).reshape(-1, 4)
+    except OverflowError as e:
+        raise OverflowError("summary durations must fit in 64 bits") from e
+
+
+def host_metrics(summaries: list[HostSummary], elapsed: int) -> HostMetrics:
+    """Host tree from per-rank totals; ``metrics.py:66-93``."""
+    if len(summaries) < 1:
+        raise ValueError("host_metrics requires at least one rank")
+    if elapsed <= 0:
+        raise ValueError(f"elapsed must be positive, got {elapsed}")
+    rows = _u64_rows([(s.d_useful, s.d_offload, s.d_mpi, s.span_end) for s in summaries])
+    return HostMetrics(*metrics_from_summaries(rows, elapsed, host_side=True))
+
+
+def device_metrics(summaries: list[DeviceSummary], elapsed: int) -> DeviceMetrics:
+    """Device tree from per-device totals; ``metrics.py:96-122``."""
+    if len(summaries) < 1:
+        raise ValueError("device_metrics requires at least one device")
+    if elapsed <= 0:
+        raise ValueError(f"elapsed must be positive, got {elapsed}")
+    rows = _u64_rows([(s.d_kernel, s.d_memory, s.d_idle, 0) for s in summaries])
+    return DeviceMetrics(*metrics_from_summaries(rows, elapsed, host_side=False))
+
+
+def compute_report(trace: Trace) -> MetricsReport:
+    """Validate, summarize and evaluate both trees in ONE kernel launch; ``metrics.py:125-154``."""
+    packed, f = _run(trace, N.MODE_REPORT)
+    report = validation_report(trace, packed, f)
+    if not report.ok:
+        raise InvalidTraceError(report)
+    if f.status == N.ANALYSIS_ERROR:
+        raise AnalysisError("elapsed time is zero: trace records no activity")
+    E = f.elapsed
+    warnings = list(report.warnings)
+    if trace.m >= 1:
+        warnings += clamp_warnings(trace, f, E)
+    host = HostMetrics(*f.host_metrics) if trace.n >= 1 else None
+    device = DeviceMetrics(*f.device_metrics) if trace.m >= 1 else None
+    return MetricsReport(
+        elapsed_ns=E, n=trace.n, m=trace.m, host=host, device=device,
+        host_summaries=tuple(_host_summaries(trace, f)),
+        device_summaries=tuple(_device_summaries(trace, f, E)) if trace.m >= 1 else (),
+        warnings=tuple(warnings))

@@ -1,0 +1,394 @@
+// capi.cu -- the extern "C" boundary (include/heteff_b200.h): context,
+// self-cleaning device workspace, host staging, result copy-back.
+#include <cuda_runtime.h>
+#include <climits>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/heteff_b200.h"
+#include "engine.cuh"
+
+namespace hb {
+cudaError_t launch_generate(const heteff_gen_side &g, u64 *S, u64 *E, int32_t *R, uint8_t *K, cudaStream_t s);
+}
+
+using hb::u64;
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+};
+
+struct heteff_ctx {
+    int device = 0;
+    int grid = 0;
+    std::string err;
+    uint32_t epoch = 0;
+    // per dense id accumulators (zero between calls)
+    DevBuf host_acc, dev_acc;      // 3 / 4 arrays of u64
+    int64_t host_ids_cap = 0, dev_ids_cap = 0;
+    // look-back tile status
+    DevBuf host_tiles, dev_tiles;
+    int64_t host_tiles_cap = 0, dev_tiles_cap = 0;
+    // outputs
+    DevBuf host_out, dev_out, lists;
+    int64_t lists_cap = 0;
+    hb::Globals *g = nullptr;
+    hb::ResultDev *res_d = nullptr;
+    hb::ResultDev *res_h = nullptr;   // pinned
+    // staging for heteff_analyze_host / metrics
+    DevBuf stage;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+static int fail(heteff_ctx *ctx, int code, const std::string &msg)
+{
+    if (ctx) ctx->err = msg;
+    return code;
+}
+
+static int cuda_fail(heteff_ctx *ctx, cudaError_t e, const char *what)
+{
+    return fail(ctx, HETEFF_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call, what)                                   \
+    do {                                                 \
+        cudaError_t e_ = (call);                         \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, what); \
+    } while (0)
+
+// grow a zero-initialized device buffer (contents are not preserved)
+static cudaError_t ensure(DevBuf &b, size_t bytes, bool zero)
+{
+    if (bytes <= b.bytes && b.p) return cudaSuccess;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    size_t want = bytes < 256 ? 256 : bytes + bytes / 4;
+    cudaError_t e = cudaMalloc(&b.p, want);
+    if (e != cudaSuccess) return e;
+    b.bytes = want;
+    if (zero) e = cudaMemset(b.p, 0, want);
+    return e;
+}
+
+static cudaError_t reset_globals(heteff_ctx *ctx)
+{
+    hb::Globals g0;
+    memset(&g0, 0, sizeof(g0));
+    g0.contract_index = LLONG_MAX;
+    return cudaMemcpy(ctx->g, &g0, sizeof(g0), cudaMemcpyHostToDevice);
+}
+
+extern "C" {
+
+int heteff_abi_version(void) { return HETEFF_ABI_VERSION; }
+
+heteff_ctx *heteff_create(int device)
+{
+    heteff_ctx *ctx = new heteff_ctx();
+    ctx->device = device;
+    if (cudaSetDevice(device) != cudaSuccess) { delete ctx; return nullptr; }
+    if (cudaMalloc(&ctx->g, sizeof(hb::Globals)) != cudaSuccess) { delete ctx; return nullptr; }
+    if (cudaMalloc(&ctx->res_d, sizeof(hb::ResultDev)) != cudaSuccess) { delete ctx; return nullptr; }
+    if (cudaMallocHost(&ctx->res_h, sizeof(hb::ResultDev)) != cudaSuccess) { delete ctx; return nullptr; }
+    if (reset_globals(ctx) != cudaSuccess) { delete ctx; return nullptr; }
+    cudaEventCreate(&ctx->ev0);
+    cudaEventCreate(&ctx->ev1);
+    ctx->grid = hb::analyze_grid(device);
+    return ctx;
+}
+
+void heteff_destroy(heteff_ctx *ctx)
+{
+    if (!ctx) return;
+    DevBuf *bufs[] = {&ctx->host_acc, &ctx->dev_acc, &ctx->host_tiles, &ctx->dev_tiles,
+                      &ctx->host_out, &ctx->dev_out, &ctx->lists, &ctx->stage};
+    for (DevBuf *b : bufs)
+        if (b->p) cudaFree(b->p);
+    if (ctx->g) cudaFree(ctx->g);
+    if (ctx->res_d) cudaFree(ctx->res_d);
+    if (ctx->res_h) cudaFreeHost(ctx->res_h);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    delete ctx;
+}
+
+const char *heteff_last_error(const heteff_ctx *ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+static int run_analysis(heteff_ctx *ctx, const heteff_trace *t, const heteff_options *opt, heteff_result *result,
+                        const heteff_outputs *out, cudaStream_t s)
+{
+    if (!ctx || !t || !opt || !result) return fail(ctx, HETEFF_BAD_ARG, "null argument");
+    if (t->host.count < 0 || t->dev.count < 0 || t->host_ids < 0 || t->dev_ids < 0 || t->n < 0 || t->m < 0 ||
+        opt->list_capacity < 0)
+        return fail(ctx, HETEFF_BAD_ARG, "negative size");
+    if (opt->mode < 0 || opt->mode > 3) return fail(ctx, HETEFF_BAD_ARG, "bad mode");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const int64_t ht = (t->host.count + hb::kTile - 1) / hb::kTile;
+    const int64_t dt = (t->dev.count + hb::kTile - 1) / hb::kTile;
+    const int64_t hid = t->host_ids > 0 ? t->host_ids : 1, did = t->dev_ids > 0 ? t->dev_ids : 1;
+
+    // workspace (grow on demand; accumulators and tile flags start zeroed)
+    bool flags_new = false;
+    if (hid > ctx->host_ids_cap) {
+        CK(ensure(ctx->host_acc, (size_t)hid * 3 * sizeof(u64), true), "alloc host accumulators");
+        ctx->host_ids_cap = (int64_t)(ctx->host_acc.bytes / (3 * sizeof(u64)));
+    }
+    if (did > ctx->dev_ids_cap) {
+        CK(ensure(ctx->dev_acc, (size_t)did * 4 * sizeof(u64), true), "alloc device accumulators");
+        ctx->dev_ids_cap = (int64_t)(ctx->dev_acc.bytes / (4 * sizeof(u64)));
+    }
+    if (ht + 1 > ctx->host_tiles_cap) {
+        CK(ensure(ctx->host_tiles, (size_t)(ht + 1) * (4 + 16), true), "alloc host tile status");
+        ctx->host_tiles_cap = (int64_t)(ctx->host_tiles.bytes / (4 + 16));
+        flags_new = true;
+    }
+    if (dt + 1 > ctx->dev_tiles_cap) {
+        CK(ensure(ctx->dev_tiles, (size_t)(dt + 1) * (4 + 32), true), "alloc device tile status");
+        ctx->dev_tiles_cap = (int64_t)(ctx->dev_tiles.bytes / (4 + 32));
+        flags_new = true;
+    }
+    (void)flags_new;
+    CK(ensure(ctx->host_out, (size_t)(t->n > 0 ? t->n : 1) * 4 * sizeof(u64), false), "alloc host summaries");
+    CK(ensure(ctx->dev_out, (size_t)(t->m > 0 ? t->m : 1) * 4 * sizeof(u64), false), "alloc device summaries");
+    if (opt->list_capacity > ctx->lists_cap) {
+        CK(ensure(ctx->lists, (size_t)opt->list_capacity * 8 * sizeof(int64_t), false), "alloc lists");
+        ctx->lists_cap = opt->list_capacity;
+    }
+    if (++ctx->epoch >= (1u << 30)) {   // epoch wrap: clear tile status once
+        CK(cudaMemset(ctx->host_tiles.p, 0, ctx->host_tiles.bytes), "memset");
+        CK(cudaMemset(ctx->dev_tiles.p, 0, ctx->dev_tiles.bytes), "memset");
+        ctx->epoch = 1;
+    }
+
+    hb::Params p;
+    memset(&p, 0, sizeof(p));
+    p.hs = (const u64 *)t->host.start; p.he = (const u64 *)t->host.end; p.hr = t->host.res; p.hk = t->host.kind; p.hn = t->host.count;
+    p.ds = (const u64 *)t->dev.start; p.de = (const u64 *)t->dev.end; p.dr = t->dev.res; p.dk = t->dev.kind; p.dn = t->dev.count;
+    p.host_ids = t->host_ids; p.dev_ids = t->dev_ids;
+    p.host_decl = t->host_decl; p.dev_decl = t->dev_decl;
+    p.n = t->n; p.m = t->m;
+    p.host_elapsed_floor = t->host_elapsed_floor;
+    p.mode = opt->mode;
+    p.elapsed_arg = opt->elapsed;
+    p.cap = opt->list_capacity;
+    p.host_tiles = ht; p.dev_tiles = dt;
+    p.epoch = ctx->epoch;
+    const void *cols[8] = {p.hs, p.he, p.hr, p.hk, p.ds, p.de, p.dr, p.dk};
+    bool al = true;
+    for (const void *c : cols) al = al && aligned16(c);
+    p.use_tma = al ? 1 : 0;
+    u64 *ha = static_cast<u64 *>(ctx->host_acc.p);
+    const size_t hc = (size_t)ctx->host_ids_cap;
+    p.h_off = ha; p.h_mpi = ha + hc; p.h_span = ha + 2 * hc;
+    u64 *da = static_cast<u64 *>(ctx->dev_acc.p);
+    const size_t dc = (size_t)ctx->dev_ids_cap;
+    p.d_k = da; p.d_km = da + dc; p.d_clamp = da + 2 * dc; p.d_maxend = da + 3 * dc;
+    {
+        const size_t cap = (size_t)ctx->host_tiles_cap;
+        uint8_t *b = static_cast<uint8_t *>(ctx->host_tiles.p);
+        p.h_valA = reinterpret_cast<u64 *>(b);
+        p.h_valP = reinterpret_cast<u64 *>(b + cap * 8);
+        p.h_flag = reinterpret_cast<uint32_t *>(b + cap * 16);
+    }
+    {
+        const size_t cap = (size_t)ctx->dev_tiles_cap;
+        uint8_t *b = static_cast<uint8_t *>(ctx->dev_tiles.p);
+        p.d_valA0 = reinterpret_cast<u64 *>(b);
+        p.d_valA1 = reinterpret_cast<u64 *>(b + cap * 8);
+        p.d_valP0 = reinterpret_cast<u64 *>(b + cap * 16);
+        p.d_valP1 = reinterpret_cast<u64 *>(b + cap * 24);
+        p.d_flag = reinterpret_cast<uint32_t *>(b + cap * 32);
+    }
+    p.g = ctx->g;
+    int64_t *lb = static_cast<int64_t *>(ctx->lists.p);
+    for (int i = 0; i < 8; ++i) p.lists[i] = lb ? lb + (size_t)i * (size_t)ctx->lists_cap : nullptr;
+    p.host_out = static_cast<u64 *>(ctx->host_out.p);
+    p.dev_out = static_cast<u64 *>(ctx->dev_out.p);
+    p.res = ctx->res_d;
+
+    CK(cudaEventRecord(ctx->ev0, s), "event");
+    CK(hb::launch_analyze(p, ctx->grid, s), "launch analyze");
+    CK(cudaEventRecord(ctx->ev1, s), "event");
+    CK(cudaMemcpyAsync(ctx->res_h, ctx->res_d, sizeof(hb::ResultDev), cudaMemcpyDeviceToHost, s), "d2h result");
+    if (out && out->host_summaries && t->n > 0)
+        CK(cudaMemcpyAsync(out->host_summaries, ctx->host_out.p, (size_t)t->n * 4 * sizeof(u64),
+                           cudaMemcpyDeviceToHost, s), "d2h host summaries");
+    if (out && out->device_summaries && t->m > 0)
+        CK(cudaMemcpyAsync(out->device_summaries, ctx->dev_out.p, (size_t)t->m * 4 * sizeof(u64),
+                           cudaMemcpyDeviceToHost, s), "d2h device summaries");
+    CK(cudaStreamSynchronize(s), "analysis");
+    const hb::ResultDev &r = *ctx->res_h;
+    if (out && opt->list_capacity > 0) {
+        for (int i = 0; i < 8; ++i) {
+            int64_t k = r.counts[i] < opt->list_capacity ? r.counts[i] : opt->list_capacity;
+            if (k > 0 && out->lists[i])
+                CK(cudaMemcpyAsync(out->lists[i], p.lists[i], (size_t)k * sizeof(int64_t), cudaMemcpyDeviceToHost, s),
+                   "d2h lists");
+        }
+        CK(cudaStreamSynchronize(s), "lists");
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    result->status = r.status;
+    result->contract_flags = r.contract_flags;
+    result->contract_index = r.contract_index;
+    result->host_elapsed = r.host_elapsed;
+    result->elapsed = r.elapsed;
+    result->dev_max_end = r.dev_max_end;
+    result->host_present = r.host_present;
+    result->device_present = r.device_present;
+    for (int i = 0; i < 5; ++i) result->host_metrics[i] = r.host_metrics[i];
+    for (int i = 0; i < 4; ++i) result->device_metrics[i] = r.device_metrics[i];
+    result->host_mask = r.host_mask;
+    result->device_mask = r.device_mask;
+    for (int i = 0; i < 8; ++i) result->counts[i] = r.counts[i];
+    result->kernel_ms = ms;
+    ctx->err.clear();
+    return r.status;
+}
+
+int heteff_analyze(heteff_ctx *ctx, const heteff_trace *trace, const heteff_options *opt, heteff_result *result,
+                   const heteff_outputs *out, void *stream)
+{
+    return run_analysis(ctx, trace, opt, result, out, static_cast<cudaStream_t>(stream));
+}
+
+// stage host columns into the context's device buffer, then analyze
+int heteff_analyze_host(heteff_ctx *ctx, const heteff_trace *trace, const heteff_options *opt, heteff_result *result,
+                        const heteff_outputs *out, void *stream)
+{
+    if (!ctx || !trace) return fail(ctx, HETEFF_BAD_ARG, "null argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const int64_t hn = trace->host.count, dn = trace->dev.count;
+    auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t hb8 = up((size_t)hn * 8), hb4 = up((size_t)hn * 4), hb1 = up((size_t)hn);
+    const size_t db8 = up((size_t)dn * 8), db4 = up((size_t)dn * 4), db1 = up((size_t)dn);
+    const size_t hd = up((size_t)(trace->host_decl ? trace->host_ids : 0) * 4);
+    const size_t dd = up((size_t)(trace->dev_decl ? trace->dev_ids : 0) * 4);
+    const size_t total = 2 * hb8 + hb4 + hb1 + 2 * db8 + db4 + db1 + hd + dd;
+    CK(ensure(ctx->stage, total, false), "alloc staging");
+    uint8_t *b = static_cast<uint8_t *>(ctx->stage.p);
+    heteff_trace d = *trace;
+    size_t o = 0;
+    auto put = [&](const void *src, size_t bytes, size_t room) -> void * {
+        void *dst = b + o;
+        o += room;
+        if (bytes && src) cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+        return dst;
+    };
+    d.host.start = static_cast<const uint64_t *>(put(trace->host.start, (size_t)hn * 8, hb8));
+    d.host.end = static_cast<const uint64_t *>(put(trace->host.end, (size_t)hn * 8, hb8));
+    d.host.res = static_cast<const int32_t *>(put(trace->host.res, (size_t)hn * 4, hb4));
+    d.host.kind = static_cast<const uint8_t *>(put(trace->host.kind, (size_t)hn, hb1));
+    d.dev.start = static_cast<const uint64_t *>(put(trace->dev.start, (size_t)dn * 8, db8));
+    d.dev.end = static_cast<const uint64_t *>(put(trace->dev.end, (size_t)dn * 8, db8));
+    d.dev.res = static_cast<const int32_t *>(put(trace->dev.res, (size_t)dn * 4, db4));
+    d.dev.kind = static_cast<const uint8_t *>(put(trace->dev.kind, (size_t)dn, db1));
+    d.host_decl = trace->host_decl
+                      ? static_cast<const int32_t *>(put(trace->host_decl, (size_t)trace->host_ids * 4, hd))
+                      : nullptr;
+    d.dev_decl = trace->dev_decl
+                     ? static_cast<const int32_t *>(put(trace->dev_decl, (size_t)trace->dev_ids * 4, dd))
+                     : nullptr;
+    CK(cudaGetLastError(), "h2d");
+    return run_analysis(ctx, &d, opt, result, out, s);
+}
+
+int heteff_overlap_covers(heteff_ctx *ctx, const heteff_trace *trace, int host_columns_on_host,
+                          const int64_t *error_idx, int64_t count, int64_t *cover_idx, void *stream)
+{
+    if (!ctx || !trace || count < 0) return fail(ctx, HETEFF_BAD_ARG, "bad argument");
+    if (count == 0) return HETEFF_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const int64_t hn = trace->host.count;
+    const size_t cols = host_columns_on_host ? (size_t)hn * 20 : 0;
+    CK(ensure(ctx->stage, cols + (size_t)count * 16 + 1024, false), "alloc staging");
+    uint8_t *b = static_cast<uint8_t *>(ctx->stage.p);
+    hb::Params p;
+    memset(&p, 0, sizeof(p));
+    p.hn = hn;
+    if (host_columns_on_host) {
+        CK(cudaMemcpyAsync(b, trace->host.start, (size_t)hn * 8, cudaMemcpyHostToDevice, s), "h2d");
+        CK(cudaMemcpyAsync(b + (size_t)hn * 8, trace->host.end, (size_t)hn * 8, cudaMemcpyHostToDevice, s), "h2d");
+        CK(cudaMemcpyAsync(b + (size_t)hn * 16, trace->host.res, (size_t)hn * 4, cudaMemcpyHostToDevice, s), "h2d");
+        p.hs = reinterpret_cast<const u64 *>(b);
+        p.he = reinterpret_cast<const u64 *>(b + (size_t)hn * 8);
+        p.hr = reinterpret_cast<const int32_t *>(b + (size_t)hn * 16);
+    } else {
+        p.hs = (const u64 *)trace->host.start; p.he = (const u64 *)trace->host.end; p.hr = trace->host.res;
+    }
+    size_t off = (cols + 255) & ~(size_t)255;
+    int64_t *err_d = reinterpret_cast<int64_t *>(b + off);
+    int64_t *cov_d = err_d + count;
+    CK(cudaMemcpyAsync(err_d, error_idx, (size_t)count * 8, cudaMemcpyHostToDevice, s), "h2d");
+    CK(hb::launch_covers(p, err_d, count, cov_d, s), "launch covers");
+    CK(cudaMemcpyAsync(cover_idx, cov_d, (size_t)count * 8, cudaMemcpyDeviceToHost, s), "d2h");
+    CK(cudaStreamSynchronize(s), "covers");
+    return HETEFF_OK;
+}
+
+static int metrics_common(heteff_ctx *ctx, const uint64_t *summaries, int32_t k, uint64_t elapsed, int host_side,
+                          double *metrics, uint32_t *mask, void *stream)
+{
+    if (!ctx || !metrics || !mask || (k > 0 && !summaries)) return fail(ctx, HETEFF_BAD_ARG, "null argument");
+    if (k < 1) return fail(ctx, HETEFF_VALUE_ERROR,
+                           host_side ? "host_metrics requires at least one rank"
+                                     : "device_metrics requires at least one device");
+    if (elapsed == 0) return fail(ctx, HETEFF_VALUE_ERROR, "elapsed must be positive, got 0");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    CK(ensure(ctx->stage, (size_t)k * 32, false), "alloc staging");
+    CK(cudaMemcpyAsync(ctx->stage.p, summaries, (size_t)k * 32, cudaMemcpyHostToDevice, s), "h2d");
+    CK(hb::launch_metrics(static_cast<const u64 *>(ctx->stage.p), k, elapsed, host_side, ctx->res_d, s),
+       "launch metrics");
+    CK(cudaMemcpyAsync(ctx->res_h, ctx->res_d, sizeof(hb::ResultDev), cudaMemcpyDeviceToHost, s), "d2h");
+    CK(cudaStreamSynchronize(s), "metrics");
+    if (host_side) {
+        for (int i = 0; i < 5; ++i) metrics[i] = ctx->res_h->host_metrics[i];
+        *mask = ctx->res_h->host_mask;
+    } else {
+        for (int i = 0; i < 4; ++i) metrics[i] = ctx->res_h->device_metrics[i];
+        *mask = ctx->res_h->device_mask;
+    }
+    return HETEFF_OK;
+}
+
+int heteff_host_metrics(heteff_ctx *ctx, const uint64_t *summaries, int32_t n, uint64_t elapsed, double metrics[5],
+                        uint32_t *mask, void *stream)
+{
+    return metrics_common(ctx, summaries, n, elapsed, 1, metrics, mask, stream);
+}
+
+int heteff_device_metrics(heteff_ctx *ctx, const uint64_t *summaries, int32_t m, uint64_t elapsed,
+                          double metrics[4], uint32_t *mask, void *stream)
+{
+    return metrics_common(ctx, summaries, m, elapsed, 0, metrics, mask, stream);
+}
+
+int heteff_generate(heteff_ctx *ctx, const heteff_gen_side *side, uint64_t *start, uint64_t *end, int32_t *res,
+                    uint8_t *kind, void *stream)
+{
+    if (!ctx || !side) return fail(ctx, HETEFF_BAD_ARG, "null argument");
+    if (side->n_res < 0 || side->per_res < 0 || side->dur_max < 1)
+        return fail(ctx, HETEFF_BAD_ARG, "bad generator parameters");
+    // the record count implied by per_res / extra_below must match
+    long long lo = side->res_base, hi = (long long)side->res_base + side->n_res, ex = side->extra_below;
+    long long extras = (hi < ex ? hi : ex) - (lo < ex ? lo : ex);
+    if (extras < 0) extras = 0;
+    if ((long long)side->per_res * side->n_res + extras != side->count)
+        return fail(ctx, HETEFF_BAD_ARG, "count does not match per_res/extra_below");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    CK(hb::launch_generate(*side, (u64 *)start, (u64 *)end, res, kind, static_cast<cudaStream_t>(stream)), "launch generate");
+    return HETEFF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,197 @@
+"""Calls into the B200 engine: packed trace in, :class:`Findings` out.
+
+Two entry shapes:
+
+* :func:`analyze_packed` -- a :class:`~.packing.PackedTrace` in host memory
+  (the drop-in API path); the C ABI stages the columns to HBM.
+* :func:`analyze_device` -- columns already resident in HBM (torch CUDA
+  tensors or raw device pointers); the bench / large-trace path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .packing import PackedTrace, RecordColumns
+
+
+@dataclass
+class Findings:
+    status: int
+    contract_flags: int
+    contract_index: int
+    host_elapsed: int
+    elapsed: int
+    dev_max_end: int
+    host_metrics: tuple          # 5 floats or None
+    device_metrics: tuple        # 4 floats or None
+    counts: tuple                # 8 ints (heteff list classes)
+    host_sum: np.ndarray         # uint64 [n][4] useful, offload, mpi, span_end (declaration order)
+    dev_sum: np.ndarray          # uint64 [m][4] kernel, memory, idle, clamped
+    lists: list = field(default_factory=list)   # 8 arrays of SoA positions (sorted), or empty
+    kernel_ms: float = 0.0
+
+
+def _ptr(a: np.ndarray | None) -> int | None:
+    return None if a is None or a.size == 0 else a.ctypes.data
+
+
+def _records(cols: RecordColumns) -> N.Records:
+    return N.Records(_ptr(cols.start), _ptr(cols.end), _ptr(cols.res), _ptr(cols.kind), cols.count)
+
+
+def _metrics(vals, mask, k):
+    return tuple(float(vals[i]) if (mask >> i) & 1 else None for i in range(k))
+
+
+def _findings(res: N.Result, host_sum, dev_sum, lists) -> Findings:
+    return Findings(
+        status=res.status, contract_flags=res.contract_flags, contract_index=res.contract_index,
+        host_elapsed=int(res.host_elapsed), elapsed=int(res.elapsed), dev_max_end=int(res.dev_max_end),
+        host_metrics=_metrics(res.host_metrics, res.host_mask, 5),
+        device_metrics=_metrics(res.device_metrics, res.device_mask, 4),
+        counts=tuple(int(c) for c in res.counts), host_sum=host_sum, dev_sum=dev_sum, lists=lists,
+        kernel_ms=float(res.kernel_ms))
+
+
+def _check(ctx, rc):
+    if rc in (N.CUDA_ERROR, N.NOMEM, N.BAD_ARG):
+        raise N.NativeError(f"engine error {rc}: {N.last_error(ctx)}")
+
+
+def analyze_packed(packed: PackedTrace, mode: int, elapsed: int = 0, want_lists: bool = True,
+                   capacity: int = 1 << 14, device: int | None = None) -> Findings:
+    """Run the engine on a host-resident packed trace (copies inside the call)."""
+    ctx = N.context(device)
+    lib = N.load()
+    t = N.TraceABI(_records(packed.host), _records(packed.dev),
+                   len(packed.host_ids), len(packed.dev_ids),
+                   _ptr(packed.host_decl), _ptr(packed.dev_decl),
+                   packed.n_unique, packed.m_unique, packed.host_elapsed_floor)
+    total = packed.host.count + packed.dev.count
+    cap = min(capacity, max(total, 1)) if want_lists else 0
+    while True:
+        host_sum = np.zeros((max(packed.n_unique, 1), 4), dtype=np.uint64)
+        dev_sum = np.zeros((max(packed.m_unique, 1), 4), dtype=np.uint64)
+        lists = [np.empty(cap, dtype=np.int64) for _ in range(N.NUM_LISTS)] if cap else []
+        out = N.Outputs(_ptr(host_sum), _ptr(dev_sum),
+                        (C.c_void_p * N.NUM_LISTS)(*[_ptr(x) for x in lists]) if cap
+                        else (C.c_void_p * N.NUM_LISTS)())
+        opt = N.Options(mode, 0, elapsed, cap)
+        res = N.Result()
+        rc = lib.heteff_analyze_host(ctx, C.byref(t), C.byref(opt), C.byref(res), C.byref(out), None)
+        _check(ctx, rc)
+        need = max(res.counts) if want_lists else 0
+        if need <= cap:
+            break
+        cap = int(need)
+    if cap:
+        lists = [np.sort(lists[i][: res.counts[i]]) for i in range(N.NUM_LISTS)]
+    return _findings(res, host_sum[: packed.n_unique], dev_sum[: packed.m_unique], lists)
+
+
+def overlap_covers(packed: PackedTrace, error_pos: np.ndarray, device: int | None = None) -> np.ndarray:
+    """Cover record (model.py:208-215) of each overlap error, by SoA position."""
+    ctx = N.context(device)
+    lib = N.load()
+    err = np.ascontiguousarray(error_pos, dtype=np.int64)
+    cover = np.empty_like(err)
+    t = N.TraceABI(_records(packed.host), _records(packed.dev), len(packed.host_ids), len(packed.dev_ids),
+                   None, None, packed.n_unique, packed.m_unique, 0)
+    rc = lib.heteff_overlap_covers(ctx, C.byref(t), 1, _ptr(err), err.size, _ptr(cover), None)
+    _check(ctx, rc)
+    return cover
+
+
+def metrics_from_summaries(rows: np.ndarray, elapsed: int, host_side: bool, device: int | None = None):
+    """host_metrics / device_metrics stage functions on the GPU."""
+    ctx = N.context(device)
+    lib = N.load()
+    rows = np.ascontiguousarray(rows, dtype=np.uint64)
+    k = 5 if host_side else 4
+    vals = (C.c_double * k)()
+    mask = C.c_uint32(0)
+    fn = lib.heteff_host_metrics if host_side else lib.heteff_device_metrics
+    rc = fn(ctx, _ptr(rows), rows.shape[0], elapsed, C.cast(vals, C.c_void_p), C.byref(mask), None)
+    if rc == N.VALUE_ERROR:
+        raise ValueError(N.last_error(ctx))
+    _check(ctx, rc)
+    return _metrics(vals, mask.value, k)
+
+
+# ---------------------------------------------------------------------------
+# device-resident columns (bench / columnar fast path)
+# ---------------------------------------------------------------------------
+@dataclass
+class DeviceTrace:
+    """Packed SoA resident in HBM: torch CUDA tensors (or anything with data_ptr)."""
+
+    h_start: object
+    h_end: object
+    h_res: object
+    h_kind: object
+    d_start: object
+    d_end: object
+    d_res: object
+    d_kind: object
+    n: int                 # declared ranks (dense ids 0..n-1)
+    m: int                 # declared devices
+    host_elapsed_floor: int = 0
+
+    @property
+    def host_count(self) -> int:
+        return int(self.h_start.numel())
+
+    @property
+    def dev_count(self) -> int:
+        return int(self.d_start.numel())
+
+
+def _dptr(t) -> int | None:
+    return t.data_ptr() if t is not None and t.numel() > 0 else None
+
+
+def device_trace_abi(dt: DeviceTrace) -> N.TraceABI:
+    return N.TraceABI(
+        N.Records(_dptr(dt.h_start), _dptr(dt.h_end), _dptr(dt.h_res), _dptr(dt.h_kind), dt.host_count),
+        N.Records(_dptr(dt.d_start), _dptr(dt.d_end), _dptr(dt.d_res), _dptr(dt.d_kind), dt.dev_count),
+        dt.n, dt.m, None, None, dt.n, dt.m, dt.host_elapsed_floor)
+
+
+def analyze_device(dt: DeviceTrace, mode: int = N.MODE_REPORT, elapsed: int = 0, stream: int | None = None,
+                   device: int | None = None, host_sum: np.ndarray | None = None,
+                   dev_sum: np.ndarray | None = None) -> Findings:
+    """Analyze HBM-resident columns (counts only, no per-record lists)."""
+    ctx = N.context(device)
+    lib = N.load()
+    t = device_trace_abi(dt)
+    if host_sum is None:
+        host_sum = np.zeros((max(dt.n, 1), 4), dtype=np.uint64)
+    if dev_sum is None:
+        dev_sum = np.zeros((max(dt.m, 1), 4), dtype=np.uint64)
+    out = N.Outputs(_ptr(host_sum), _ptr(dev_sum), (C.c_void_p * N.NUM_LISTS)())
+    opt = N.Options(mode, 0, elapsed, 0)
+    res = N.Result()
+    rc = lib.heteff_analyze(ctx, C.byref(t), C.byref(opt), C.byref(res), C.byref(out), stream)
+    _check(ctx, rc)
+    return _findings(res, host_sum[: dt.n], dev_sum[: dt.m], [])
+
+
+def analyze_host_columns(dt: DeviceTrace, mode: int = N.MODE_REPORT, stream: int | None = None,
+                         device: int | None = None) -> Findings:
+    """Same as :func:`analyze_device` but the columns are HOST tensors (pinned); H2D inside."""
+    ctx = N.context(device)
+    lib = N.load()
+    t = device_trace_abi(dt)
+    host_sum = np.zeros((max(dt.n, 1), 4), dtype=np.uint64)
+    dev_sum = np.zeros((max(dt.m, 1), 4), dtype=np.uint64)
+    out = N.Outputs(_ptr(host_sum), _ptr(dev_sum), (C.c_void_p * N.NUM_LISTS)())
+    opt = N.Options(mode, 0, 0, 0)
+    res = N.Result()
+    rc = lib.heteff_analyze_host(ctx, C.byref(t), C.byref(opt), C.byref(res), C.byref(out), stream)
+    _check(ctx, rc)
+    return _findings(res, host_sum[: dt.n], dev_sum[: dt.m], [])

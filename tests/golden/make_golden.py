@@ -1,0 +1,307 @@
+"""Generate the golden fixtures by running the REFERENCE package.
+
+Run in the build container (the only place /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports ``heteff`` from /root/reference/pkg/src (read-only) and the
+reference's own corpus generator ``random_valid_trace``
+(pkg/tests/strategies.py:39-78), runs the reference's hot path on
+
+  * every preset at scales 1, 7, 1000 (pkg/tests/test_scenario.py:226-248,
+    test_acceptance.py:270-280),
+  * the acceptance corpora, seeds 0x5EED01 / 0x5EED05 / 0x5EED06
+    (test_acceptance.py:69-267), the last one with its stream reassignment,
+  * a corpus of deliberately INVALID traces (overlaps, malformed, zero-length,
+    undeclared, duplicate declarations, late device records, out-of-domain
+    timestamps) for exact validation-message parity (model.py:160-230),
+  * summarize_device with explicit elapsed windows (summarize.py:95-138),
+  * host_metrics / device_metrics on random and extreme summaries
+    (metrics.py:66-122, exact int/int division),
+  * config-shaped traces from oracle/gen.py: C1 in full and rank shards of
+    C2, C3, C5,
+
+and writes the inputs plus the reference's outputs (floats as float.hex) to
+tests/golden/*.json.gz.  Nothing on the GPU box reads /root/reference.
+"""
+
+from __future__ import annotations
+
+import gzip
+import json
+import random
+import sys
+from pathlib import Path
+
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parent.parent
+REF = Path("/root/reference/pkg")
+sys.path.insert(0, str(REF / "src"))
+sys.path.insert(0, str(REF / "tests"))
+sys.path.insert(0, str(ROOT))
+
+import heteff  # noqa: E402  (the reference)
+from heteff import (  # noqa: E402
+    AnalysisError, DeviceActivityKind, DeviceDecl, DeviceRecord, DeviceSummary, HostRecord, HostState,
+    HostSummary, Interval, InvalidTraceError, Trace, compute_report, device_metrics, host_metrics,
+    summarize_device, validate,
+)
+from strategies import random_valid_trace  # noqa: E402  (reference corpus generator)
+
+from oracle import gen as ogen  # noqa: E402
+from paper_2603_26576_b200.configs import CONFIGS  # noqa: E402
+
+KINDS = {"kernel": DeviceActivityKind.KERNEL, "memory": DeviceActivityKind.MEMORY}
+STATES = {"useful": HostState.USEFUL, "offload": HostState.OFFLOAD, "mpi": HostState.MPI}
+
+
+def fx(v):
+    return None if v is None else float(v).hex()
+
+
+def enc_trace(t: Trace) -> dict:
+    return {
+        "hp": list(t.host_processes),
+        "dev": [[d.device_id, d.owner_rank] for d in t.devices],
+        "h": [[r.rank, r.state.value, r.interval.start, r.interval.end] for r in t.host_records],
+        "d": [[r.device_id, r.kind.value, r.interval.start, r.interval.end, r.stream] for r in t.device_records],
+        "tu": t.time_unit,
+    }
+
+
+def dec_trace(x: dict) -> Trace:
+    return Trace(
+        host_processes=tuple(x["hp"]),
+        devices=tuple(DeviceDecl(i, o) for i, o in x["dev"]),
+        host_records=tuple(HostRecord(r, STATES[s], Interval(a, b)) for r, s, a, b in x["h"]),
+        device_records=tuple(DeviceRecord(d, KINDS[k], Interval(a, b), st) for d, k, a, b, st in x["d"]),
+        time_unit=x["tu"],
+    )
+
+
+def enc_report(t: Trace) -> dict:
+    try:
+        r = compute_report(t)
+    except InvalidTraceError as e:
+        return {"raise": "InvalidTraceError", "msg": str(e)}
+    except AnalysisError as e:
+        return {"raise": "AnalysisError", "msg": str(e)}
+    host = None if r.host is None else [fx(getattr(r.host, f)) for f in (
+        "parallel_efficiency", "mpi_parallel_efficiency", "mpi_communication_efficiency", "mpi_load_balance",
+        "device_offload_efficiency")]
+    dev = None if r.device is None else [fx(getattr(r.device, f)) for f in (
+        "parallel_efficiency", "load_balance", "communication_efficiency", "orchestration_efficiency")]
+    return {
+        "E": r.elapsed_ns, "n": r.n, "m": r.m, "host": host, "device": dev,
+        "hs": [[s.rank, s.d_useful, s.d_offload, s.d_mpi, s.span_end] for s in r.host_summaries],
+        "ds": [[s.device_id, s.d_kernel, s.d_memory, s.d_idle] for s in r.device_summaries],
+        "warnings": list(r.warnings),
+    }
+
+
+def enc_validate(t: Trace) -> dict:
+    v = validate(t)
+    return {"errors": v.errors, "warnings": v.warnings}
+
+
+def case(t: Trace, tag: str) -> dict:
+    return {"tag": tag, "trace": enc_trace(t), "report": enc_report(t), "validate": enc_validate(t)}
+
+
+def write(name: str, obj) -> None:
+    path = HERE / f"{name}.json.gz"
+    with gzip.open(path, "wt", encoding="utf-8") as f:
+        json.dump(obj, f, separators=(",", ":"))
+    print(f"wrote {path.relative_to(ROOT)} ({path.stat().st_size} bytes)")
+
+
+# ---------------------------------------------------------------------------
+def presets() -> list:
+    out = []
+    for name in heteff.PRESET_NAMES:
+        for k in (1, 7, 1000):
+            out.append(case(heteff.build(heteff.preset(name, k)), f"{name}@{k}"))
+    return out
+
+
+def acceptance_corpora() -> list:
+    out = []
+    rng = random.Random(0x5EED01)
+    for i in range(1000):
+        out.append(case(random_valid_trace(rng), f"5EED01/{i}"))
+    rng = random.Random(0x5EED05)
+    for i in range(200):
+        out.append(case(random_valid_trace(rng, require_devices=True), f"5EED05/{i}"))
+    rng = random.Random(0x5EED06)
+    for i in range(100):
+        t = random_valid_trace(rng, require_devices=True)
+        shuffled = Trace(
+            host_processes=t.host_processes, devices=t.devices, host_records=t.host_records,
+            device_records=tuple(DeviceRecord(r.device_id, r.kind, r.interval, rng.choice([None, 0, 3, 7]))
+                                 for r in t.device_records))
+        out.append(case(t, f"5EED06/{i}"))
+        out.append(case(shuffled, f"5EED06/{i}/shuffled"))
+    return out
+
+
+def invalid_corpus() -> list:
+    """Traces that exercise every validation message (model.py:160-230)."""
+    rng = random.Random(0xBAD5EED)
+    out = []
+    for i in range(400):
+        base = random_valid_trace(rng, max_ranks=4, max_devices=3, max_segments=8)
+        hp = list(base.host_processes)
+        devs = list(base.devices)
+        hrec = list(base.host_records)
+        drec = list(base.device_records)
+        span = max((r.interval.end for r in hrec), default=100)
+        for _ in range(rng.randint(1, 4)):
+            what = rng.randrange(12)
+            if what == 0 and hp:        # overlapping host record
+                r = rng.choice(hp)
+                a = rng.randint(0, span)
+                hrec.append(HostRecord(r, rng.choice(list(HostState)), Interval(a, a + rng.randint(1, 50))))
+            elif what == 1 and hp:      # malformed host
+                r = rng.choice(hp)
+                a = rng.randint(1, span + 1)
+                hrec.append(HostRecord(r, rng.choice(list(HostState)), Interval(a, a - rng.randint(1, a))))
+            elif what == 2 and hp:      # zero-length host
+                r = rng.choice(hp)
+                a = rng.randint(0, span + 20)
+                hrec.append(HostRecord(r, rng.choice(list(HostState)), Interval(a, a)))
+            elif what == 3:             # undeclared rank
+                a = rng.randint(0, span)
+                hrec.append(HostRecord(rng.choice([7, 9, -3]), HostState.MPI, Interval(a, a + 5)))
+            elif what == 4:             # undeclared device
+                a = rng.randint(0, span)
+                drec.append(DeviceRecord(rng.choice([5, 11]), DeviceActivityKind.KERNEL, Interval(a, a + 3)))
+            elif what == 5 and devs:    # malformed / zero-length device
+                dd = rng.choice(devs).device_id
+                a = rng.randint(1, span)
+                b = a - rng.randint(0, a)
+                drec.append(DeviceRecord(dd, rng.choice(list(DeviceActivityKind)), Interval(a, b)))
+            elif what == 6 and devs:    # late device record (clamped)
+                dd = rng.choice(devs).device_id
+                a = rng.randint(span - 10 if span > 10 else 0, span + 50)
+                drec.append(DeviceRecord(dd, rng.choice(list(DeviceActivityKind)), Interval(a, a + rng.randint(0, 80))))
+            elif what == 7 and hp:      # duplicate rank declaration
+                hp.append(rng.choice(hp))
+            elif what == 8 and devs:    # duplicate device declaration / unknown owner
+                d = rng.choice(devs)
+                devs.append(DeviceDecl(d.device_id, d.owner_rank) if rng.random() < 0.5
+                            else DeviceDecl(d.device_id + 50, 99))
+            elif what == 9 and hp:      # out-of-domain timestamps (quarantined by the packer)
+                r = rng.choice(hp)
+                kind = rng.randrange(4)
+                iv = [Interval(-5, 10), Interval(3, 2 ** 64 + 1), Interval(-5, -9), Interval(2 ** 64 + 5, 2 ** 64 + 1)][kind]
+                hrec.append(HostRecord(r, HostState.USEFUL, iv))
+            elif what == 10 and devs:   # out-of-domain device timestamps
+                dd = rng.choice(devs).device_id
+                drec.append(DeviceRecord(dd, DeviceActivityKind.MEMORY, Interval(-1, 4)))
+            elif what == 11 and hp:     # exact-duplicate and touching host records
+                r = rng.choice(hp)
+                recs = [x for x in hrec if x.rank == r]
+                if recs:
+                    x = rng.choice(recs)
+                    hrec.append(x)
+        t = Trace(host_processes=tuple(hp), devices=tuple(devs), host_records=tuple(hrec),
+                  device_records=tuple(drec))
+        out.append(case(t, f"invalid/{i}"))
+    # declaration-level specials
+    out.append(case(Trace(), "empty"))
+    out.append(case(Trace(host_processes=(0,), time_unit="us",
+                          host_records=(HostRecord(0, HostState.USEFUL, Interval(0, 1)),)), "time_unit"))
+    out.append(case(Trace(host_processes=(0,)), "zero_elapsed"))
+    out.append(case(Trace(devices=(DeviceDecl(0),)), "zero_elapsed_dev"))
+    return out
+
+
+def summarize_device_corpus() -> list:
+    rng = random.Random(0x5D5D)
+    out = []
+    for i in range(300):
+        t = random_valid_trace(rng, require_devices=True)
+        _, E = heteff.summarize_host(t)
+        for el in {max(1, E // 2), max(1, E), E + rng.randint(1, 100), rng.randint(1, 40)}:
+            s, w = summarize_device(t, el)
+            out.append({"tag": f"sd/{i}/{el}", "trace": enc_trace(t), "elapsed": el,
+                        "ds": [[x.device_id, x.d_kernel, x.d_memory, x.d_idle] for x in s], "warnings": w})
+    return out
+
+
+def metrics_corpus() -> list:
+    rng = random.Random(0x3E7)
+    out = []
+    for i in range(600):
+        k = rng.randint(1, 9)
+        big = i % 3 == 0
+        hi = (1 << 62) if big else 10 ** 6
+        hs = []
+        for r in range(k):
+            u = rng.randint(0, hi)
+            w = rng.randint(0, hi) if rng.random() < 0.8 else 0
+            p = rng.randint(0, hi) if rng.random() < 0.5 else 0
+            if rng.random() < 0.1:
+                u = w = 0
+            hs.append(HostSummary(r, u, w, p, u + w + p))
+        E = max(s.span_end for s in hs) or 1
+        if rng.random() < 0.3:
+            E += rng.randint(1, hi)
+        E = min(E, (1 << 64) - 1) if all(s.span_end < (1 << 64) for s in hs) else E
+        hm = host_metrics(hs, E)
+        ds = []
+        for d in range(rng.randint(1, 9)):
+            kk = rng.randint(0, hi) if rng.random() < 0.85 else 0
+            mm = rng.randint(0, hi) if rng.random() < 0.6 else 0
+            ds.append(DeviceSummary(d, kk, mm, 0))
+        Ed = max(s.d_kernel + s.d_memory for s in ds) + rng.randint(1, hi)
+        dm = device_metrics(ds, Ed)
+        out.append({
+            "hs": [[s.rank, s.d_useful, s.d_offload, s.d_mpi, s.span_end] for s in hs], "E": E,
+            "host": [fx(getattr(hm, f)) for f in ("parallel_efficiency", "mpi_parallel_efficiency",
+                                                   "mpi_communication_efficiency", "mpi_load_balance",
+                                                   "device_offload_efficiency")],
+            "ds": [[s.device_id, s.d_kernel, s.d_memory, s.d_idle] for s in ds], "Ed": Ed,
+            "device": [fx(getattr(dm, f)) for f in ("parallel_efficiency", "load_balance",
+                                                     "communication_efficiency", "orchestration_efficiency")],
+        })
+    return out
+
+
+def config_trace(cfg, r0, r1) -> Trace:
+    (hs, he, hr, hk), (ds, de, dr, dk) = ogen.generate(cfg, r0, r1)
+    g = cfg.gpus_per_rank
+    states = [HostState.USEFUL, HostState.OFFLOAD, HostState.MPI]
+    kinds = [DeviceActivityKind.KERNEL, DeviceActivityKind.MEMORY]
+    hrec = [HostRecord(int(r) + r0, states[k], Interval(int(a), int(b)))
+            for a, b, r, k in zip(hs.tolist(), he.tolist(), hr.tolist(), hk.tolist())]
+    drec = [DeviceRecord(int(r) + r0 * g, kinds[k], Interval(int(a), int(b)))
+            for a, b, r, k in zip(ds.tolist(), de.tolist(), dr.tolist(), dk.tolist())]
+    return Trace(host_processes=tuple(range(r0, r1)),
+                 devices=tuple(DeviceDecl(d, d // g) for d in range(r0 * g, r1 * g)),
+                 host_records=tuple(hrec), device_records=tuple(drec))
+
+
+def config_shards() -> list:
+    out = []
+    for name, r0, r1 in (("c1", 0, 4), ("c2", 0, 2), ("c2", 127, 129), ("c3", 0, 1), ("c5", 0, 2)):
+        cfg = CONFIGS[name]
+        t = config_trace(cfg, r0, r1)
+        rep = enc_report(t)
+        out.append({"config": name, "r0": r0, "r1": r1, "records": len(t.host_records) + len(t.device_records),
+                    "report": rep})
+        print(f"  {name}[{r0}:{r1}] {len(t.host_records) + len(t.device_records)} records, E={rep.get('E')}")
+    return out
+
+
+def main() -> None:
+    write("presets", presets())
+    write("acceptance", acceptance_corpora())
+    write("invalid", invalid_corpus())
+    write("summarize_device", summarize_device_corpus())
+    write("metrics", metrics_corpus())
+    write("config_shards", config_shards())
+
+
+if __name__ == "__main__":
+    main()

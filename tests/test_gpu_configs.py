@@ -1,0 +1,97 @@
+"""Config-shaped traces generated in HBM: generator bit-exactness vs the numpy
+twin, parity with the reference on rank shards, and full-scale parity with
+the C oracle (C2, 1e8 intervals) plus size-independent properties."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import gpu_available
+from golden_io import load, unhex
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+from paper_2603_26576_b200 import _native as N  # noqa: E402
+from paper_2603_26576_b200.configs import CONFIGS  # noqa: E402
+from paper_2603_26576_b200.engine import analyze_device  # noqa: E402
+from paper_2603_26576_b200.synth import generate  # noqa: E402
+
+
+def _host(t):
+    return t.cpu().numpy()
+
+
+def _u64(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c5"])
+def test_gpu_generator_matches_numpy_twin(name):
+    from oracle import gen as ogen
+    cfg = CONFIGS[name]
+    dt = generate(cfg, 0, 2 if name != "c1" else 4)
+    (hs, he, hr, hk), (ds, de, dr, dk) = ogen.generate(cfg, 0, 2 if name != "c1" else 4)
+    assert np.array_equal(_u64(dt.h_start), hs) and np.array_equal(_u64(dt.h_end), he)
+    assert np.array_equal(_host(dt.h_res), hr) and np.array_equal(_host(dt.h_kind), hk)
+    assert np.array_equal(_u64(dt.d_start), ds) and np.array_equal(_u64(dt.d_end), de)
+    assert np.array_equal(_host(dt.d_res), dr) and np.array_equal(_host(dt.d_kind), dk)
+
+
+SHARDS = load("config_shards")
+
+
+@pytest.mark.parametrize("shard", SHARDS, ids=[f"{s['config']}[{s['r0']}:{s['r1']}]" for s in SHARDS])
+def test_config_shard_matches_reference(shard):
+    cfg = CONFIGS[shard["config"]]
+    dt = generate(cfg, shard["r0"], shard["r1"])
+    f = analyze_device(dt)
+    rep = shard["report"]
+    assert f.status == N.OK
+    assert f.elapsed == rep["E"]
+    assert [list(map(int, r)) for r in f.host_sum] == [x[1:] for x in rep["hs"]]
+    assert [list(map(int, r[:3])) for r in f.dev_sum] == [x[1:] for x in rep["ds"]]
+    assert list(f.host_metrics) == [unhex(v) for v in rep["host"]]
+    assert list(f.device_metrics) == [unhex(v) for v in rep["device"]]
+
+
+def test_c2_full_scale_matches_oracle():
+    """C2 in full (1e8 intervals): every summary bit-exact vs the C oracle."""
+    from oracle import oracle as O
+    cfg = CONFIGS["c2"]
+    dt = generate(cfg)
+    f = analyze_device(dt)
+    assert f.status == N.OK
+    h = (_u64(dt.h_start), _u64(dt.h_end), _host(dt.h_res), _host(dt.h_kind))
+    d = (_u64(dt.d_start), _u64(dt.d_end), _host(dt.d_res), _host(dt.d_kind))
+    ref = O.analyze(h, d, cfg.n_ranks, cfg.n_devices)
+    assert ref.status == 0
+    assert f.elapsed == ref.elapsed
+    assert np.array_equal(f.host_sum, ref.host_sum)
+    assert np.array_equal(f.dev_sum, ref.dev_sum)
+    assert f.host_metrics == ref.host_metrics and f.device_metrics == ref.device_metrics
+
+
+@pytest.mark.parametrize("name", ["c3", "c5"])
+def test_full_scale_properties(name):
+    """Size-independent properties at full config size (single GPU)."""
+    cfg = CONFIGS[name]
+    dt = generate(cfg)
+    f = analyze_device(dt)
+    assert f.status == N.OK
+    E = f.elapsed
+    hs = f.host_sum.astype(object)
+    ds = f.dev_sum.astype(object)
+    # host: useful + offload + mpi == span_end, E == max span_end
+    assert all(r[0] + r[1] + r[2] == r[3] for r in hs)
+    assert E == max(r[3] for r in hs)
+    # device partition identity (summarize.py docstring: kernel + memory + idle == elapsed)
+    assert all(r[0] + r[1] + r[2] == E for r in ds)
+    # a second run gives identical bits (integer sums are order independent)
+    g = analyze_device(dt)
+    assert np.array_equal(f.host_sum, g.host_sum) and np.array_equal(f.dev_sum, g.dev_sum)
+    # metric identities (metrics.py docstring)
+    pe, mpe, ce, lb, oe = f.host_metrics
+    assert abs(pe - mpe * oe) <= 1e-12 * pe and abs(mpe - ce * lb) <= 1e-12 * mpe
+    dpe, dlb, dce, doe = f.device_metrics
+    assert abs(dpe - dlb * dce * doe) <= 1e-12 * dpe
