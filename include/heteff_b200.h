@@ -180,6 +180,10 @@ typedef struct {
     int32_t reserved;
 } heteff_gen_side;
 
+/* developer instrumentation: per-CTA clock64 phase counters of the last analysis
+ * (only in builds with -DHB_PROF; returns the number of counters copied, 0 otherwise) */
+int heteff_prof_read(unsigned long long *out, int n);
+
 int heteff_generate(heteff_ctx *ctx, const heteff_gen_side *side, uint64_t *start, uint64_t *end,
                     int32_t *res, uint8_t *kind, void *stream);
 

@@ -13,7 +13,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libheteff_b200.so"
+LIB_PATH = Path(os.environ.get("HETEFF_LIB", Path(__file__).resolve().parent / "libheteff_b200.so"))
 
 # status codes (heteff_status)
 OK, INVALID_TRACE, ANALYSIS_ERROR, VALUE_ERROR, CONTRACT, CUDA_ERROR, NOMEM, BAD_ARG = range(8)
@@ -74,7 +74,7 @@ class GenSide(C.Structure):
 EXPORTED = (
     "heteff_abi_version", "heteff_create", "heteff_destroy", "heteff_last_error",
     "heteff_analyze", "heteff_analyze_host", "heteff_overlap_covers",
-    "heteff_host_metrics", "heteff_device_metrics", "heteff_generate",
+    "heteff_host_metrics", "heteff_device_metrics", "heteff_generate", "heteff_prof_read",
 )
 
 _lib = None
@@ -105,6 +105,8 @@ def load() -> C.CDLL:
         f = getattr(lib, name)
         f.restype = C.c_int
         f.argtypes = [_p, _p, C.c_int32, C.c_uint64, _p, C.POINTER(C.c_uint32), _p]
+    lib.heteff_prof_read.restype = C.c_int
+    lib.heteff_prof_read.argtypes = [_p, C.c_int]
     lib.heteff_generate.restype = C.c_int
     lib.heteff_generate.argtypes = [_p, C.POINTER(GenSide), _p, _p, _p, _p, _p]
     _lib = lib

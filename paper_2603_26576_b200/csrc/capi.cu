@@ -38,8 +38,8 @@ struct heteff_ctx {
     hb::Globals *g = nullptr;
     hb::ResultDev *res_d = nullptr;
     hb::ResultDev *res_h = nullptr;   // pinned
-    // staging for heteff_analyze_host / metrics
-    DevBuf stage;
+    // staging for heteff_analyze_host / metrics; scratch of the overlap error path
+    DevBuf stage, aux;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
@@ -106,7 +106,7 @@ void heteff_destroy(heteff_ctx *ctx)
 {
     if (!ctx) return;
     DevBuf *bufs[] = {&ctx->host_acc, &ctx->dev_acc, &ctx->host_tiles, &ctx->dev_tiles,
-                      &ctx->host_out, &ctx->dev_out, &ctx->lists, &ctx->stage};
+                      &ctx->host_out, &ctx->dev_out, &ctx->lists, &ctx->stage, &ctx->aux};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->g) cudaFree(ctx->g);
@@ -135,7 +135,6 @@ static int run_analysis(heteff_ctx *ctx, const heteff_trace *t, const heteff_opt
     const int64_t hid = t->host_ids > 0 ? t->host_ids : 1, did = t->dev_ids > 0 ? t->dev_ids : 1;
 
     // workspace (grow on demand; accumulators and tile flags start zeroed)
-    bool flags_new = false;
     if (hid > ctx->host_ids_cap) {
         CK(ensure(ctx->host_acc, (size_t)hid * 3 * sizeof(u64), true), "alloc host accumulators");
         ctx->host_ids_cap = (int64_t)(ctx->host_acc.bytes / (3 * sizeof(u64)));
@@ -144,17 +143,15 @@ static int run_analysis(heteff_ctx *ctx, const heteff_trace *t, const heteff_opt
         CK(ensure(ctx->dev_acc, (size_t)did * 4 * sizeof(u64), true), "alloc device accumulators");
         ctx->dev_ids_cap = (int64_t)(ctx->dev_acc.bytes / (4 * sizeof(u64)));
     }
+    // look-back slots: host 2 x 2 words, device 2 x 4 words per tile
     if (ht + 1 > ctx->host_tiles_cap) {
-        CK(ensure(ctx->host_tiles, (size_t)(ht + 1) * (4 + 16), true), "alloc host tile status");
-        ctx->host_tiles_cap = (int64_t)(ctx->host_tiles.bytes / (4 + 16));
-        flags_new = true;
+        CK(ensure(ctx->host_tiles, (size_t)(ht + 1) * 32, true), "alloc host tile status");
+        ctx->host_tiles_cap = (int64_t)(ctx->host_tiles.bytes / 32);
     }
     if (dt + 1 > ctx->dev_tiles_cap) {
-        CK(ensure(ctx->dev_tiles, (size_t)(dt + 1) * (4 + 32), true), "alloc device tile status");
-        ctx->dev_tiles_cap = (int64_t)(ctx->dev_tiles.bytes / (4 + 32));
-        flags_new = true;
+        CK(ensure(ctx->dev_tiles, (size_t)(dt + 1) * 64, true), "alloc device tile status");
+        ctx->dev_tiles_cap = (int64_t)(ctx->dev_tiles.bytes / 64);
     }
-    (void)flags_new;
     CK(ensure(ctx->host_out, (size_t)(t->n > 0 ? t->n : 1) * 4 * sizeof(u64), false), "alloc host summaries");
     CK(ensure(ctx->dev_out, (size_t)(t->m > 0 ? t->m : 1) * 4 * sizeof(u64), false), "alloc device summaries");
     if (opt->list_capacity > ctx->lists_cap) {
@@ -191,20 +188,14 @@ static int run_analysis(heteff_ctx *ctx, const heteff_trace *t, const heteff_opt
     const size_t dc = (size_t)ctx->dev_ids_cap;
     p.d_k = da; p.d_km = da + dc; p.d_clamp = da + 2 * dc; p.d_maxend = da + 3 * dc;
     {
-        const size_t cap = (size_t)ctx->host_tiles_cap;
-        uint8_t *b = static_cast<uint8_t *>(ctx->host_tiles.p);
-        p.h_valA = reinterpret_cast<u64 *>(b);
-        p.h_valP = reinterpret_cast<u64 *>(b + cap * 8);
-        p.h_flag = reinterpret_cast<uint32_t *>(b + cap * 16);
+        u64 *b = static_cast<u64 *>(ctx->host_tiles.p);
+        p.h_slotA = b;
+        p.h_slotP = b + 2 * (size_t)ctx->host_tiles_cap;
     }
     {
-        const size_t cap = (size_t)ctx->dev_tiles_cap;
-        uint8_t *b = static_cast<uint8_t *>(ctx->dev_tiles.p);
-        p.d_valA0 = reinterpret_cast<u64 *>(b);
-        p.d_valA1 = reinterpret_cast<u64 *>(b + cap * 8);
-        p.d_valP0 = reinterpret_cast<u64 *>(b + cap * 16);
-        p.d_valP1 = reinterpret_cast<u64 *>(b + cap * 24);
-        p.d_flag = reinterpret_cast<uint32_t *>(b + cap * 32);
+        u64 *b = static_cast<u64 *>(ctx->dev_tiles.p);
+        p.d_slotA = b;
+        p.d_slotP = b + 4 * (size_t)ctx->dev_tiles_cap;
     }
     p.g = ctx->g;
     int64_t *lb = static_cast<int64_t *>(ctx->lists.p);
@@ -224,6 +215,19 @@ static int run_analysis(heteff_ctx *ctx, const heteff_trace *t, const heteff_opt
         CK(cudaMemcpyAsync(out->device_summaries, ctx->dev_out.p, (size_t)t->m * 4 * sizeof(u64),
                            cudaMemcpyDeviceToHost, s), "d2h device summaries");
     CK(cudaStreamSynchronize(s), "analysis");
+    if (ctx->res_h->status == -1) {
+        // some host records overlap: exact overlap findings, then the finalize
+        CK(ensure(ctx->aux, (size_t)(ht + 1) * 3 * sizeof(u64), false), "alloc overlap scratch");
+        CK(hb::launch_overlap_pass(p, static_cast<u64 *>(ctx->aux.p), s), "launch overlap pass");
+        CK(cudaMemcpyAsync(ctx->res_h, ctx->res_d, sizeof(hb::ResultDev), cudaMemcpyDeviceToHost, s), "d2h result");
+        if (out && out->host_summaries && t->n > 0)
+            CK(cudaMemcpyAsync(out->host_summaries, ctx->host_out.p, (size_t)t->n * 4 * sizeof(u64),
+                               cudaMemcpyDeviceToHost, s), "d2h host summaries");
+        if (out && out->device_summaries && t->m > 0)
+            CK(cudaMemcpyAsync(out->device_summaries, ctx->dev_out.p, (size_t)t->m * 4 * sizeof(u64),
+                               cudaMemcpyDeviceToHost, s), "d2h device summaries");
+        CK(cudaStreamSynchronize(s), "overlap pass");
+    }
     const hb::ResultDev &r = *ctx->res_h;
     if (out && opt->list_capacity > 0) {
         for (int i = 0; i < 8; ++i) {
@@ -373,6 +377,9 @@ int heteff_device_metrics(heteff_ctx *ctx, const uint64_t *summaries, int32_t m,
 {
     return metrics_common(ctx, summaries, m, elapsed, 0, metrics, mask, stream);
 }
+
+// developer instrumentation (builds with -DHB_PROF): per-CTA clock64 phase counters
+int heteff_prof_read(unsigned long long *out, int n) { return hb::prof_read(out, n); }
 
 int heteff_generate(heteff_ctx *ctx, const heteff_gen_side *side, uint64_t *start, uint64_t *end, int32_t *res,
                     uint8_t *kind, void *stream)

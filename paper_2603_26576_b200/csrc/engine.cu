@@ -2,34 +2,40 @@
 //
 // One persistent kernel turns the packed host + device record SoA into every
 // per-rank / per-device summary, all validation findings and both metric
-// trees (reference: compute_report, metrics.py:125-154).  Structure:
+// trees (reference: compute_report, metrics.py:125-154).
 //
-//  * Tiles of kTile=4352 records (17 per compute thread), host tiles first,
-//    then device tiles, claimed in order through one global counter.
-//  * A producer warp streams each tile HBM -> shared memory with 1-D TMA bulk
-//    copies (cp.async.bulk, evict-first) into a 2-stage ring completed on
-//    mbarriers; 8 compute warps pull their 17 records (blocked, odd stride =
-//    bank-conflict free) into registers.  Every record byte is read once.
-//  * The reference's device pipeline flatten/intersect/subtract/complement
-//    (intervals.py:40-105, summarize.py:119-132) reduces to a segmented
-//    running-max scan over start-sorted records:
-//        c_i = max(0, min(e_i,E) - max(s_i, run_i)),  run_i = max earlier end
-//    once over kernel records (U_K) and once over all records (U_KM):
-//        d_kernel = U_K, d_memory = U_KM - U_K, d_idle = E - U_KM.
-//    The host overlap check (model.py:203-215) is the same scan over ends.
-//  * The scan carry across tiles is a decoupled look-back (32-wide window,
-//    epoch-tagged flags, release/acquire).  Contributions are computed first
-//    with the tile-local carry; after the look-back only the prefix of the
-//    tile's head segment with max(s, run) < carry is corrected, so the
-//    look-back latency overlaps the per-record work.
-//  * Per-resource totals leave through warp-level segmented reductions and
-//    one L2 reduction (red.add / red.max) per (segment, warp).
-//  * Device tiles need E (= max host end, summarize.py:88-89): the producer
-//    warp of the first device tile waits for the host tiles (all claimed
-//    earlier, so no deadlock) -- no second launch.
-//  * The last CTA to finish runs the finalize: summaries in declaration
-//    order, the two metric trees with exactly rounded u128/u128 -> f64
-//    divisions (Python int/int semantics), status, and resets the workspace.
+// Tiles of kTile records (kItems per compute thread), host tiles first, then
+// device tiles, claimed in order through one global counter.  Each CTA is
+// warp-specialized:
+//
+//  * a PRODUCER warp streams tiles HBM -> shared memory with 1-D TMA bulk
+//    copies (cp.async.bulk, L2 evict-first) into a kStages ring (mbarriers
+//    full[] / empty[]); after refilling a stage it runs the decoupled
+//    look-back for the scan carry of the tile that just left it and applies
+//    the carry correction to that tile's head segment (a few records, read
+//    from global memory) -- off the critical path;
+//  * kComputeWarps COMPUTE warps pull their records from shared memory
+//    (blocked, odd stride = bank-conflict free), publish the tile's scan
+//    aggregate, compute all per-record work with carry 0 and emit
+//    per-resource totals.  They never wait for a look-back.
+//
+// The reference's device pipeline flatten/intersect/subtract/complement
+// (intervals.py:40-105, summarize.py:119-132) reduces to a segmented
+// running-max scan over start-sorted records: with e' = min(e,E),
+// s' = min(s,e'), run = running max of earlier e',
+//     c = max(run, e') - max(run, s')           (exact, empty if malformed)
+// once over kernel records (U_K) and once over all records (U_KM):
+//     d_kernel = U_K, d_memory = U_KM - U_K, d_idle = E - U_KM.
+// The host overlap check (model.py:203-215) is the same scan over ends.
+// When a tile's time range fits in 32 bits (the common case) the per-record
+// arithmetic runs tile-relative in 32 bits; otherwise in 64 bits.
+//
+// E (= max host end, summarize.py:88-89) is needed by device tiles; host
+// tiles come first and publish their max end, so the first device tile of a
+// warp waits for the host phase once -- no second launch.  The last CTA to
+// finish runs the finalize: summaries in declaration order, both metric
+// trees with exactly rounded u128/u128 -> f64 divisions (Python int/int
+// semantics), status, and the workspace reset.
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <climits>
@@ -37,7 +43,43 @@
 #include "engine.cuh"
 #include "ptx.cuh"
 
+#ifndef HB_UNROLL_A
+#define HB_UNROLL_A HB_ITEMS
+#endif
+#ifndef HB_UNROLL_B
+#define HB_UNROLL_B HB_ITEMS
+#endif
+
 namespace hb {
+
+#ifdef HB_PROF
+// per-CTA clock64 phase counters (tools/prof build only): read back with heteff_prof_read
+constexpr int kProfSlots = 16;
+__device__ unsigned long long hb_prof_buf[1024 * kProfSlots];
+#define PROF_DECL(x) long long x = 0
+#define PROF_NOW() clock64()
+#define PROF_ADD(acc, t0) (acc += clock64() - (t0))
+#else
+#define PROF_DECL(x)
+#define PROF_NOW() 0
+#define PROF_ADD(acc, t0)
+#endif
+
+struct Phases {
+#ifdef HB_PROF
+    long long a = 0, bar = 0, b = 0, emit = 0, t = 0;
+    __device__ __forceinline__ void mark() { t = clock64(); }
+    __device__ __forceinline__ void add(long long &acc) { const long long n = clock64(); acc += n - t; t = n; }
+#else
+    __device__ __forceinline__ void mark() {}
+    template <typename X>
+    __device__ __forceinline__ void add(X &) {}
+    int a, bar, b, emit;
+#endif
+};
+
+constexpr int kUnrollA = HB_UNROLL_A;
+constexpr int kUnrollB = HB_UNROLL_B;
 
 struct StageSmem {
     u64 s[kTile];
@@ -47,22 +89,29 @@ struct StageSmem {
 };
 
 struct Ctrl {
-    uint64_t full[kStages];
+    uint64_t full[kStages];    // producer -> compute: tile data landed
+    uint64_t empty[kStages];   // compute -> producer: stage consumed (+ tile aggregate below)
     int64_t tile[kStages];
     int32_t cnt[kStages];
     int32_t has_prev[kStages];
     int32_t prev_res[kStages];
-    int32_t pad0;
-    u64 prev_start[kStages];
-    // per-tile exchange
-    int32_t w_flag[kComputeWarps];
-    u64 w_v0[kComputeWarps];
-    u64 w_v1[kComputeWarps];
-    u64 w_max[kComputeWarps];
-    u64 carry0[kStages], carry1[kStages];
-    u64 E[kStages];
-    int32_t head_cont[kStages];
     int32_t is_last;
+    u64 prev_start[kStages];
+    u64 prev_end[kStages];
+    // host tiles: per-stage max end and finished-warp count (smem atomics)
+    u64 h_max[kStages];
+    unsigned int h_cnt[kStages];
+    // tile aggregate and head continuation, for the producer's epilogue
+    int32_t t_flag[kStages];
+    int32_t t_head[kStages];
+    u64 t_v0[kStages];
+    u64 t_v1[kStages];
+    // per-stage warp aggregates of the tile (written by compute warps)
+    int32_t w_flag[kStages][kComputeWarps];
+    u64 w_v0[kStages][kComputeWarps];
+    u64 w_v1[kStages][kComputeWarps];
+    u64 w_mn[kStages][kComputeWarps];
+    u64 w_mx[kStages][kComputeWarps];
 };
 
 size_t analyze_smem_bytes() { return sizeof(StageSmem) * kStages + sizeof(Ctrl) + 128; }
@@ -76,20 +125,23 @@ __device__ __forceinline__ bool declared(const int32_t *decl, int32_t ids, int32
     return decl ? (__ldg(decl + r) >= 0) : (r < n);
 }
 
-__device__ __forceinline__ void push(const Params &p, int cls, int64_t gi)
+__device__ __noinline__ void push(const Params &p, int cls, int64_t gi)
 {
     u64 idx = atomicAdd(&p.g->counts[cls], 1ull);
     if ((int64_t)idx < p.cap) p.lists[cls][idx] = gi;
 }
 
-__device__ __forceinline__ void contract(const Params &p, unsigned flag, int64_t gi)
+__device__ __noinline__ void contract(const Params &p, unsigned flag, int64_t gi)
 {
     atomicOr(&p.g->contract_flags, flag);
     atomicMin(&p.g->contract_index, (long long)gi);
 }
 
-// B2: all kThreads threads, reached from the producer and the compute branch
-__device__ __forceinline__ void bar_b2() { asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory"); }
+// named barrier over the compute warps only
+__device__ __forceinline__ void bar_compute()
+{
+    asm volatile("bar.sync 1, %0;" ::"n"(kComputeThreads) : "memory");
+}
 
 __device__ __forceinline__ u64 warp_max(u64 v)
 {
@@ -98,8 +150,59 @@ __device__ __forceinline__ u64 warp_max(u64 v)
     return v;
 }
 
+__device__ __forceinline__ u64 warp_min(u64 v)
+{
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v = umin(v, __shfl_xor_sync(0xffffffffu, v, d));
+    return v;
+}
+
+// 64-bit warp reductions on the REDUX unit (32-bit ops): max/min via the
+// high word first, sums via three 21-bit limbs (exact mod 2^64)
+__device__ __forceinline__ u64 warp_max_rx(u64 v)
+{
+    const unsigned hi = (unsigned)(v >> 32), lo = (unsigned)v;
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    return ((u64)mh << 32) | ml;
+}
+
+__device__ __forceinline__ u64 warp_min_rx(u64 v)
+{
+    const unsigned hi = (unsigned)(v >> 32), lo = (unsigned)v;
+    const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+    return ((u64)mh << 32) | ml;
+}
+
+__device__ __forceinline__ u64 warp_sum_rx(u64 v)
+{
+    const unsigned l0 = (unsigned)v & 0x1fffffu, l1 = (unsigned)(v >> 21) & 0x1fffffu, l2 = (unsigned)(v >> 42);
+    return (u64)__reduce_add_sync(0xffffffffu, l0) + ((u64)__reduce_add_sync(0xffffffffu, l1) << 21) +
+           ((u64)__reduce_add_sync(0xffffffffu, l2) << 42);
+}
+
+__device__ __forceinline__ u64 warp_sum(u64 v)
+{
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    return v;
+}
+
+// E for device tiles: the explicit window, the max host end (after every
+// host tile published), or "no clamp" for device-only traces
+__device__ u64 device_window(const Params &p)
+{
+    if (p.mode == kSummarizeDevice) return p.elapsed_arg;
+    if ((p.mode == kReport || p.mode == kValidate) && p.n >= 1) {
+        while (ld_acquire64(&p.g->host_done) < (u64)p.host_tiles) __nanosleep(64);
+        return umax(ld_relaxed(&p.g->host_max_end), p.host_elapsed_floor);
+    }
+    return ~0ull;
+}
+
 // -------------------------------------------------------------------------
-// producer: claim a tile and stream it into a stage
+// producer: stream a claimed tile into a stage
 // -------------------------------------------------------------------------
 template <typename T>
 __device__ __forceinline__ uint32_t bulk_bytes(int cnt, bool tma)
@@ -122,11 +225,44 @@ __device__ __forceinline__ void issue_bulk(T *dst, const T *src, int cnt, bool t
     if (b) tma_load_1d(dst, src, b, bar, pol);
 }
 
-__device__ void produce(const Params &p, StageSmem *stages, Ctrl *c, int st, int lane, uint64_t pol)
+// the record before a tile (for segment / order checks), loaded one
+// iteration ahead of the refill so its latency is hidden
+struct Claim {
+    int64_t t;
+    int32_t prev_r;
+    u64 prev_s, prev_e;
+};
+
+__device__ __forceinline__ int64_t claim_issue(const Params &p, int lane)
 {
     int64_t t = 0;
     if (lane == 0) t = (int64_t)atomicAdd(&p.g->tile_counter, 1ull);
-    t = __shfl_sync(0xffffffffu, t, 0);
+    return t;
+}
+
+// the claimed index (issued earlier by lane 0) and the record before the tile
+__device__ __forceinline__ Claim claim_finish(const Params &p, int64_t issued)
+{
+    Claim cl;
+    cl.t = __shfl_sync(0xffffffffu, issued, 0);
+    cl.prev_r = 0;
+    cl.prev_s = 0;
+    cl.prev_e = 0;
+    if (cl.t < p.host_tiles + p.dev_tiles) {
+        const bool dev = cl.t >= p.host_tiles;
+        const int64_t base = (dev ? cl.t - p.host_tiles : cl.t) * kTile;
+        if (base > 0) {
+            cl.prev_r = __ldcg((dev ? p.dr : p.hr) + base - 1);
+            cl.prev_s = __ldcg((dev ? p.ds : p.hs) + base - 1);
+            cl.prev_e = __ldcg((dev ? p.de : p.he) + base - 1);
+        }
+    }
+    return cl;
+}
+
+__device__ void produce(const Params &p, StageSmem *stages, Ctrl *c, int st, const Claim &cl, int lane, uint64_t pol)
+{
+    const int64_t t = cl.t;
     const int64_t total = p.host_tiles + p.dev_tiles;
     if (t >= total) {
         if (lane == 0) {
@@ -150,8 +286,9 @@ __device__ void produce(const Params &p, StageSmem *stages, Ctrl *c, int st, int
         c->tile[st] = t;
         c->cnt[st] = cnt;
         c->has_prev[st] = base > 0;
-        c->prev_res[st] = base > 0 ? R[-1] : 0;
-        c->prev_start[st] = base > 0 ? S[-1] : 0;
+        c->prev_res[st] = cl.prev_r;
+        c->prev_start[st] = cl.prev_s;
+        c->prev_end[st] = cl.prev_e;
     }
     copy_tail(sm.s, S, cnt, tma, lane);
     copy_tail(sm.e, E, cnt, tma, lane);
@@ -159,7 +296,8 @@ __device__ void produce(const Params &p, StageSmem *stages, Ctrl *c, int st, int
     copy_tail(sm.k, K, cnt, tma, lane);
     __syncwarp();
     if (lane == 0) {
-        const uint32_t tx = bulk_bytes<u64>(cnt, tma) * 2 + bulk_bytes<int32_t>(cnt, tma) + bulk_bytes<uint8_t>(cnt, tma);
+        const uint32_t tx =
+            bulk_bytes<u64>(cnt, tma) * 2 + bulk_bytes<int32_t>(cnt, tma) + bulk_bytes<uint8_t>(cnt, tma);
         if (tx) {
             fence_proxy_async_smem();   // generic accesses of this stage -> async-proxy writes
             mbar_arrive_expect_tx(&c->full[st], tx);
@@ -174,125 +312,106 @@ __device__ void produce(const Params &p, StageSmem *stages, Ctrl *c, int st, int
 }
 
 // -------------------------------------------------------------------------
-// decoupled look-back over a 32-tile window (producer warp)
+// decoupled look-back (producer warp), 32-tile window, one round trip:
+// every slot word is (epoch << 32 | 32-bit half of the value), so a slot is
+// valid iff all its words carry the current epoch -- no flag / value
+// ordering needed.  Separate A (aggregate) and P (inclusive prefix) slots.
 // -------------------------------------------------------------------------
 template <int NV>
-__device__ void look_back(const uint32_t *flags, const u64 *valA0, const u64 *valA1, const u64 *valP0,
-                          const u64 *valP1, int64_t t, uint32_t epoch, int lane, u64 &c0, u64 &c1)
+__device__ __forceinline__ void publish(u64 *slot, uint32_t epoch, u64 v0, u64 v1)
 {
+    const u64 tag = (u64)epoch << 32;
+    st_relaxed(slot + 0, tag | (v0 >> 32));
+    st_relaxed(slot + 1, tag | (v0 & 0xffffffffull));
+    if (NV == 2) {
+        st_relaxed(slot + 2, tag | (v1 >> 32));
+        st_relaxed(slot + 3, tag | (v1 & 0xffffffffull));
+    }
+}
+
+template <int NV>
+__device__ __forceinline__ bool read_slot(const u64 *slot, uint32_t epoch, u64 &v0, u64 &v1)
+{
+    const u64 a = ld_relaxed(slot + 0), b = ld_relaxed(slot + 1);
+    bool ok = (a >> 32) == epoch && (b >> 32) == epoch;
+    v0 = (a << 32) | (b & 0xffffffffull);
+    v1 = 0;
+    if (NV == 2) {
+        const u64 c = ld_relaxed(slot + 2), d = ld_relaxed(slot + 3);
+        ok = ok && (c >> 32) == epoch && (d >> 32) == epoch;
+        v1 = (c << 32) | (d & 0xffffffffull);
+    }
+    return ok;
+}
+
+template <int NV>
+__device__ void look_back(const u64 *slotA, const u64 *slotP, int64_t t, uint32_t epoch, int lane, u64 &c0, u64 &c1)
+{
+    constexpr int W = 2 * NV;   // words per slot
+    constexpr int Q = 4;        // tiles per lane: 128-tile window per round trip
     u64 acc0 = 0, acc1 = 0;
     int64_t pos = t - 1;
     while (pos >= 0) {
-        const int64_t i = pos - lane;
-        uint32_t stt = 2;                      // before tile 0: identity, acts as prefix
-        if (i >= 0) {
-            const uint32_t f = ld_acquire(flags + i);
-            stt = ((f >> 2) == epoch) ? (f & 3u) : 0u;
-        }
-        const unsigned pm = __ballot_sync(0xffffffffu, stt == 2);
-        const unsigned xm = __ballot_sync(0xffffffffu, stt == 0);
-        const int firstP = pm ? (__ffs(pm) - 1) : 32;
-        const unsigned need = firstP >= 31 ? 0xffffffffu : ((2u << firstP) - 1u);
-        if (xm & need) {
-            __nanosleep(20);
-            continue;
-        }
-        u64 v0 = 0, v1 = 0;
-        if (i >= 0 && lane <= firstP) {
-            if (lane == firstP) {
-                v0 = ld_relaxed(valP0 + i);
-                if (NV == 2) v1 = ld_relaxed(valP1 + i);
-            } else {
-                v0 = ld_relaxed(valA0 + i);
-                if (NV == 2) v1 = ld_relaxed(valA1 + i);
+        uint32_t stt[Q];
+        u64 v0[Q], v1[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const int64_t i = pos - lane - 32 * q;
+            stt[q] = 2;                        // before tile 0: identity, acts as prefix
+            v0[q] = v1[q] = 0;
+            if (i >= 0) {
+                u64 p0, p1, a0, a1;
+                const bool pv = read_slot<NV>(slotP + i * W, epoch, p0, p1);
+                const bool av = read_slot<NV>(slotA + i * W, epoch, a0, a1);
+                stt[q] = pv ? 2u : (av ? 1u : 0u);
+                v0[q] = pv ? p0 : a0;
+                v1[q] = pv ? p1 : a1;
             }
         }
-        acc0 = umax(acc0, warp_max(v0));
-        if (NV == 2) acc1 = umax(acc1, warp_max(v1));
-        if (firstP < 32) break;
-        pos -= 32;
+        bool ready = true, done = false;
+        u64 r0 = 0, r1 = 0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            if (!done) {
+                const unsigned pm = __ballot_sync(0xffffffffu, stt[q] == 2);
+                const unsigned xm = __ballot_sync(0xffffffffu, stt[q] == 0);
+                const int firstP = pm ? (__ffs(pm) - 1) : 32;
+                const unsigned need = firstP >= 31 ? 0xffffffffu : ((2u << firstP) - 1u);
+                if (xm & need) {
+                    ready = false;
+                    done = true;
+                } else {
+                    r0 = umax(r0, warp_max(lane <= firstP ? v0[q] : 0));
+                    if (NV == 2) r1 = umax(r1, warp_max(lane <= firstP ? v1[q] : 0));
+                    if (firstP < 32) done = true;
+                }
+            }
+        }
+        if (!ready) {
+            __nanosleep(32);
+            continue;
+        }
+        acc0 = umax(acc0, r0);
+        acc1 = umax(acc1, r1);
+        if (done) break;
+        pos -= 32 * Q;
     }
     c0 = acc0;
     c1 = acc1;
 }
 
-// -------------------------------------------------------------------------
-// per-tile processing, shared skeleton
-// -------------------------------------------------------------------------
 struct TileCtx {
     int64_t lt;        // tile index within its side
     int64_t gbase;     // global record index of item 0 of this tile
     int cnt;
     int st;            // stage holding this tile
-    int refill;        // stage the producer refills at B1 (-1: none)
 };
 
-// Phase A scan state of one compute thread over its kItems records.
-struct Scan {
-    uint32_t sfm;      // bit j: record j starts a new resource segment
-    int nv;            // valid records of this thread
-    bool t_flag;       // thread contains a segment start
-    u64 t_v0, t_v1;    // max end over the thread's LAST segment (v0: kernel-only for devices)
-    u64 t_max;         // max end over all records of the thread
-};
-
-// Phase A: stream the thread's records from shared memory once, derive the
-// segment-start mask, check the canonical-order contract and the kind codes,
-// and reduce the scan aggregate.
-template <bool PARTIAL, bool DEV>
-__device__ __forceinline__ Scan phase_a(const Params &p, const StageSmem &sm, const Ctrl *c, const TileCtx &tc,
-                                        int ctid, int64_t gi0)
+// combine two segmented-max scan elements, a earlier than b
+__device__ __forceinline__ void seg_combine(bool af, u64 a0, u64 a1, bool &bf, u64 &b0, u64 &b1)
 {
-    Scan sc;
-    const int b = ctid * kItems;
-    sc.nv = PARTIAL ? max(0, min(kItems, tc.cnt - b)) : kItems;
-    sc.sfm = 0;
-    sc.t_flag = false;
-    sc.t_v0 = sc.t_v1 = sc.t_max = 0;
-    if (sc.nv == 0) return sc;
-    bool hp;
-    int32_t pr;
-    u64 ps;
-    if (ctid == 0) {
-        hp = c->has_prev[tc.st] != 0;
-        pr = c->prev_res[tc.st];
-        ps = c->prev_start[tc.st];
-    } else {
-        hp = true;
-        pr = sm.r[b - 1];
-        ps = sm.s[b - 1];
-    }
-    int bad = -1;
-    bool badkind = false;
-#pragma unroll
-    for (int j = 0; j < kItems; ++j) {
-        if (PARTIAL && j >= sc.nv) break;
-        const int32_t r = sm.r[b + j];
-        const u64 s = sm.s[b + j], e = sm.e[b + j];
-        const uint8_t k = sm.k[b + j];
-        const bool h = j > 0 || hp;
-        if (!h || r != pr) {
-            sc.sfm |= 1u << j;
-            sc.t_flag = true;
-            sc.t_v0 = 0;
-            sc.t_v1 = 0;
-        }
-        if (bad < 0 && h && (r < pr || (r == pr && s < ps))) bad = j;
-        if (DEV) {
-            badkind |= k > 1;
-            sc.t_v1 = umax(sc.t_v1, e);
-            if (k == 0) sc.t_v0 = umax(sc.t_v0, e);
-        } else {
-            badkind |= k > 2;
-            sc.t_v0 = umax(sc.t_v0, e);
-        }
-        sc.t_max = umax(sc.t_max, e);
-        pr = r;
-        ps = s;
-    }
-    if (bad >= 0) contract(p, DEV ? 2u : 1u, gi0 + bad);
-    if (badkind) contract(p, DEV ? 8u : 4u, gi0);
-    return sc;
+    if (!bf) { b0 = umax(a0, b0); b1 = umax(a1, b1); }
+    bf = bf || af;
 }
 
 // warp inclusive segmented max scan of (flag, v0, v1)
@@ -302,47 +421,101 @@ __device__ __forceinline__ void warp_seg_max(bool &f, u64 &v0, u64 &v1, int lane
     for (int d = 1; d < 32; d <<= 1) {
         const bool of = __shfl_up_sync(0xffffffffu, f, d);
         const u64 o0 = shfl_up64(v0, d), o1 = shfl_up64(v1, d);
-        if (lane >= d) {
-            if (!f) { v0 = umax(v0, o0); v1 = umax(v1, o1); }
-            f |= of;
-        }
+        if (lane >= d) seg_combine(of, o0, o1, f, v0, v1);
     }
 }
 
-// thread-exclusive prefix inside the tile from the warp aggregates (smem)
-// and the lane-inclusive scan values
-__device__ __forceinline__ void tile_exclusive(const Ctrl *c, int warp, int lane, bool in_f, u64 in0, u64 in1,
-                                               bool &xf, u64 &x0, u64 &x1)
+// Per-tile values every compute thread derives (cooperatively per warp)
+// from the warp aggregates.
+struct TileView {
+    bool xf;           // a segment starts before this thread inside the tile
+    u64 x0, x1;        // exclusive segmented max (v0 / v1) for this thread
+    u64 base, top;     // min start / max end over the tile's records
+    bool fits32;       // top - base < 2^32: tile-relative 32-bit arithmetic is exact
+    bool tf;           // tile aggregate: a segment starts in the tile,
+    u64 t0, t1;        //   max ends over the tile's last segment
+};
+
+__device__ __forceinline__ TileView tile_view(const Ctrl *c, int st, int warp, int lane, bool in_f, u64 in0, u64 in1)
 {
-    xf = false;
-    x0 = x1 = 0;
-#pragma unroll
-    for (int w = 0; w < kComputeWarps; ++w) {
-        if (w < warp) {
-            if (c->w_flag[w]) { xf = true; x0 = c->w_v0[w]; x1 = c->w_v1[w]; }
-            else { x0 = umax(x0, c->w_v0[w]); x1 = umax(x1, c->w_v1[w]); }
-        }
+    TileView v;
+    bool f = false;
+    u64 a0 = 0, a1 = 0, mn = ~0ull, mx = 0;
+    if (lane < kComputeWarps) {
+        f = c->w_flag[st][lane] != 0;
+        a0 = c->w_v0[st][lane];
+        a1 = c->w_v1[st][lane];
+        mn = c->w_mn[st][lane];
+        mx = c->w_mx[st][lane];
     }
+    v.base = warp_min_rx(mn);
+    v.top = warp_max_rx(mx);
+    v.fits32 = v.top >= v.base && (v.top - v.base) < (1ull << 32);
+    warp_seg_max(f, a0, a1, lane);                 // inclusive over warps 0..lane
+    v.tf = __shfl_sync(0xffffffffu, f, kComputeWarps - 1);
+    v.t0 = __shfl_sync(0xffffffffu, a0, kComputeWarps - 1);
+    v.t1 = __shfl_sync(0xffffffffu, a1, kComputeWarps - 1);
+    const int src = warp > 0 ? warp - 1 : 0;
+    const bool wf = __shfl_sync(0xffffffffu, f, src);
+    const u64 w0 = __shfl_sync(0xffffffffu, a0, src), w1 = __shfl_sync(0xffffffffu, a1, src);
+    v.xf = warp > 0 && wf;
+    v.x0 = warp > 0 ? w0 : 0;
+    v.x1 = warp > 0 ? w1 : 0;
     const bool lf = __shfl_up_sync(0xffffffffu, in_f, 1);
     const u64 l0 = shfl_up64(in0, 1), l1 = shfl_up64(in1, 1);
     if (lane > 0) {
-        if (lf) { xf = true; x0 = l0; x1 = l1; }
-        else { x0 = umax(x0, l0); x1 = umax(x1, l1); }
+        bool bf = lf;
+        u64 b0 = l0, b1 = l1;
+        seg_combine(v.xf, v.x0, v.x1, bf, b0, b1);
+        v.xf = bf; v.x0 = b0; v.x1 = b1;
     }
+    return v;
 }
 
-// Emit per-resource totals: warp-level segmented reduction of per-thread
-// pieces, then one L2 reduction per (segment, warp).  A thread's record run
-// splits into a head piece (records before its first segment start, which
-// continue the left neighbour's segment), complete middle segments (already
-// emitted) and a tail piece.  NA = number of add fields, field NA is a max.
+// Right after the tile view: publish the tile aggregate (P if a segment
+// starts in the tile -- its tail prefix is then local -- else A), the host
+// max end for E, and hand the producer what its epilogue needs.
+template <bool DEV>
+__device__ __forceinline__ void publish_tile(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc,
+                                             const TileView &tv)
+{
+    const bool head = tc.cnt > 0 && c->has_prev[tc.st] && sm.r[0] == c->prev_res[tc.st];
+    if (DEV) publish<2>(tv.tf ? p.d_slotP + 4 * tc.lt : p.d_slotA + 4 * tc.lt, p.epoch, tv.t0, tv.t1);
+    else publish<1>(tv.tf ? p.h_slotP + 2 * tc.lt : p.h_slotA + 2 * tc.lt, p.epoch, tv.t0, 0);
+    c->t_flag[tc.st] = tv.tf;
+    c->t_head[tc.st] = head;
+    c->t_v0[tc.st] = tv.t0;
+    c->t_v1[tc.st] = tv.t1;
+}
+
+// Emit per-resource totals.  A thread's records split into a head piece
+// (records before its first segment start -- they continue the left
+// neighbour's segment), complete middle segments (emitted in the record
+// loop) and a tail piece.  Warps without any segment start reduce with a
+// butterfly; otherwise a warp-level segmented scan.  One L2 reduction per
+// (segment, warp).  Fields [0, NA) are sums, field NA is a max.
 template <int NA>
-__device__ __forceinline__ void emit_segments(u64 (&head)[NA + 1], u64 (&tail)[NA + 1], uint32_t sfm, int nv,
-                                              int32_t first_r, int32_t tail_r, int32_t ids, u64 *const (&dst)[NA + 1],
-                                              int lane)
+__device__ __forceinline__ void emit_segments(const u64 (&head)[NA + 1], const u64 (&tail)[NA + 1], uint32_t sfm,
+                                              int nv, int32_t first_r, int32_t tail_r, int32_t ids,
+                                              u64 *const (&dst)[NA + 1], int lane)
 {
     const bool any = nv > 0;
     const bool f = sfm != 0;
+    if (__ballot_sync(0xffffffffu, f) == 0) {
+        u64 v[NA + 1];
+#pragma unroll
+        for (int i = 0; i < NA; ++i) v[i] = warp_sum_rx(tail[i]);
+        v[NA] = warp_max_rx(tail[NA]);
+        const int32_t r = __shfl_sync(0xffffffffu, first_r, 0);
+        const bool a0 = __shfl_sync(0xffffffffu, any, 0);
+        if (lane == 0 && a0 && r >= 0 && r < ids) {
+#pragma unroll
+            for (int i = 0; i < NA; ++i)
+                if (v[i]) red_add(dst[i] + r, v[i]);
+            if (v[NA]) red_max(dst[NA] + r, v[NA]);
+        }
+        return;
+    }
     u64 v[NA + 1];
 #pragma unroll
     for (int i = 0; i <= NA; ++i) v[i] = tail[i];
@@ -368,7 +541,6 @@ __device__ __forceinline__ void emit_segments(u64 (&head)[NA + 1], u64 (&tail)[N
     for (int i = 0; i <= NA; ++i) l[i] = shfl_up64(v[i], 1);
     const int32_t lr = __shfl_up_sync(0xffffffffu, sr, 1);
     if (any && f) {
-        // the segment that ends right before this thread's first segment start
         const bool sf0 = sfm & 1u;
         bool have = !sf0;
         int32_t r = first_r;
@@ -397,274 +569,514 @@ __device__ __forceinline__ void emit_segments(u64 (&head)[NA + 1], u64 (&tail)[N
     }
 }
 
-// =========================================================================
-// HOST tiles: per-rank sums + span, overlap validation (summarize.py:57-92,
-// model.py:192-215)
-// =========================================================================
-template <bool PARTIAL>
-__device__ __forceinline__ void host_tile(const Params &p, StageSmem *stages, Ctrl *c, const TileCtx &tc, int tid,
-                                          uint64_t pol)
+// Phase A: segment-start mask, the scan aggregate (max end over the thread's
+// LAST segment; devices: v0 kernel-only, v1 all) and the thread's min start /
+// max end, from res + end (+ kind) in shared memory.
+template <bool DEV>
+__device__ __forceinline__ void phase_a(const StageSmem &sm, const Ctrl *c, int st, int b, int nv, uint32_t &sfm,
+                                        u64 &v0, u64 &v1, u64 &mn, u64 &mx)
 {
-    const int warp = tid >> 5, lane = tid & 31;
-    const bool producer = warp == kComputeWarps;
-    const StageSmem &sm = stages[tc.st];
-    const int b = tid * kItems;
-    const int64_t gi0 = tc.gbase + (int64_t)b;
-
-    Scan sc;
-    bool in_f = false;
-    u64 in0 = 0, in1 = 0;
-    if (!producer) {
-        sc = phase_a<PARTIAL, false>(p, sm, c, tc, tid, gi0);
-        in_f = sc.t_flag; in0 = sc.t_v0;
-        warp_seg_max(in_f, in0, in1, lane);
-        const u64 wm = warp_max(sc.t_max);
-        if (lane == 31) { c->w_flag[warp] = in_f; c->w_v0[warp] = in0; c->w_v1[warp] = 0; c->w_max[warp] = wm; }
-    } else if (lane == 0) {
-        c->head_cont[tc.st] = c->has_prev[tc.st] && sm.r[0] == c->prev_res[tc.st];
+    sfm = 0;
+    v0 = v1 = 0;
+    mn = ~0ull;
+    mx = 0;
+    if (nv == 0) return;
+    bool hp;
+    int32_t pr;
+    if (b == 0) {
+        hp = c->has_prev[st] != 0;
+        pr = c->prev_res[st];
+    } else {
+        hp = true;
+        pr = sm.r[b - 1];
     }
-    __syncthreads();  // B1 ------------------------------------------------
-
-    if (producer) {
-        bool f = false;
-        u64 v = 0, mx = 0;
-#pragma unroll
-        for (int w = 0; w < kComputeWarps; ++w) {
-            if (c->w_flag[w]) { f = true; v = c->w_v0[w]; }
-            else v = umax(v, c->w_v0[w]);
-            mx = umax(mx, c->w_max[w]);
-        }
-        if (lane == 0) {
-            st_relaxed(f ? p.h_valP + tc.lt : p.h_valA + tc.lt, v);
-            st_release(p.h_flag + tc.lt, (p.epoch << 2) | (f ? 2u : 1u));
-            red_max(&p.g->host_max_end, mx);
-            asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(&p.g->host_done) : "memory");
-        }
-        if (tc.refill >= 0) produce(p, stages, c, tc.refill, lane, pol);
-        u64 carry = 0, dummy = 0;
-        if (c->head_cont[tc.st]) {
-            look_back<1>(p.h_flag, p.h_valA, nullptr, p.h_valP, nullptr, tc.lt, p.epoch, lane, carry, dummy);
-            if (!f && lane == 0) {
-                st_relaxed(p.h_valP + tc.lt, umax(carry, v));
-                st_release(p.h_flag + tc.lt, (p.epoch << 2) | 2u);
-            }
-        }
-        if (lane == 0) c->carry0[tc.st] = carry;
-        bar_b2();  // B2 (producer side)
-        return;
-    }
-
-    bool xf;
-    u64 xv, xdummy;
-    tile_exclusive(c, warp, lane, in_f, in0, in1, xf, xv, xdummy);
-    // pieces: [0]=offload, [1]=mpi (adds), [2]=span (max)
-    u64 head[3] = {0, 0, 0}, cur[3] = {0, 0, 0};
-    bool head_open = !(sc.sfm & 1u);
-    int32_t cur_r = sc.nv ? sm.r[b] : 0;
-    const int32_t first_r = cur_r;
-    bool cur_decl = sc.nv ? declared(p.host_decl, p.host_ids, p.n, cur_r) : false;
-    u64 run = xv;
-#pragma unroll
+    mn = sm.s[b];
+#pragma unroll kUnrollA
     for (int j = 0; j < kItems; ++j) {
-        if (PARTIAL && j >= sc.nv) break;
-        if ((sc.sfm >> j) & 1u) {
-            if (j > 0) {
-                if (head_open) {
-                    head[0] = cur[0]; head[1] = cur[1]; head[2] = cur[2];
-                } else if (cur_r >= 0 && cur_r < p.host_ids) {   // complete segment inside the thread
-                    if (cur[0]) red_add(p.h_off + cur_r, cur[0]);
-                    if (cur[1]) red_add(p.h_mpi + cur_r, cur[1]);
-                    if (cur[2]) red_max(p.h_span + cur_r, cur[2]);
-                }
-                head_open = false;
-                cur_r = sm.r[b + j];
-                cur_decl = declared(p.host_decl, p.host_ids, p.n, cur_r);
+        if (j < nv) {
+            const int32_t r = sm.r[b + j];
+            const u64 e = sm.e[b + j];
+            if ((j == 0 && !hp) || r != pr) {
+                sfm |= 1u << j;
+                mx = umax(mx, DEV ? v1 : v0);
+                v0 = 0;
+                v1 = 0;
+                mn = umin(mn, sm.s[b + j]);
             }
-            cur[0] = cur[1] = cur[2] = 0;
-            run = 0;
+            if (DEV) {
+                if (sm.k[b + j] == 0) v0 = umax(v0, e);
+                v1 = umax(v1, e);
+            } else {
+                v0 = umax(v0, e);
+            }
+            pr = r;
         }
-        const u64 s = sm.s[b + j], e = sm.e[b + j];
-        const uint8_t k = sm.k[b + j];
-        const int64_t gi = gi0 + j;
-        if (s > e) push(p, 0, gi);
-        else if (s == e) push(p, 1, gi);
-        if (!cur_decl) push(p, 2, gi);
-        if (cur_decl && s < e && s < run) push(p, 3, gi);
-        run = umax(run, e);
-        if (s <= e) {
-            if (k == 1) cur[0] += e - s;
-            else if (k == 2) cur[1] += e - s;
-        }
-        cur[2] = umax(cur[2], e);
     }
-    bar_b2();  // B2 ------------------------------------------------
+    mx = umax(mx, DEV ? v1 : v0);
+}
 
-    // overlap fix-up: prefix of the tile head segment with start < carry
-    if (c->head_cont[tc.st] && !xf && sc.nv > 0 && !(sc.sfm & 1u) && declared(p.host_decl, p.host_ids, p.n, first_r)) {
-        const u64 carry = c->carry0[tc.st];
-        u64 r2 = xv;
-#pragma unroll
-        for (int j = 0; j < kItems; ++j) {
-            if ((PARTIAL && j >= sc.nv) || ((sc.sfm >> j) & 1u)) break;
-            const u64 s = sm.s[b + j], e = sm.e[b + j];
-            if (s >= carry) break;
-            if (s < e && s >= r2) push(p, 3, gi0 + j);   // overlap only visible with the carry
-            r2 = umax(r2, e);
-        }
+// record values in the arithmetic domain of phase B: 32-bit tile-relative
+// (exact when the tile's time range fits in 32 bits) or absolute 64-bit
+template <typename T>
+struct Dom;
+template <>
+struct Dom<uint32_t> {
+    u64 base, top;
+    uint32_t bl;
+    __device__ __forceinline__ Dom(u64 b, u64 t) : base(b), top(t), bl((uint32_t)b) {}
+    __device__ __forceinline__ uint32_t ld(const u64 *a, int i) const
+    {
+        return reinterpret_cast<const uint32_t *>(a)[2 * i] - bl;
     }
-    if (head_open) { head[0] = head[1] = head[2] = 0; }
-    u64 *const dst[3] = {p.h_off, p.h_mpi, p.h_span};
-    emit_segments<2>(head, cur, sc.sfm, sc.nv, first_r, cur_r, p.host_ids, dst, lane);
+    // saturating map of an absolute value into [0, top - base]
+    __device__ __forceinline__ uint32_t rel(u64 v) const
+    {
+        return v <= base ? 0u : (v >= top ? (uint32_t)(top - base) : (uint32_t)(v - base));
+    }
+    __device__ __forceinline__ u64 abs(uint32_t v) const { return base + v; }
+};
+template <>
+struct Dom<u64> {
+    __device__ __forceinline__ Dom(u64, u64) {}
+    __device__ __forceinline__ u64 ld(const u64 *a, int i) const { return a[i]; }
+    __device__ __forceinline__ u64 rel(u64 v) const { return v; }
+    __device__ __forceinline__ u64 abs(u64 v) const { return v; }
+};
+
+template <typename T>
+__device__ __forceinline__ T tmax(T a, T b) { return a > b ? a : b; }
+template <typename T>
+__device__ __forceinline__ T tmin(T a, T b) { return a < b ? a : b; }
+
+struct Pieces3 {
+    u64 head[3], cur[3];
+    bool head_open;
+    int32_t cur_r, first_r;
+    bool cur_decl;
+};
+
+// close the running piece at a segment start: the first piece becomes the
+// head piece, later ones are complete segments inside the thread
+__device__ __forceinline__ void close_piece(Pieces3 &P, int32_t ids, u64 *d0, u64 *d1, u64 *d2)
+{
+    if (P.head_open) {
+        P.head[0] = P.cur[0]; P.head[1] = P.cur[1]; P.head[2] = P.cur[2];
+    } else if (P.cur_r >= 0 && P.cur_r < ids) {
+        if (P.cur[0]) red_add(d0 + P.cur_r, P.cur[0]);
+        if (P.cur[1]) red_add(d1 + P.cur_r, P.cur[1]);
+        if (P.cur[2]) red_max(d2 + P.cur_r, P.cur[2]);
+    }
+    P.head_open = false;
 }
 
 // =========================================================================
-// DEVICE tiles: dual running-max union scan (summarize.py:95-138)
+// per-thread 64-bit rescan for threads whose fast pass flagged anything
+// rare: findings lists (model.py:192-228), clamp counts (summarize.py:113),
+// canonical-order contract.  Exact for any input, including records whose
+// ends wrap the 32-bit tile-relative domain (malformed).
 // =========================================================================
-template <bool PARTIAL>
-__device__ __forceinline__ void dev_tile(const Params &p, StageSmem *stages, Ctrl *c, const TileCtx &tc, int tid,
-                                         uint64_t pol, u64 &E_cache, bool &E_known)
+template <bool DEV>
+__device__ __noinline__ void rescan(const Params &p, const StageSmem &sm, const Ctrl *c, int st, int b, int nv,
+                                    u64 x0, u64 E, bool late_check, int64_t gi0)
 {
-    const int warp = tid >> 5, lane = tid & 31;
-    const bool producer = warp == kComputeWarps;
-    const StageSmem &sm = stages[tc.st];
-    const int b = tid * kItems;
-    const int64_t gi0 = tc.gbase + (int64_t)b;
-
-    Scan sc;
-    bool in_f = false;
-    u64 in0 = 0, in1 = 0;
-    if (!producer) {
-        sc = phase_a<PARTIAL, true>(p, sm, c, tc, tid, gi0);
-        in_f = sc.t_flag; in0 = sc.t_v0; in1 = sc.t_v1;
-        warp_seg_max(in_f, in0, in1, lane);
-        if (lane == 31) { c->w_flag[warp] = in_f; c->w_v0[warp] = in0; c->w_v1[warp] = in1; }
-    } else if (lane == 0) {
-        c->head_cont[tc.st] = c->has_prev[tc.st] && sm.r[0] == c->prev_res[tc.st];
-        if (!E_known) {
-            u64 E;
-            if (p.mode == kSummarizeDevice) E = p.elapsed_arg;
-            else if ((p.mode == kReport || p.mode == kValidate) && p.n >= 1) {
-                // E = max host end (summarize.py:88-89): wait for every host tile
-                while (ld_acquire64(&p.g->host_done) < (u64)p.host_tiles) __nanosleep(64);
-                E = umax(ld_relaxed(&p.g->host_max_end), p.host_elapsed_floor);
-            } else {
-                E = ~0ull;   // device-only trace: E = max device end, nothing is clamped
-            }
-            E_cache = E;
-            E_known = true;
-        }
-        c->E[tc.st] = E_cache;
+    bool hp = true;
+    int32_t pr = 0;
+    u64 ps = 0;
+    if (b == 0) {
+        hp = c->has_prev[st] != 0;
+        pr = c->prev_res[st];
+        ps = c->prev_start[st];
+    } else {
+        pr = sm.r[b - 1];
+        ps = sm.s[b - 1];
     }
-    __syncthreads();  // B1 ------------------------------------------------
-
-    if (producer) {
-        bool f = false;
-        u64 vk = 0, vkm = 0;
-#pragma unroll
-        for (int w = 0; w < kComputeWarps; ++w) {
-            if (c->w_flag[w]) { f = true; vk = c->w_v0[w]; vkm = c->w_v1[w]; }
-            else { vk = umax(vk, c->w_v0[w]); vkm = umax(vkm, c->w_v1[w]); }
-        }
-        if (lane == 0) {
-            if (f) { st_relaxed(p.d_valP0 + tc.lt, vk); st_relaxed(p.d_valP1 + tc.lt, vkm); }
-            else { st_relaxed(p.d_valA0 + tc.lt, vk); st_relaxed(p.d_valA1 + tc.lt, vkm); }
-            st_release(p.d_flag + tc.lt, (p.epoch << 2) | (f ? 2u : 1u));
-        }
-        if (tc.refill >= 0) produce(p, stages, c, tc.refill, lane, pol);
-        u64 ck = 0, ckm = 0;
-        if (c->head_cont[tc.st]) {
-            look_back<2>(p.d_flag, p.d_valA0, p.d_valA1, p.d_valP0, p.d_valP1, tc.lt, p.epoch, lane, ck, ckm);
-            if (!f && lane == 0) {
-                st_relaxed(p.d_valP0 + tc.lt, umax(ck, vk));
-                st_relaxed(p.d_valP1 + tc.lt, umax(ckm, vkm));
-                st_release(p.d_flag + tc.lt, (p.epoch << 2) | 2u);
-            }
-        }
-        if (lane == 0) { c->carry0[tc.st] = ck; c->carry1[tc.st] = ckm; }
-        bar_b2();  // B2 (producer side)
-        return;
-    }
-
-    const u64 E = c->E[tc.st];
-    const bool late_check = (p.mode == kReport || p.mode == kValidate) && p.n >= 1;
-    bool xf;
-    u64 xk, xkm;
-    tile_exclusive(c, warp, lane, in_f, in0, in1, xf, xk, xkm);
-    // pieces: [0]=U_K, [1]=U_KM, [2]=clamped (adds), [3]=max end (max)
-    u64 head[4] = {0, 0, 0, 0}, cur[4] = {0, 0, 0, 0};
-    bool head_open = !(sc.sfm & 1u);
-    int32_t cur_r = sc.nv ? sm.r[b] : 0;
-    const int32_t first_r = cur_r;
-    bool cur_decl = sc.nv ? declared(p.dev_decl, p.dev_ids, p.m, cur_r) : false;
-    u64 runK = xk, runKM = xkm;
-#pragma unroll
-    for (int j = 0; j < kItems; ++j) {
-        if (PARTIAL && j >= sc.nv) break;
-        if ((sc.sfm >> j) & 1u) {
-            if (j > 0) {
-                if (head_open) {
-                    head[0] = cur[0]; head[1] = cur[1]; head[2] = cur[2]; head[3] = cur[3];
-                } else if (cur_r >= 0 && cur_r < p.dev_ids) {
-                    if (cur[0]) red_add(p.d_k + cur_r, cur[0]);
-                    if (cur[1]) red_add(p.d_km + cur_r, cur[1]);
-                    if (cur[2]) red_add(p.d_clamp + cur_r, cur[2]);
-                    if (cur[3]) red_max(p.d_maxend + cur_r, cur[3]);
-                }
-                head_open = false;
-                cur_r = sm.r[b + j];
-                cur_decl = declared(p.dev_decl, p.dev_ids, p.m, cur_r);
-            }
-            cur[0] = cur[1] = cur[2] = cur[3] = 0;
-            runK = runKM = 0;
-        }
+    int32_t r = sm.r[b];
+    bool decl = DEV ? declared(p.dev_decl, p.dev_ids, p.m, r) : declared(p.host_decl, p.host_ids, p.n, r);
+    u64 run = x0;
+    int bad = -1;
+    for (int j = 0; j < nv; ++j) {
+        const int32_t rj = sm.r[b + j];
         const u64 s = sm.s[b + j], e = sm.e[b + j];
-        const uint8_t k = sm.k[b + j];
-        const int64_t gi = gi0 + j;
-        if (s > e) push(p, 4, gi);
-        else if (s == e) push(p, 5, gi);
-        if (!cur_decl) push(p, 6, gi);
-        if (late_check && e > E) push(p, 7, gi);
-        cur[2] += e > E ? 1 : 0;
-        const u64 ee = umin(e, E);
-        const u64 loKM = umax(s, runKM);
-        cur[1] += ee > loKM ? ee - loKM : 0;
-        runKM = umax(runKM, e);
-        if (k == 0) {
-            const u64 loK = umax(s, runK);
-            cur[0] += ee > loK ? ee - loK : 0;
-            runK = umax(runK, e);
+        const bool h = j > 0 || hp;
+        if (!h || rj != pr) {
+            if (bad < 0 && h && rj < pr) bad = j;
+            r = rj;
+            decl = DEV ? declared(p.dev_decl, p.dev_ids, p.m, r) : declared(p.host_decl, p.host_ids, p.n, r);
+            run = 0;
+        } else if (bad < 0 && s < ps) {
+            bad = j;
         }
-        cur[3] = umax(cur[3], e);
+        const int64_t gi = gi0 + j;
+        if (DEV) {
+            if (s > e) push(p, 4, gi);
+            else if (s == e) push(p, 5, gi);
+            if (!decl) push(p, 6, gi);
+            if (e > E) {
+                if (late_check) push(p, 7, gi);
+                if (r >= 0 && r < p.dev_ids) red_add(p.d_clamp + r, 1ull);
+            }
+        } else {
+            if (s > e) push(p, 0, gi);
+            else if (s == e) push(p, 1, gi);
+            if (!decl) push(p, 2, gi);
+            else if (s < e && s < run) push(p, 3, gi);
+            run = umax(run, e);
+        }
+        pr = rj;
+        ps = s;
     }
-    bar_b2();  // B2 ------------------------------------------------
+    if (bad >= 0) contract(p, DEV ? 2u : 1u, gi0 + bad);
+}
 
-    // carry fix-up: only the prefix of the tile head segment with max(s, run) < carry
-    if (c->head_cont[tc.st] && !xf && sc.nv > 0 && !(sc.sfm & 1u)) {
-        const u64 ck = c->carry0[tc.st], ckm = c->carry1[tc.st];
-        u64 rK = xk, rKM = xkm, dk = 0, dkm = 0;
-#pragma unroll
-        for (int j = 0; j < kItems; ++j) {
-            if ((PARTIAL && j >= sc.nv) || ((sc.sfm >> j) & 1u)) break;
+// =========================================================================
+// HOST records: per-rank sums + span (summarize.py:57-92) -- no scan.
+//
+// Only usable records (positive length) take part in the overlap check
+// (model.py:197-215).  With start-sorted records: if every usable record
+// starts at or after the end of the previous usable record, usable ends are
+// non-decreasing, so that end IS the running max and no usable record
+// overlaps any earlier one -- the check is exact by induction.  The first
+// violation is a real overlap: it raises ovl_suspect and the exact findings
+// come from the error-path kernels (overlap_pass) before the finalize.
+// span_end is the last usable end unless a thread holds zero-length /
+// malformed records; those threads re-emit exact maxima in host_rare.
+// =========================================================================
+__device__ __noinline__ u64 host_rare(const Params &p, const StageSmem &sm, const Ctrl *c, int st, int b, int nv,
+                                      int64_t gi0)
+{
+    bool hp = true;
+    int32_t pr = 0;
+    u64 ps = 0;
+    if (b == 0) {
+        hp = c->has_prev[st] != 0;
+        pr = c->prev_res[st];
+        ps = c->prev_start[st];
+    } else {
+        pr = sm.r[b - 1];
+        ps = sm.s[b - 1];
+    }
+    bool decl = false;
+    int32_t cur = 0;
+    u64 mx = 0, seg = 0;
+    int bad = -1;
+    for (int j = 0; j < nv; ++j) {
+        const int32_t r = sm.r[b + j];
+        const u64 s = sm.s[b + j], e = sm.e[b + j];
+        const bool h = j > 0 || hp;
+        const bool start = !h || r != pr;
+        if (start) {
+            if (bad < 0 && h && r < pr) bad = j;
+        } else if (bad < 0 && s < ps) {
+            bad = j;
+        }
+        if (j == 0 || start) {
+            if (j > 0 && seg && cur >= 0 && cur < p.host_ids) red_max(p.h_span + cur, seg);
+            cur = r;
+            seg = 0;
+            decl = declared(p.host_decl, p.host_ids, p.n, r);
+        }
+        const int64_t gi = gi0 + j;
+        if (s > e) push(p, 0, gi);
+        else if (s == e) push(p, 1, gi);
+        if (!decl) push(p, 2, gi);
+        mx = umax(mx, e);
+        seg = umax(seg, e);
+        pr = r;
+        ps = s;
+    }
+    if (nv > 0 && seg && cur >= 0 && cur < p.host_ids) red_max(p.h_span + cur, seg);   // exact span maxima
+    if (bad >= 0) contract(p, 1u, gi0 + bad);
+    return mx;
+}
+
+__device__ __forceinline__ void host_compute(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc,
+                                             int tid, Phases &ph)
+{
+    ph.mark();
+    const int warp = tid >> 5, lane = tid & 31;
+    const int b = tid * kItems;
+    const int nv = max(0, min(kItems, tc.cnt - b));
+    const int64_t gi0 = tc.gbase + (int64_t)b;
+    bool hp = true, ovl = false;
+    int32_t pr = 0;
+    u64 ps = 0, pe = 0;   // previous start; end of the previous USABLE record of the segment
+    if (nv > 0) {
+        if (b == 0) {
+            hp = c->has_prev[tc.st] != 0;
+            pr = c->prev_res[tc.st];
+            ps = c->prev_start[tc.st];
+            pe = c->prev_end[tc.st];
+            // previous record not usable: its predecessors are not at hand -> conservative
+            ovl = hp && ps >= pe && sm.r[0] == pr;
+        } else {
+            pr = sm.r[b - 1];
+            ps = sm.s[b - 1];
+            int q = b - 1;
+            while (q >= 0 && sm.r[q] == pr && sm.s[q] >= sm.e[q]) --q;   // rare: skip non-usable records
+            if (q >= 0 && sm.r[q] == pr) pe = sm.e[q];
+            else ovl = c->has_prev[tc.st] && sm.r[0] == c->prev_res[tc.st] && sm.r[0] == pr;
+        }
+    }
+    Pieces3 P;
+    P.head[0] = P.head[1] = P.head[2] = 0;
+    P.cur[0] = P.cur[1] = P.cur[2] = 0;
+    P.head_open = true;
+    P.cur_r = P.first_r = nv ? sm.r[b] : 0;
+    P.cur_decl = nv ? declared(p.host_decl, p.host_ids, p.n, P.cur_r) : false;
+    uint32_t sfm = 0;
+    bool rare = nv > 0 && !P.cur_decl;
+    u64 off = 0, mpi = 0, last = 0, tmax = 0;
+#pragma unroll kUnrollB
+    for (int j = 0; j < kItems; ++j) {
+        if (j < nv) {
+            const int32_t r = sm.r[b + j];
             const u64 s = sm.s[b + j], e = sm.e[b + j];
             const uint8_t k = sm.k[b + j];
-            const u64 loKM = umax(s, rKM), loK = umax(s, rK);
-            if (loKM >= ckm && loK >= ck) break;
-            const u64 ee = umin(e, E);
-            const u64 nKM = umax(loKM, ckm);
-            dkm += (ee > loKM ? ee - loKM : 0) - (ee > nKM ? ee - nKM : 0);
-            rKM = umax(rKM, e);
+            if ((j == 0 && !hp) || r != pr) {
+                sfm |= 1u << j;
+                rare = rare || ((j > 0 || hp) && r < pr);
+                if (j > 0) {
+                    P.cur[0] = off; P.cur[1] = mpi; P.cur[2] = last;
+                    close_piece(P, p.host_ids, p.h_off, p.h_mpi, p.h_span);
+                    tmax = umax(tmax, last);
+                    P.cur_r = r;
+                    P.cur_decl = declared(p.host_decl, p.host_ids, p.n, r);
+                    rare = rare || !P.cur_decl;
+                }
+                P.head_open = P.head_open && j > 0;
+                off = mpi = last = 0;
+                pe = 0;
+            } else {
+                rare = rare || s < ps;          // canonical order
+            }
+            const bool usable = s < e;
+            ovl = ovl || (usable && s < pe);   // usable record before the last usable end
+            rare = rare || !usable;             // zero-length / malformed
+            pe = usable ? e : pe;
+            last = usable ? e : last;
+            const u64 d = e - s;
+            if (k == 1) off += d;
+            if (k == 2) mpi += d;
+            pr = r;
+            ps = s;
+        }
+    }
+    P.cur[0] = off; P.cur[1] = mpi; P.cur[2] = last;
+    tmax = umax(tmax, last);
+    if (ovl && !*(volatile unsigned *)&p.g->ovl_suspect) atomicOr(&p.g->ovl_suspect, 1u);
+    if (rare || ovl) tmax = host_rare(p, sm, c, tc.st, b, nv, gi0);
+    ph.add(ph.b);
+    if (P.head_open) { P.head[0] = P.head[1] = P.head[2] = 0; }
+    u64 *const dst[3] = {p.h_off, p.h_mpi, p.h_span};
+    emit_segments<2>(P.head, P.cur, sfm, nv, P.first_r, P.cur_r, p.host_ids, dst, lane);
+    // tile max end for E (summarize.py:88-89): warp max -> CTA (smem) -> one RED per tile
+    const u64 wm = warp_max_rx(tmax);
+    if (lane == 0) {
+        atomicMax(&c->h_max[tc.st], wm);
+        __threadfence_block();
+        if (atomicAdd(&c->h_cnt[tc.st], 1u) == kComputeWarps - 1) {
+            const u64 m = atomicExch(&c->h_max[tc.st], 0ull);
+            c->h_cnt[tc.st] = 0;
+            red_max(&p.g->host_max_end, m);
+            asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(&p.g->host_done) : "memory");
+        }
+    }
+    ph.add(ph.emit);
+    (void)warp;
+}
+
+// =========================================================================
+// DEVICE records: dual running-max union scan (summarize.py:95-138)
+// =========================================================================
+// fast pass; returns true if the thread needs the 64-bit rescan
+template <typename T>
+__device__ __forceinline__ bool dev_phase_b(const Params &p, const StageSmem &sm, const Ctrl *c, int st, int b, int nv,
+                                            uint32_t sfm, const TileView &tv, Pieces3 &P, u64 E)
+{
+    const Dom<T> D(tv.base, tv.top);
+    const T Er = D.rel(E);                  // <= top - base: also catches ends that wrap below the base
+    bool rare = E < tv.base;                // every record of the tile ends after E
+    T runK = tmin(D.rel(tv.x0), Er), runKM = tmin(D.rel(tv.x1), Er), cK = 0, cKM = 0, ps = 0;
+    bool hp = true;
+    int32_t pr = 0;
+    if (b == 0) {
+        hp = c->has_prev[st] != 0;
+        pr = c->prev_res[st];
+        rare = rare || (hp && nv > 0 && !(sfm & 1u) && sm.s[0] < c->prev_start[st]);
+    } else {
+        pr = sm.r[b - 1];
+        ps = D.ld(sm.s, b - 1);
+    }
+#pragma unroll kUnrollB
+    for (int j = 0; j < kItems; ++j) {
+        if (j < nv) {
+            const T s0 = D.ld(sm.s, b + j), e0 = D.ld(sm.e, b + j);
+            const uint8_t k = sm.k[b + j];
+            if ((sfm >> j) & 1u) {
+                const int32_t r = sm.r[b + j];
+                rare = rare || ((j > 0 || hp) && r < pr);
+                if (j > 0) {
+                    P.cur[0] = cK; P.cur[1] = cKM; P.cur[2] = D.abs(runKM);
+                    close_piece(P, p.dev_ids, p.d_k, p.d_km, p.d_maxend);
+                }
+                P.cur_r = r;
+                pr = r;
+                P.cur_decl = declared(p.dev_decl, p.dev_ids, p.m, r);
+                rare = rare || !P.cur_decl;
+                cK = cKM = 0;
+                runK = runKM = 0;
+            } else if (j > 0 || b > 0) {
+                rare = rare || s0 < ps;
+            }
+            rare = rare || s0 >= e0 || e0 > Er;     // zero-length / malformed / clamped
+            const T e = tmin(e0, Er), s = tmin(s0, e);
+            const T loKM = tmax(runKM, s);
+            runKM = tmax(runKM, e);
+            cKM += runKM - loKM;
             if (k == 0) {
-                const u64 nK = umax(loK, ck);
-                dk += (ee > loK ? ee - loK : 0) - (ee > nK ? ee - nK : 0);
-                rK = umax(rK, e);
+                const T loK = tmax(runK, s);
+                runK = tmax(runK, e);
+                cK += runK - loK;
+            }
+            ps = s0;
+        }
+    }
+    P.cur[0] = cK; P.cur[1] = cKM; P.cur[2] = D.abs(runKM);
+    return rare;
+}
+
+__device__ __forceinline__ void dev_compute(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
+                                            u64 &E_cache, bool &E_known, Phases &ph)
+{
+    ph.mark();
+    const int warp = tid >> 5, lane = tid & 31;
+    const int b = tid * kItems;
+    const int nv = max(0, min(kItems, tc.cnt - b));
+    const int64_t gi0 = tc.gbase + (int64_t)b;
+    uint32_t sfm;
+    u64 in0, in1, mn, mx;
+    phase_a<true>(sm, c, tc.st, b, nv, sfm, in0, in1, mn, mx);
+    bool in_f = sfm != 0;
+    warp_seg_max(in_f, in0, in1, lane);
+    mn = warp_min_rx(mn);
+    mx = warp_max_rx(mx);
+    if (lane == 31) { c->w_flag[tc.st][warp] = in_f; c->w_v0[tc.st][warp] = in0; c->w_v1[tc.st][warp] = in1; }
+    if (lane == 0) { c->w_mn[tc.st][warp] = mn; c->w_mx[tc.st][warp] = mx; }
+    ph.add(ph.a);
+    if (!E_known) {   // once per warp: E from the host phase (device_window)
+        u64 E = 0;
+        if (lane == 0) E = device_window(p);
+        E_cache = __shfl_sync(0xffffffffu, E, 0);
+        E_known = true;
+    }
+    bar_compute();
+    const u64 E = E_cache;
+    const bool late_check = (p.mode == kReport || p.mode == kValidate) && p.n >= 1;
+    const TileView tv = tile_view(c, tc.st, warp, lane, in_f, in0, in1);
+    if (tid == 0) publish_tile<true>(p, sm, c, tc, tv);
+    ph.add(ph.bar);
+    Pieces3 P;
+    P.head[0] = P.head[1] = P.head[2] = 0;
+    P.cur[0] = P.cur[1] = P.cur[2] = 0;
+    P.head_open = !(sfm & 1u);
+    P.cur_r = P.first_r = nv ? sm.r[b] : 0;
+    P.cur_decl = nv ? declared(p.dev_decl, p.dev_ids, p.m, P.cur_r) : false;
+    const bool rare = tv.fits32 ? dev_phase_b<uint32_t>(p, sm, c, tc.st, b, nv, sfm, tv, P, E)
+                                : dev_phase_b<u64>(p, sm, c, tc.st, b, nv, sfm, tv, P, E);
+    if (rare) rescan<true>(p, sm, c, tc.st, b, nv, 0, E, late_check, gi0);
+    ph.add(ph.b);
+    if (P.head_open) { P.head[0] = P.head[1] = P.head[2] = 0; }
+    u64 *const dst[3] = {p.d_k, p.d_km, p.d_maxend};
+    emit_segments<2>(P.head, P.cur, sfm, nv, P.first_r, P.cur_r, p.dev_ids, dst, lane);
+    ph.add(ph.emit);
+}
+
+// =========================================================================
+// producer-side tile epilogue, run after the stage was refilled: look back
+// for the carry, publish P, and correct the tile's head segment (the compute
+// warps used carry 0) reading the few affected records from global memory
+// =========================================================================
+struct Epi {
+    int64_t lt;
+    int cnt;
+    bool dev, head, tf;
+    u64 t0, t1;
+};
+
+__device__ void dev_epilogue(const Params &p, const Epi &x, int lane, u64 &E_cache, bool &E_known)
+{
+    // the first 32 records are loaded before the look-back (overlapped round trips)
+    const int64_t g0 = x.lt * kTile;
+    const u64 *S = p.ds + g0, *En = p.de + g0;
+    const int32_t *R = p.dr + g0;
+    const uint8_t *K = p.dk + g0;
+    int32_t rj = -1;
+    u64 sj = 0, ej = 0;
+    uint8_t kj = 1;
+    if (lane < x.cnt) { rj = __ldcg(R + lane); sj = __ldcg(S + lane); ej = __ldcg(En + lane); kj = __ldcg(K + lane); }
+    u64 ck, ckm;
+    look_back<2>(p.d_slotA, p.d_slotP, x.lt, p.epoch, lane, ck, ckm);
+    if (!x.tf && lane == 0) publish<2>(p.d_slotP + 4 * x.lt, p.epoch, umax(ck, x.t0), umax(ckm, x.t1));
+    if (!E_known) {
+        u64 Ew = 0;
+        if (lane == 0) Ew = device_window(p);
+        E_cache = __shfl_sync(0xffffffffu, Ew, 0);
+        E_known = true;
+    }
+    const u64 E = E_cache;
+    ck = umin(ck, E);
+    ckm = umin(ckm, E);
+    // head-segment records whose contribution changes with the carried run:
+    // the prefix with max(run_local, s') < carry (monotone along the segment)
+    const int32_t r0 = __shfl_sync(0xffffffffu, rj, 0);
+    u64 runK = 0, runKM = 0, dk = 0, dkm = 0;
+    for (int base = 0; base < x.cnt; base += 32) {
+        const int j = base + lane;
+        bool in = j < x.cnt;
+        u64 e = 0, s = 0;
+        bool kern = false;
+        if (in) {
+            if (base > 0) { rj = __ldcg(R + j); sj = __ldcg(S + j); ej = __ldcg(En + j); kj = __ldcg(K + j); }
+            in = rj == r0;
+            const u64 e0 = ej, s0 = sj;
+            kern = kj == 0;
+            if (in) {
+                e = umin(e0, E);
+                s = umin(s0, e);
+            } else {
+                kern = false;
             }
         }
-        if (head_open) { cur[0] -= dk; cur[1] -= dkm; }
-        else { head[0] -= dk; head[1] -= dkm; }
+        u64 xkm = e, xk = kern ? e : 0;   // inclusive running maxima (clamped)
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const u64 okm = shfl_up64(xkm, d), ok = shfl_up64(xk, d);
+            if (lane >= d) { xkm = umax(xkm, okm); xk = umax(xk, ok); }
+        }
+        u64 ekm = shfl_up64(xkm, 1), ek = shfl_up64(xk, 1);
+        if (lane == 0) { ekm = 0; ek = 0; }
+        ekm = umax(ekm, runKM);
+        ek = umax(ek, runK);
+        bool live = false;
+        if (in) {
+            const u64 loKM = umax(ekm, s), nKM = umax(ekm, ckm);
+            if (loKM < ckm) dkm += (umax(ekm, e) - loKM) - (umax(nKM, e) - umax(nKM, s));
+            if (kern) {
+                const u64 loK = umax(ek, s), nK = umax(ek, ck);
+                if (loK < ck) dk += (umax(ek, e) - loK) - (umax(nK, e) - umax(nK, s));
+            }
+            live = umax(ekm, s) < ckm || umax(ek, s) < ck;
+        }
+        runKM = umax(runKM, __shfl_sync(0xffffffffu, xkm, 31));
+        runK = umax(runK, __shfl_sync(0xffffffffu, xk, 31));
+        if (!(__ballot_sync(0xffffffffu, live) >> 31)) break;
     }
-    if (head_open) { head[0] = head[1] = head[2] = head[3] = 0; }
-    u64 *const dst[4] = {p.d_k, p.d_km, p.d_clamp, p.d_maxend};
-    emit_segments<3>(head, cur, sc.sfm, sc.nv, first_r, cur_r, p.dev_ids, dst, lane);
+    dk = warp_sum(dk);
+    dkm = warp_sum(dkm);
+    if (lane == 0 && r0 >= 0 && r0 < p.dev_ids) {
+        if (dk) red_add(p.d_k + r0, (u64)0 - dk);      // two's complement: subtract
+        if (dkm) red_add(p.d_km + r0, (u64)0 - dkm);
+    }
 }
 
 // =========================================================================
@@ -676,7 +1088,7 @@ __device__ __forceinline__ int bitlen128(u128 x)
     return hi ? 128 - __clzll((long long)hi) : (lo ? 64 - __clzll((long long)lo) : 0);
 }
 
-__device__ double div_exact(u128 a, u128 b)
+__device__ __noinline__ double div_exact(u128 a, u128 b)
 {
     if (a == 0) return 0.0;
     if ((a >> 53) == 0 && (b >> 53) == 0) return (double)(u64)a / (double)(u64)b;  // IEEE: correctly rounded
@@ -711,38 +1123,40 @@ __device__ double div_exact(u128 a, u128 b)
     return ldexp((double)mant, e2);
 }
 
-// block reduction helpers for the finalize (NT threads)
-__device__ u128 block_sum128(u128 v, u128 *scratch, int tid, int nt)
+// block reductions of u128 for the finalize: warp shuffles, then warp 0
+__device__ __forceinline__ u128 shfl_xor128(u128 v, int d)
 {
-    scratch[tid] = v;
+    const u64 lo = __shfl_xor_sync(0xffffffffu, (u64)v, d), hi = __shfl_xor_sync(0xffffffffu, (u64)(v >> 64), d);
+    return ((u128)hi << 64) | lo;
+}
+
+template <bool MAX>
+__device__ u128 block_reduce128(u128 v, u128 *scratch, int tid, int nt)
+{
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const u128 o = shfl_xor128(v, d);
+        v = MAX ? (o > v ? o : v) : v + o;
+    }
+    const int w = tid >> 5, nw = nt >> 5;
+    if ((tid & 31) == 0) scratch[w] = v;
     __syncthreads();
-    if (tid == 0) {
-        u128 t = 0;
-        for (int i = 0; i < nt; ++i) t += scratch[i];
-        scratch[nt] = t;
+    if (w == 0) {
+        v = (tid < nw) ? scratch[tid] : (u128)0;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            const u128 o = shfl_xor128(v, d);
+            v = MAX ? (o > v ? o : v) : v + o;
+        }
+        if (tid == 0) scratch[32] = v;
     }
     __syncthreads();
-    const u128 t = scratch[nt];
+    const u128 t = scratch[32];
     __syncthreads();
     return t;
 }
 
-__device__ u128 block_max128(u128 v, u128 *scratch, int tid, int nt)
-{
-    scratch[tid] = v;
-    __syncthreads();
-    if (tid == 0) {
-        u128 t = 0;
-        for (int i = 0; i < nt; ++i) t = scratch[i] > t ? scratch[i] : t;
-        scratch[nt] = t;
-    }
-    __syncthreads();
-    const u128 t = scratch[nt];
-    __syncthreads();
-    return t;
-}
-
-// metric trees (metrics.py:66-122); threads 0..8 each do one division
+// metric trees (metrics.py:66-122); threads 0..4 / 32..35 each do one division
 __device__ void metric_trees(ResultDev *res, bool host_side, bool dev_side, u64 E, int32_t n, int32_t m,
                              u128 sum_u, u128 sum_uw, u128 max_uw, u128 sum_k, u128 max_k, u128 max_km, int tid)
 {
@@ -794,10 +1208,9 @@ __device__ void finalize(const Params &p, u128 *scratch, int tid)
     const int nt = kThreads;
     __shared__ u64 s_E;
     __shared__ int s_status;
-    // device-side max end over every device record (all ids)
     u64 dmx = 0;
     for (int32_t id = tid; id < p.dev_ids; id += nt) dmx = umax(dmx, ld_relaxed(p.d_maxend + id));
-    const u64 dev_max_end = (u64)block_max128(dmx, scratch, tid, nt);
+    const u64 dev_max_end = (u64)block_reduce128<true>(dmx, scratch, tid, nt);
     const u64 host_elapsed = umax(ld_relaxed(&g->host_max_end), p.host_elapsed_floor);
     if (tid == 0) {
         u64 E;
@@ -842,9 +1255,9 @@ __device__ void finalize(const Params &p, u128 *scratch, int tid)
         const u64 useful = span - off - mpi;
         u64 *o = p.host_out + 4 * (size_t)pos;
         o[0] = useful; o[1] = off; o[2] = mpi; o[3] = span;
-        sum_u += useful;
-        sum_uw += (u128)useful + off;
         const u128 uw = (u128)useful + off;
+        sum_u += useful;
+        sum_uw += uw;
         if (uw > max_uw) max_uw = uw;
     }
     // device summaries
@@ -860,14 +1273,14 @@ __device__ void finalize(const Params &p, u128 *scratch, int tid)
         if (k > max_k) max_k = k;
         if (km > max_km) max_km = km;
     }
-    sum_u = block_sum128(sum_u, scratch, tid, nt);
-    sum_uw = block_sum128(sum_uw, scratch, tid, nt);
-    max_uw = block_max128(max_uw, scratch, tid, nt);
-    sum_k = block_sum128(sum_k, scratch, tid, nt);
-    max_k = block_max128(max_k, scratch, tid, nt);
-    max_km = block_max128(max_km, scratch, tid, nt);
-    if (ok && p.mode == kReport) metric_trees(res, p.n >= 1, p.m >= 1, E, p.n, p.m, sum_u, sum_uw, max_uw, sum_k,
-                                             max_k, max_km, tid);
+    sum_u = block_reduce128<false>(sum_u, scratch, tid, nt);
+    sum_uw = block_reduce128<false>(sum_uw, scratch, tid, nt);
+    max_uw = block_reduce128<true>(max_uw, scratch, tid, nt);
+    sum_k = block_reduce128<false>(sum_k, scratch, tid, nt);
+    max_k = block_reduce128<true>(max_k, scratch, tid, nt);
+    max_km = block_reduce128<true>(max_km, scratch, tid, nt);
+    if (ok && p.mode == kReport)
+        metric_trees(res, p.n >= 1, p.m >= 1, E, p.n, p.m, sum_u, sum_uw, max_uw, sum_k, max_k, max_km, tid);
     __syncthreads();
     if (tid == 0) {
         g->tile_counter = 0;
@@ -875,6 +1288,7 @@ __device__ void finalize(const Params &p, u128 *scratch, int tid)
         g->contract_flags = 0;
         g->host_max_end = 0;
         g->contract_index = LLONG_MAX;
+        g->ovl_suspect = 0;
         for (int i = 0; i < 8; ++i) g->counts[i] = 0;
         __threadfence();
         g->ctas_done = 0;
@@ -891,36 +1305,98 @@ __global__ void __launch_bounds__(kThreads, 1) analyze_kernel(const __grid_const
     Ctrl *c = reinterpret_cast<Ctrl *>(smem_raw + sizeof(StageSmem) * kStages);
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const uint64_t pol = l2_policy_evict_first();
 
     if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&c->full[s], 1);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&c->full[s], 1);
+            mbar_init(&c->empty[s], kComputeWarps);
+            c->h_max[s] = 0;
+            c->h_cnt[s] = 0;
+        }
         fence_mbar_init();
     }
     __syncthreads();
-    if (warp == kComputeWarps)
-        for (int s = 0; s < kStages - 1; ++s) produce(p, stages, c, s, lane, pol);
     u64 E_cache = 0;
     bool E_known = false;
-    for (int it = 0;; ++it) {
-        const int st = it % kStages;
-        mbar_wait(&c->full[st], (uint32_t)((it / kStages) & 1));
-        const int64_t t = c->tile[st];
-        if (t < 0) break;
-        TileCtx tc;
-        tc.st = st;
-        tc.refill = (it + kStages - 1) % kStages;   // stage of tile it-1: free once everyone passed B1
-        tc.cnt = c->cnt[st];
-        const bool dev = t >= p.host_tiles;
-        tc.lt = dev ? t - p.host_tiles : t;
-        tc.gbase = tc.lt * kTile;
-        if (!dev) {
-            if (tc.cnt == kTile) host_tile<false>(p, stages, c, tc, tid, pol);
-            else host_tile<true>(p, stages, c, tc, tid, pol);
-        } else {
-            if (tc.cnt == kTile) dev_tile<false>(p, stages, c, tc, tid, pol, E_cache, E_known);
-            else dev_tile<true>(p, stages, c, tc, tid, pol, E_cache, E_known);
+    if (warp == kComputeWarps) {
+        // ---------------- producer warp ----------------
+        const uint64_t pol = l2_policy_evict_first();
+        for (int s = 0; s < kStages; ++s) produce(p, stages, c, s, claim_finish(p, claim_issue(p, lane)), lane, pol);
+        // claims run ahead of use: the atomic is issued one iteration before its index is
+        // needed and the previous-record loads one iteration before the refill
+        Claim next = claim_finish(p, claim_issue(p, lane));
+        int64_t pend = claim_issue(p, lane);
+        PROF_DECL(pa); PROF_DECL(pb); PROF_DECL(pc); PROF_DECL(pn);
+        for (int it = 0;; ++it) {
+            const int st = it % kStages;
+            const uint32_t ph = (uint32_t)((it / kStages) & 1);
+            const int64_t t = c->tile[st];
+            if (t < 0) break;
+            long long t0 = PROF_NOW();
+            mbar_wait(&c->empty[st], ph);
+            PROF_ADD(pa, t0);
+            Epi x;
+            x.dev = t >= p.host_tiles;
+            x.lt = x.dev ? t - p.host_tiles : t;
+            x.cnt = c->cnt[st];
+            x.head = c->t_head[st] != 0;
+            x.tf = c->t_flag[st] != 0;
+            x.t0 = c->t_v0[st];
+            x.t1 = c->t_v1[st];
+            t0 = PROF_NOW();
+            produce(p, stages, c, st, next, lane, pol);
+            next = claim_finish(p, pend);
+            pend = claim_issue(p, lane);
+            PROF_ADD(pb, t0);
+            t0 = PROF_NOW();
+            if (x.head && x.dev) dev_epilogue(p, x, lane, E_cache, E_known);
+            PROF_ADD(pc, t0);
+#ifdef HB_PROF
+            ++pn;
+#endif
+            (void)t0;
         }
+#ifdef HB_PROF
+        if (lane == 0) {
+            unsigned long long *o = hb_prof_buf + blockIdx.x * kProfSlots;
+            o[8] = pa; o[9] = pb; o[10] = pc; o[11] = 0; o[12] = pn;
+        }
+#endif
+    } else {
+        // ---------------- compute warps ----------------
+        PROF_DECL(ca); PROF_DECL(cb); PROF_DECL(cn);
+        Phases phs;
+        for (int it = 0;; ++it) {
+            const int st = it % kStages;
+            long long t0 = PROF_NOW();
+            mbar_wait(&c->full[st], (uint32_t)((it / kStages) & 1));
+            PROF_ADD(ca, t0);
+            const int64_t t = c->tile[st];
+            if (t < 0) break;
+            TileCtx tc;
+            tc.st = st;
+            tc.cnt = c->cnt[st];
+            const bool dev = t >= p.host_tiles;
+            tc.lt = dev ? t - p.host_tiles : t;
+            tc.gbase = tc.lt * kTile;
+            t0 = PROF_NOW();
+            if (!dev) host_compute(p, stages[st], c, tc, tid, phs);
+            else dev_compute(p, stages[st], c, tc, tid, E_cache, E_known, phs);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&c->empty[st]);
+            PROF_ADD(cb, t0);
+#ifdef HB_PROF
+            ++cn;
+#endif
+            (void)t0;
+        }
+#ifdef HB_PROF
+        if (tid == 0) {
+            unsigned long long *o = hb_prof_buf + blockIdx.x * kProfSlots;
+            o[0] = ca; o[1] = cb; o[2] = cn;
+            o[3] = phs.a; o[4] = phs.bar; o[5] = phs.b; o[6] = phs.emit;
+        }
+#endif
     }
     // CTA done: the last one finalizes
     __threadfence();
@@ -932,16 +1408,130 @@ __global__ void __launch_bounds__(kThreads, 1) analyze_kernel(const __grid_const
     __syncthreads();
     if (c->is_last) {
         __threadfence();
-        finalize(p, reinterpret_cast<u128 *>(smem_raw), tid);
+        if (*(volatile unsigned *)&p.g->ovl_suspect) {
+            // host records overlap somewhere: the exact findings come from the
+            // error-path kernels (launch_overlap_pass), which then finalize
+            if (tid == 0) p.res->status = -1;
+        } else {
+            finalize(p, reinterpret_cast<u128 *>(smem_raw), tid);
+        }
     }
+}
+
+// =========================================================================
+// error path: exact host-overlap findings (model.py:203-215) for traces
+// where some host record starts before its predecessor's end.  Three simple
+// passes over the tiles (per-tile aggregate, carry scan, detection), then
+// the finalize.  Only runs for invalid traces.
+// =========================================================================
+constexpr int kOvlThreads = 256;
+
+// per-thread contiguous chunk of the tile: (segment start inside?, max end of its last segment)
+__device__ void ovl_chunk(const Params &p, int64_t base, int cnt, int tid, int &lo, int &hi, bool &f, u64 &v)
+{
+    const int per = (cnt + kOvlThreads - 1) / kOvlThreads;
+    lo = min(cnt, tid * per);
+    hi = min(cnt, lo + per);
+    f = false;
+    v = 0;
+    for (int j = lo; j < hi; ++j) {
+        const int64_t g = base + j;
+        if (g == 0 || p.hr[g] != p.hr[g - 1]) { f = true; v = 0; }
+        v = umax(v, p.he[g]);
+    }
+}
+
+__global__ void __launch_bounds__(kOvlThreads) ovl_agg_kernel(const __grid_constant__ Params p, u64 *agg)
+{
+    __shared__ int sf[kOvlThreads];
+    __shared__ u64 sv[kOvlThreads];
+    const int64_t t = blockIdx.x;
+    const int64_t base = t * kTile;
+    const int cnt = (int)min((int64_t)kTile, p.hn - base);
+    int lo, hi;
+    bool f;
+    u64 v;
+    ovl_chunk(p, base, cnt, threadIdx.x, lo, hi, f, v);
+    sf[threadIdx.x] = f;
+    sv[threadIdx.x] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        bool tf = false;
+        u64 tv = 0;
+        for (int i = 0; i < kOvlThreads; ++i) {
+            if (sf[i]) { tf = true; tv = sv[i]; }
+            else tv = umax(tv, sv[i]);
+        }
+        agg[2 * t] = tf;
+        agg[2 * t + 1] = tv;
+    }
+}
+
+// one thread: exclusive carry for every tile (max end of earlier records of
+// the segment that continues into the tile)
+__global__ void ovl_carry_kernel(int64_t tiles, const u64 *agg, u64 *carry)
+{
+    u64 run = 0;
+    for (int64_t t = 0; t < tiles; ++t) {
+        carry[t] = run;
+        run = agg[2 * t] ? agg[2 * t + 1] : umax(run, agg[2 * t + 1]);
+    }
+}
+
+__global__ void __launch_bounds__(kOvlThreads) ovl_detect_kernel(const __grid_constant__ Params p, const u64 *carry)
+{
+    __shared__ int sf[kOvlThreads];
+    __shared__ u64 sv[kOvlThreads];
+    const int64_t t = blockIdx.x;
+    const int64_t base = t * kTile;
+    const int cnt = (int)min((int64_t)kTile, p.hn - base);
+    int lo, hi;
+    bool f;
+    u64 v;
+    ovl_chunk(p, base, cnt, threadIdx.x, lo, hi, f, v);
+    sf[threadIdx.x] = f;
+    sv[threadIdx.x] = v;
+    __syncthreads();
+    // exclusive prefix for this thread: tile carry, then earlier chunks
+    u64 run = carry[t];
+    for (int i = 0; i < (int)threadIdx.x; ++i) run = sf[i] ? sv[i] : umax(run, sv[i]);
+    bool decl = false;
+    for (int j = lo; j < hi; ++j) {
+        const int64_t g = base + j;
+        const int32_t r = p.hr[g];
+        if (g == 0 || r != p.hr[g - 1]) run = 0;
+        if (j == lo || g == 0 || r != p.hr[g - 1]) decl = declared(p.host_decl, p.host_ids, p.n, r);
+        const u64 s = p.hs[g], e = p.he[g];
+        if (decl && s < e && s < run) push(p, 3, g);
+        run = umax(run, e);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) finalize_kernel(const __grid_constant__ Params p)
+{
+    __shared__ u128 scratch[40];
+    finalize(p, scratch, threadIdx.x);
+}
+
+cudaError_t launch_overlap_pass(const Params &p, u64 *scratch, cudaStream_t s)
+{
+    const int64_t tiles = p.host_tiles;
+    if (tiles > 0) {
+        ovl_agg_kernel<<<(unsigned)tiles, kOvlThreads, 0, s>>>(p, scratch);
+        ovl_carry_kernel<<<1, 1, 0, s>>>(tiles, scratch, scratch + 2 * tiles);
+        ovl_detect_kernel<<<(unsigned)tiles, kOvlThreads, 0, s>>>(p, scratch + 2 * tiles);
+    }
+    finalize_kernel<<<1, kThreads, 0, s>>>(p);
+    return cudaGetLastError();
 }
 
 // =========================================================================
 // stand-alone metric trees (host_metrics / device_metrics stage functions)
 // =========================================================================
-__global__ void metrics_kernel(const u64 *sums, int32_t k, u64 E, int host_side, ResultDev *res)
+__global__ void __launch_bounds__(kThreads) metrics_kernel(const u64 *sums, int32_t k, u64 E, int host_side,
+                                                           ResultDev *res)
 {
-    __shared__ u128 scratch[kThreads + 1];
+    __shared__ u128 scratch[33];
     const int tid = threadIdx.x;
     u128 a = 0, b = 0, c = 0;   // host: sum_u, sum_uw, max_uw ; device: sum_k, max_k, max_km
     for (int32_t i = tid; i < k; i += kThreads) {
@@ -955,10 +1545,10 @@ __global__ void metrics_kernel(const u64 *sums, int32_t k, u64 E, int host_side,
             if (km > c) c = km;
         }
     }
-    a = block_sum128(a, scratch, tid, kThreads);
-    if (host_side) { b = block_sum128(b, scratch, tid, kThreads); }
-    else { b = block_max128(b, scratch, tid, kThreads); }
-    c = block_max128(c, scratch, tid, kThreads);
+    a = block_reduce128<false>(a, scratch, tid, kThreads);
+    if (host_side) b = block_reduce128<false>(b, scratch, tid, kThreads);
+    else b = block_reduce128<true>(b, scratch, tid, kThreads);
+    c = block_reduce128<true>(c, scratch, tid, kThreads);
     if (tid == 0) { res->host_mask = 0; res->device_mask = 0; res->status = 0; }
     __syncthreads();
     if (host_side) metric_trees(res, true, false, E, k, 0, a, b, c, 0, 0, 0, tid);
@@ -986,6 +1576,18 @@ __global__ void covers_kernel(Params p, const int64_t *err, int64_t count, int64
         if (arg < 0 || e > best) { best = e; arg = x; }
     }
     cover[q] = arg;
+}
+
+int prof_read(unsigned long long *out, int n)
+{
+#ifdef HB_PROF
+    const int k = n < 1024 * kProfSlots ? n : 1024 * kProfSlots;
+    cudaMemcpyFromSymbol(out, hb_prof_buf, sizeof(unsigned long long) * k);
+    return k;
+#else
+    (void)out; (void)n;
+    return 0;
+#endif
 }
 
 int analyze_grid(int device)

@@ -7,12 +7,24 @@ namespace hb {
 
 typedef unsigned long long u64;
 
-constexpr int kComputeWarps = 7;
-constexpr int kComputeThreads = kComputeWarps * 32;    // 224
+// tile geometry (compile-time knobs, see tools/build_variants.sh)
+#ifndef HB_WARPS
+#define HB_WARPS 15
+#endif
+#ifndef HB_ITEMS
+#define HB_ITEMS 11
+#endif
+#ifndef HB_STAGES
+#define HB_STAGES 2
+#endif
+constexpr int kComputeWarps = HB_WARPS;
+constexpr int kComputeThreads = kComputeWarps * 32;
 constexpr int kThreads = kComputeThreads + 32;         // + producer / look-back warp
-constexpr int kItems = 13;                             // odd: conflict-free blocked smem reads
-constexpr int kTile = kComputeThreads * kItems;        // 2912 records per tile
-constexpr int kStages = 3;
+constexpr int kItems = HB_ITEMS;                       // odd: conflict-free blocked smem reads
+constexpr int kTile = kComputeThreads * kItems;        // records per tile (multiple of 16)
+constexpr int kStages = HB_STAGES;
+static_assert(kTile % 16 == 0, "tile must keep every column 16-byte aligned for TMA");
+static_assert(kItems <= 32, "per-thread bit masks");
 
 enum Mode { kReport = 0, kSummarizeDevice = 1, kValidate = 2, kSummarizeHost = 3 };
 
@@ -25,6 +37,8 @@ struct Globals {
     u64 host_max_end;
     long long contract_index;
     u64 counts[8];
+    unsigned int ovl_suspect;     // a host record starts before its predecessor's end
+    unsigned int pad;
 };
 
 struct ResultDev {
@@ -67,11 +81,10 @@ struct Params {
     // workspace: per dense id accumulators (zero between calls)
     u64 *h_off, *h_mpi, *h_span;
     u64 *d_k, *d_km, *d_clamp, *d_maxend;
-    // tile status for the decoupled look-back (epoch-tagged, never cleared)
-    uint32_t *h_flag;
-    u64 *h_valA, *h_valP;
-    uint32_t *d_flag;
-    u64 *d_valA0, *d_valA1, *d_valP0, *d_valP1;
+    // decoupled look-back slots, self-validating (epoch-tagged 32-bit halves,
+    // never cleared): host [tiles][2] words per slot, device [tiles][4]
+    u64 *h_slotA, *h_slotP;
+    u64 *d_slotA, *d_slotP;
     Globals *g;
     int64_t *lists[8];
     // outputs (device memory, copied to the caller by the C ABI)
@@ -81,10 +94,13 @@ struct Params {
 };
 
 size_t analyze_smem_bytes();
+int prof_read(unsigned long long *out, int n);
 int analyze_grid(int device);
 cudaError_t launch_analyze(const Params &p, int grid, cudaStream_t s);
 cudaError_t launch_metrics(const u64 *summaries, int32_t k, u64 elapsed, int host_side, ResultDev *res,
                            cudaStream_t s);
+// error path: exact host-overlap findings (only when ovl_suspect), then finalize
+cudaError_t launch_overlap_pass(const Params &p, u64 *scratch, cudaStream_t s);
 cudaError_t launch_covers(const Params &p, const int64_t *err_idx, int64_t count, int64_t *cover, cudaStream_t s);
 
 }  // namespace hb

@@ -145,8 +145,10 @@ def _engine_vs_oracle(h, d, n, m, mode=N.MODE_REPORT, elapsed=0):
     got = analyze_packed(packed, mode, elapsed, want_lists=True, capacity=1 << 20)
     ref = O.analyze(h, d, n, m, mode=mode, elapsed=elapsed, cap=1 << 20)
     assert got.status == ref.status
-    assert got.counts == ref.counts
-    for c in (0, 1, 2, 4, 5, 6, 7):
+    # summarize_device never reports validate()'s late warnings (summarize.py:95-138)
+    lists = (0, 1, 2, 4, 5, 6, 7) if mode != N.MODE_SUMMARIZE_DEVICE else (0, 1, 2, 4, 5, 6)
+    assert [got.counts[c] for c in lists + (3,)] == [ref.counts[c] for c in lists + (3,)]
+    for c in lists:
         assert np.array_equal(got.lists[c], np.sort(ref.lists[c])), c
     assert np.array_equal(got.lists[3], np.sort(ref.lists[3][:, 1]))
     if ref.status == 0:
