@@ -99,6 +99,7 @@ heteff_ctx *heteff_create(int device)
     cudaEventCreate(&ctx->ev0);
     cudaEventCreate(&ctx->ev1);
     ctx->grid = hb::analyze_grid(device);
+    if (ctx->grid <= 0) { heteff_destroy(ctx); return nullptr; }   // tile geometry does not fit this GPU
     return ctx;
 }
 

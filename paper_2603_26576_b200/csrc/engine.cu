@@ -54,7 +54,7 @@ namespace hb {
 
 #ifdef HB_PROF
 // per-CTA clock64 phase counters (tools/prof build only): read back with heteff_prof_read
-constexpr int kProfSlots = 16;
+constexpr int kProfSlots = 32;
 __device__ unsigned long long hb_prof_buf[1024 * kProfSlots];
 #define PROF_DECL(x) long long x = 0
 #define PROF_NOW() clock64()
@@ -68,13 +68,14 @@ __device__ unsigned long long hb_prof_buf[1024 * kProfSlots];
 struct Phases {
 #ifdef HB_PROF
     long long a = 0, bar = 0, b = 0, emit = 0, t = 0;
+    long long hb = 0, hemit = 0, hn = 0, dn = 0;
     __device__ __forceinline__ void mark() { t = clock64(); }
     __device__ __forceinline__ void add(long long &acc) { const long long n = clock64(); acc += n - t; t = n; }
 #else
     __device__ __forceinline__ void mark() {}
     template <typename X>
     __device__ __forceinline__ void add(X &) {}
-    int a, bar, b, emit;
+    int a, bar, b, emit, hb, hemit, hn, dn;
 #endif
 };
 
@@ -88,9 +89,20 @@ struct StageSmem {
     uint8_t k[kTile];
 };
 
+constexpr int kRing = 8;       // device-tile epilogue descriptors in flight
+
+struct TileInfo {
+    int64_t t;                 // global tile index, -1 = end
+    int32_t cnt, head, tf, pad;
+    u64 t0, t1;
+};
+
 struct Ctrl {
-    uint64_t full[kStages];    // producer -> compute: tile data landed
-    uint64_t empty[kStages];   // compute -> producer: stage consumed (+ tile aggregate below)
+    uint64_t full[kStages];    // TMA warp -> compute: tile data landed
+    uint64_t empty[kStages];   // compute -> TMA warp: stage consumed
+    uint64_t info_full[kRing];  // compute -> epilogue warp: device tile published
+    uint64_t info_empty[kRing]; // epilogue warp -> compute: descriptor slot free
+    TileInfo info[kRing];
     int64_t tile[kStages];
     int32_t cnt[kStages];
     int32_t has_prev[kStages];
@@ -101,11 +113,6 @@ struct Ctrl {
     // host tiles: per-stage max end and finished-warp count (smem atomics)
     u64 h_max[kStages];
     unsigned int h_cnt[kStages];
-    // tile aggregate and head continuation, for the producer's epilogue
-    int32_t t_flag[kStages];
-    int32_t t_head[kStages];
-    u64 t_v0[kStages];
-    u64 t_v1[kStages];
     // per-stage warp aggregates of the tile (written by compute warps)
     int32_t w_flag[kStages][kComputeWarps];
     u64 w_v0[kStages][kComputeWarps];
@@ -189,13 +196,20 @@ __device__ __forceinline__ u64 warp_sum(u64 v)
     return v;
 }
 
-// E for device tiles: the explicit window, the max host end (after every
-// host tile published), or "no clamp" for device-only traces
+// E for device tiles: the explicit window, the max host end (after every CTA
+// finished its host tiles, host_phase_done), or "no clamp" for device-only traces
+// one release per CTA when its compute warps are past their last host tile
+// (tiles are claimed in order): all their host max-end REDs become visible
+__device__ __forceinline__ void host_phase_done(const Params &p)
+{
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(&p.g->host_done) : "memory");
+}
+
 __device__ u64 device_window(const Params &p)
 {
     if (p.mode == kSummarizeDevice) return p.elapsed_arg;
     if ((p.mode == kReport || p.mode == kValidate) && p.n >= 1) {
-        while (ld_acquire64(&p.g->host_done) < (u64)p.host_tiles) __nanosleep(64);
+        while (ld_acquire64(&p.g->host_done) < (u64)gridDim.x) __nanosleep(64);
         return umax(ld_relaxed(&p.g->host_max_end), p.host_elapsed_floor);
     }
     return ~0ull;
@@ -475,17 +489,30 @@ __device__ __forceinline__ TileView tile_view(const Ctrl *c, int st, int warp, i
 // Right after the tile view: publish the tile aggregate (P if a segment
 // starts in the tile -- its tail prefix is then local -- else A), the host
 // max end for E, and hand the producer what its epilogue needs.
+// hand a device tile's epilogue to the epilogue warp (descriptor ring)
+__device__ __forceinline__ void post_info(Ctrl *c, int &k, int64_t t, int cnt, bool head, bool tf, u64 t0, u64 t1)
+{
+    const int slot = k % kRing;
+    if (k >= kRing) mbar_wait(&c->info_empty[slot], (uint32_t)(((k / kRing) - 1) & 1));
+    TileInfo &x = c->info[slot];
+    x.t = t;
+    x.cnt = cnt;
+    x.head = head;
+    x.tf = tf;
+    x.t0 = t0;
+    x.t1 = t1;
+    mbar_arrive(&c->info_full[slot]);
+    ++k;
+}
+
 template <bool DEV>
 __device__ __forceinline__ void publish_tile(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc,
-                                             const TileView &tv)
+                                             const TileView &tv, int &k)
 {
     const bool head = tc.cnt > 0 && c->has_prev[tc.st] && sm.r[0] == c->prev_res[tc.st];
     if (DEV) publish<2>(tv.tf ? p.d_slotP + 4 * tc.lt : p.d_slotA + 4 * tc.lt, p.epoch, tv.t0, tv.t1);
     else publish<1>(tv.tf ? p.h_slotP + 2 * tc.lt : p.h_slotA + 2 * tc.lt, p.epoch, tv.t0, 0);
-    c->t_flag[tc.st] = tv.tf;
-    c->t_head[tc.st] = head;
-    c->t_v0[tc.st] = tv.t0;
-    c->t_v1[tc.st] = tv.t1;
+    if (head) post_info(c, k, tc.lt, tc.cnt, head, tv.tf, tv.t0, tv.t1);
 }
 
 // Emit per-resource totals.  A thread's records split into a head piece
@@ -865,7 +892,7 @@ __device__ __forceinline__ void host_compute(const Params &p, const StageSmem &s
     tmax = umax(tmax, last);
     if (ovl && !*(volatile unsigned *)&p.g->ovl_suspect) atomicOr(&p.g->ovl_suspect, 1u);
     if (rare || ovl) tmax = host_rare(p, sm, c, tc.st, b, nv, gi0);
-    ph.add(ph.b);
+    ph.add(ph.hb);
     if (P.head_open) { P.head[0] = P.head[1] = P.head[2] = 0; }
     u64 *const dst[3] = {p.h_off, p.h_mpi, p.h_span};
     emit_segments<2>(P.head, P.cur, sfm, nv, P.first_r, P.cur_r, p.host_ids, dst, lane);
@@ -877,11 +904,10 @@ __device__ __forceinline__ void host_compute(const Params &p, const StageSmem &s
         if (atomicAdd(&c->h_cnt[tc.st], 1u) == kComputeWarps - 1) {
             const u64 m = atomicExch(&c->h_max[tc.st], 0ull);
             c->h_cnt[tc.st] = 0;
-            red_max(&p.g->host_max_end, m);
-            asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(&p.g->host_done) : "memory");
+            red_max(&p.g->host_max_end, m);   // host_done is signalled once per CTA (host_phase_done)
         }
     }
-    ph.add(ph.emit);
+    ph.add(ph.hemit);
     (void)warp;
 }
 
@@ -946,7 +972,7 @@ __device__ __forceinline__ bool dev_phase_b(const Params &p, const StageSmem &sm
 }
 
 __device__ __forceinline__ void dev_compute(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
-                                            u64 &E_cache, bool &E_known, Phases &ph)
+                                            u64 &E_cache, bool &E_known, bool &signalled, int &k, Phases &ph)
 {
     ph.mark();
     const int warp = tid >> 5, lane = tid & 31;
@@ -963,17 +989,19 @@ __device__ __forceinline__ void dev_compute(const Params &p, const StageSmem &sm
     if (lane == 31) { c->w_flag[tc.st][warp] = in_f; c->w_v0[tc.st][warp] = in0; c->w_v1[tc.st][warp] = in1; }
     if (lane == 0) { c->w_mn[tc.st][warp] = mn; c->w_mx[tc.st][warp] = mx; }
     ph.add(ph.a);
+    bar_compute();
     if (!E_known) {   // once per warp: E from the host phase (device_window)
+        if (tid == 0 && !signalled) host_phase_done(p);   // every warp of this CTA is past its host tiles
+        signalled = true;
         u64 E = 0;
         if (lane == 0) E = device_window(p);
         E_cache = __shfl_sync(0xffffffffu, E, 0);
         E_known = true;
     }
-    bar_compute();
     const u64 E = E_cache;
     const bool late_check = (p.mode == kReport || p.mode == kValidate) && p.n >= 1;
     const TileView tv = tile_view(c, tc.st, warp, lane, in_f, in0, in1);
-    if (tid == 0) publish_tile<true>(p, sm, c, tc, tv);
+    if (tid == 0) publish_tile<true>(p, sm, c, tc, tv, k);
     ph.add(ph.bar);
     Pieces3 P;
     P.head[0] = P.head[1] = P.head[2] = 0;
@@ -996,17 +1024,11 @@ __device__ __forceinline__ void dev_compute(const Params &p, const StageSmem &sm
 // for the carry, publish P, and correct the tile's head segment (the compute
 // warps used carry 0) reading the few affected records from global memory
 // =========================================================================
-struct Epi {
-    int64_t lt;
-    int cnt;
-    bool dev, head, tf;
-    u64 t0, t1;
-};
 
-__device__ void dev_epilogue(const Params &p, const Epi &x, int lane, u64 &E_cache, bool &E_known)
+__device__ void dev_epilogue(const Params &p, const TileInfo &x, int lane, u64 &E_cache, bool &E_known)
 {
     // the first 32 records are loaded before the look-back (overlapped round trips)
-    const int64_t g0 = x.lt * kTile;
+    const int64_t g0 = x.t * kTile;
     const u64 *S = p.ds + g0, *En = p.de + g0;
     const int32_t *R = p.dr + g0;
     const uint8_t *K = p.dk + g0;
@@ -1015,8 +1037,8 @@ __device__ void dev_epilogue(const Params &p, const Epi &x, int lane, u64 &E_cac
     uint8_t kj = 1;
     if (lane < x.cnt) { rj = __ldcg(R + lane); sj = __ldcg(S + lane); ej = __ldcg(En + lane); kj = __ldcg(K + lane); }
     u64 ck, ckm;
-    look_back<2>(p.d_slotA, p.d_slotP, x.lt, p.epoch, lane, ck, ckm);
-    if (!x.tf && lane == 0) publish<2>(p.d_slotP + 4 * x.lt, p.epoch, umax(ck, x.t0), umax(ckm, x.t1));
+    look_back<2>(p.d_slotA, p.d_slotP, x.t, p.epoch, lane, ck, ckm);
+    if (!x.tf && lane == 0) publish<2>(p.d_slotP + 4 * x.t, p.epoch, umax(ck, x.t0), umax(ckm, x.t1));
     if (!E_known) {
         u64 Ew = 0;
         if (lane == 0) Ew = device_window(p);
@@ -1313,44 +1335,36 @@ __global__ void __launch_bounds__(kThreads, 1) analyze_kernel(const __grid_const
             c->h_max[s] = 0;
             c->h_cnt[s] = 0;
         }
+        for (int s = 0; s < kRing; ++s) {
+            mbar_init(&c->info_full[s], 1);
+            mbar_init(&c->info_empty[s], 1);
+        }
         fence_mbar_init();
     }
     __syncthreads();
     u64 E_cache = 0;
     bool E_known = false;
     if (warp == kComputeWarps) {
-        // ---------------- producer warp ----------------
+        // ---------------- TMA warp: keep every stage in flight ----------------
         const uint64_t pol = l2_policy_evict_first();
         for (int s = 0; s < kStages; ++s) produce(p, stages, c, s, claim_finish(p, claim_issue(p, lane)), lane, pol);
-        // claims run ahead of use: the atomic is issued one iteration before its index is
-        // needed and the previous-record loads one iteration before the refill
+        // claims run ahead of use: the atomic is issued one refill before its index is
+        // needed and the previous-record loads one refill before the TMA issue
         Claim next = claim_finish(p, claim_issue(p, lane));
         int64_t pend = claim_issue(p, lane);
-        PROF_DECL(pa); PROF_DECL(pb); PROF_DECL(pc); PROF_DECL(pn);
+        PROF_DECL(pa); PROF_DECL(pb); PROF_DECL(pn);
         for (int it = 0;; ++it) {
             const int st = it % kStages;
             const uint32_t ph = (uint32_t)((it / kStages) & 1);
-            const int64_t t = c->tile[st];
-            if (t < 0) break;
+            if (c->tile[st] < 0) break;
             long long t0 = PROF_NOW();
             mbar_wait(&c->empty[st], ph);
             PROF_ADD(pa, t0);
-            Epi x;
-            x.dev = t >= p.host_tiles;
-            x.lt = x.dev ? t - p.host_tiles : t;
-            x.cnt = c->cnt[st];
-            x.head = c->t_head[st] != 0;
-            x.tf = c->t_flag[st] != 0;
-            x.t0 = c->t_v0[st];
-            x.t1 = c->t_v1[st];
             t0 = PROF_NOW();
             produce(p, stages, c, st, next, lane, pol);
             next = claim_finish(p, pend);
             pend = claim_issue(p, lane);
             PROF_ADD(pb, t0);
-            t0 = PROF_NOW();
-            if (x.head && x.dev) dev_epilogue(p, x, lane, E_cache, E_known);
-            PROF_ADD(pc, t0);
 #ifdef HB_PROF
             ++pn;
 #endif
@@ -1359,13 +1373,38 @@ __global__ void __launch_bounds__(kThreads, 1) analyze_kernel(const __grid_const
 #ifdef HB_PROF
         if (lane == 0) {
             unsigned long long *o = hb_prof_buf + blockIdx.x * kProfSlots;
-            o[8] = pa; o[9] = pb; o[10] = pc; o[11] = 0; o[12] = pn;
+            o[8] = pa; o[9] = pb; o[12] = pn;
+        }
+#endif
+    } else if (warp == kComputeWarps + 1) {
+        // ---------------- epilogue warp: look-back + carry fix-up of device tiles ----------------
+        PROF_DECL(pc); PROF_DECL(pw);
+        for (int k = 0;; ++k) {
+            const int slot = k % kRing;
+            long long t0 = PROF_NOW();
+            mbar_wait(&c->info_full[slot], (uint32_t)((k / kRing) & 1));
+            PROF_ADD(pw, t0);
+            const TileInfo x = c->info[slot];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&c->info_empty[slot]);
+            if (x.t < 0) break;
+            t0 = PROF_NOW();
+            dev_epilogue(p, x, lane, E_cache, E_known);
+            PROF_ADD(pc, t0);
+            (void)t0;
+        }
+#ifdef HB_PROF
+        if (lane == 0) {
+            unsigned long long *o = hb_prof_buf + blockIdx.x * kProfSlots;
+            o[10] = pc; o[11] = pw;
         }
 #endif
     } else {
         // ---------------- compute warps ----------------
         PROF_DECL(ca); PROF_DECL(cb); PROF_DECL(cn);
         Phases phs;
+        bool signalled = false;
+        int k = 0;
         for (int it = 0;; ++it) {
             const int st = it % kStages;
             long long t0 = PROF_NOW();
@@ -1381,7 +1420,10 @@ __global__ void __launch_bounds__(kThreads, 1) analyze_kernel(const __grid_const
             tc.gbase = tc.lt * kTile;
             t0 = PROF_NOW();
             if (!dev) host_compute(p, stages[st], c, tc, tid, phs);
-            else dev_compute(p, stages[st], c, tc, tid, E_cache, E_known, phs);
+            else dev_compute(p, stages[st], c, tc, tid, E_cache, E_known, signalled, k, phs);
+#ifdef HB_PROF
+            if (dev) ++phs.dn; else ++phs.hn;
+#endif
             __syncwarp();
             if (lane == 0) mbar_arrive(&c->empty[st]);
             PROF_ADD(cb, t0);
@@ -1390,11 +1432,16 @@ __global__ void __launch_bounds__(kThreads, 1) analyze_kernel(const __grid_const
 #endif
             (void)t0;
         }
+        if (tid == 0) {
+            post_info(c, k, -1, 0, false, false, 0, 0);     // end of the epilogue stream
+            if (!signalled) host_phase_done(p);             // CTAs without device tiles
+        }
 #ifdef HB_PROF
         if (tid == 0) {
             unsigned long long *o = hb_prof_buf + blockIdx.x * kProfSlots;
             o[0] = ca; o[1] = cb; o[2] = cn;
             o[3] = phs.a; o[4] = phs.bar; o[5] = phs.b; o[6] = phs.emit;
+            o[16] = phs.hb; o[17] = phs.hemit; o[18] = phs.hn; o[19] = phs.dn;
         }
 #endif
     }
@@ -1590,14 +1637,19 @@ int prof_read(unsigned long long *out, int n)
 #endif
 }
 
+// persistent grid: every SM x resident CTAs; 0 when the tile geometry does not fit
 int analyze_grid(int device)
 {
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaFuncSetAttribute(analyze_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)analyze_smem_bytes());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, analyze_kernel, kThreads, analyze_smem_bytes());
-    if (per < 1) per = 1;
-    return sms * per;
+    if (cudaFuncSetAttribute(analyze_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)analyze_smem_bytes()) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, analyze_kernel, kThreads, analyze_smem_bytes()) !=
+            cudaSuccess) {
+        cudaGetLastError();   // not sticky: clear it so later launches report their own status
+        return 0;
+    }
+    return sms * (per < 1 ? 1 : per);
 }
 
 cudaError_t launch_analyze(const Params &p, int grid, cudaStream_t s)

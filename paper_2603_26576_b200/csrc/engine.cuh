@@ -9,7 +9,7 @@ typedef unsigned long long u64;
 
 // tile geometry (compile-time knobs, see tools/build_variants.sh)
 #ifndef HB_WARPS
-#define HB_WARPS 15
+#define HB_WARPS 14
 #endif
 #ifndef HB_ITEMS
 #define HB_ITEMS 11
@@ -19,7 +19,7 @@ typedef unsigned long long u64;
 #endif
 constexpr int kComputeWarps = HB_WARPS;
 constexpr int kComputeThreads = kComputeWarps * 32;
-constexpr int kThreads = kComputeThreads + 32;         // + producer / look-back warp
+constexpr int kThreads = kComputeThreads + 64;         // + TMA warp + look-back/epilogue warp
 constexpr int kItems = HB_ITEMS;                       // odd: conflict-free blocked smem reads
 constexpr int kTile = kComputeThreads * kItems;        // records per tile (multiple of 16)
 constexpr int kStages = HB_STAGES;

@@ -16,14 +16,16 @@ cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
 dt = generate(cfg)
 for _ in range(3):
     f = analyze_device(dt)
-buf = np.zeros(1024 * 16, dtype=np.uint64)
+buf = np.zeros(1024 * 32, dtype=np.uint64)
 k = N.load().heteff_prof_read(buf.ctypes.data, buf.size)
 grid = N.load()  # noqa
-P = buf[: k].reshape(-1, 16)
+P = buf[: k].reshape(-1, 32)
 P = P[P[:, 2] > 0]
-names = {0: "c.wait_full", 1: "c.compute", 3: "c.phaseA", 4: "c.bar+view", 5: "c.phaseB", 6: "c.emit",
-         8: "p.wait_empty", 9: "p.produce", 10: "p.epilogue"}
+names = {0: ("c.wait_full", 2), 1: ("c.compute", 2), 16: ("host.loop", 18), 17: ("host.emit+max", 18),
+         3: ("dev.phaseA", 19), 4: ("dev.bar+view", 19), 5: ("dev.phaseB", 19), 6: ("dev.emit", 19),
+         8: ("tma.wait_empty", 12), 9: ("tma.produce", 12), 10: ("epi.work", 19), 11: ("epi.wait_info", 19)}
 print(f"{cfg.name}: kernel {f.kernel_ms:.3f} ms, CTAs {P.shape[0]}, tiles/CTA {P[:, 2].mean():.1f}")
-for i, nm in names.items():
-    per = P[:, i].astype(float) / np.maximum(P[:, 2 if i < 8 else 12], 1)
+print(f"  host tiles/CTA {P[:, 18].mean():.1f}, device tiles/CTA {P[:, 19].mean():.1f}")
+for i, (nm, den) in names.items():
+    per = P[:, i].astype(float) / np.maximum(P[:, den], 1)
     print(f"  {nm:14s} mean {per.mean():9.0f} cyc/tile   p10 {np.percentile(per, 10):9.0f}  p90 {np.percentile(per, 90):9.0f}")
