@@ -113,6 +113,10 @@ struct Ctrl {
     // host tiles: per-stage max end and finished-warp count (smem atomics)
     u64 h_max[kStages];
     unsigned int h_cnt[kStages];
+    // single-segment device tiles: per-warp 32-bit aggregates relative to the tile base
+    uint32_t f_k[kStages][kComputeWarps];
+    uint32_t f_km[kStages][kComputeWarps];
+    int32_t f_fit[kStages][kComputeWarps];
     // per-stage warp aggregates of the tile (written by compute warps)
     int32_t w_flag[kStages][kComputeWarps];
     u64 w_v0[kStages][kComputeWarps];
@@ -437,6 +441,22 @@ __device__ __forceinline__ void warp_seg_max(bool &f, u64 &v0, u64 &v1, int lane
         const u64 o0 = shfl_up64(v0, d), o1 = shfl_up64(v1, d);
         if (lane >= d) seg_combine(of, o0, o1, f, v0, v1);
     }
+}
+
+// warp inclusive max scan of two 32-bit values
+__device__ __forceinline__ void warp_max_scan2(uint32_t &a, uint32_t &b, int lane)
+{
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t oa = __shfl_up_sync(0xffffffffu, a, d), ob = __shfl_up_sync(0xffffffffu, b, d);
+        if (lane >= d) { a = max(a, oa); b = max(b, ob); }
+    }
+}
+
+// exact warp sum of 32-bit values (two 16-bit limbs on the REDUX unit)
+__device__ __forceinline__ u64 warp_sum32(uint32_t v)
+{
+    return (u64)__reduce_add_sync(0xffffffffu, v & 0xffffu) + ((u64)__reduce_add_sync(0xffffffffu, v >> 16) << 16);
 }
 
 // Per-tile values every compute thread derives (cooperatively per warp)
@@ -971,9 +991,122 @@ __device__ __forceinline__ bool dev_phase_b(const Params &p, const StageSmem &sm
     return rare;
 }
 
+// E once per warp (and the CTA's host-phase release), after the CTA barrier
+__device__ __forceinline__ u64 device_E(const Params &p, int tid, int lane, u64 &E_cache, bool &E_known,
+                                        bool &signalled)
+{
+    if (!E_known) {
+        if (tid == 0 && !signalled) host_phase_done(p);   // every warp of this CTA is past its host tiles
+        signalled = true;
+        u64 E = 0;
+        if (lane == 0) E = device_window(p);
+        E_cache = __shfl_sync(0xffffffffu, E, 0);
+        E_known = true;
+    }
+    return E_cache;
+}
+
+// -------------------------------------------------------------------------
+// Single-segment device tile (every record of one device -- the common case):
+// no segment flags, the tile base is its first start (records are
+// start-sorted), every running max is a plain 32-bit max relative to it.
+// Returns false (nothing done) if some end leaves the base's 2^32 window.
+// -------------------------------------------------------------------------
+__device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
+                                           u64 &E_cache, bool &E_known, bool &signalled, int &kq, Phases &ph)
+{
+    const int warp = tid >> 5, lane = tid & 31;
+    const int b = tid * kItems;
+    const int nv = max(0, min(kItems, tc.cnt - b));
+    const int64_t gi0 = tc.gbase + (int64_t)b;
+    const u64 base = sm.s[0];
+    const uint32_t bl = (uint32_t)base, bh = (uint32_t)(base >> 32);
+    const uint32_t *S32 = reinterpret_cast<const uint32_t *>(sm.s);
+    const uint32_t *E32 = reinterpret_cast<const uint32_t *>(sm.e);
+    // phase A: kernel-only and all-record max of relative ends
+    uint32_t vK = 0, vKM = 0;
+    bool out = false;
+#pragma unroll kUnrollA
+    for (int j = 0; j < kItems; ++j) {
+        if (j < nv) {
+            const uint32_t el = E32[2 * (b + j)], eh = E32[2 * (b + j) + 1];
+            const uint32_t e = el - bl;
+            out = out || eh != bh || el < bl;      // end outside [base, base + 2^32): 64-bit path
+            vKM = max(vKM, e);
+            if (sm.k[b + j] == 0) vK = max(vK, e);
+        }
+    }
+    const bool fit_w = __all_sync(0xffffffffu, !out);
+    warp_max_scan2(vK, vKM, lane);
+    if (lane == 31) { c->f_k[tc.st][warp] = vK; c->f_km[tc.st][warp] = vKM; c->f_fit[tc.st][warp] = fit_w; }
+    ph.add(ph.a);
+    bar_compute();
+    const u64 E = device_E(p, tid, lane, E_cache, E_known, signalled);
+    // tile-wide: all warps in the window?  cross-warp exclusive prefix
+    uint32_t wK = 0, wKM = 0;
+    bool fit = true;
+    if (lane < kComputeWarps) { wK = c->f_k[tc.st][lane]; wKM = c->f_km[tc.st][lane]; fit = c->f_fit[tc.st][lane] != 0; }
+    if (!__all_sync(0xffffffffu, fit)) return false;
+    warp_max_scan2(wK, wKM, lane);
+    const uint32_t tK = __shfl_sync(0xffffffffu, wK, kComputeWarps - 1), tKM = __shfl_sync(0xffffffffu, wKM, kComputeWarps - 1);
+    const uint32_t xwK = __shfl_sync(0xffffffffu, wK, warp > 0 ? warp - 1 : 0);
+    const uint32_t xwKM = __shfl_sync(0xffffffffu, wKM, warp > 0 ? warp - 1 : 0);
+    uint32_t xK = __shfl_up_sync(0xffffffffu, vK, 1), xKM = __shfl_up_sync(0xffffffffu, vKM, 1);
+    if (lane == 0) { xK = 0; xKM = 0; }
+    if (warp > 0) { xK = max(xK, xwK); xKM = max(xKM, xwKM); }
+    const bool head = c->has_prev[tc.st] && sm.r[0] == c->prev_res[tc.st];
+    if (tid == 0) {
+        // tile aggregate (a segment starts here iff the tile does not continue one)
+        publish<2>(!head ? p.d_slotP + 4 * tc.lt : p.d_slotA + 4 * tc.lt, p.epoch, base + tK, base + tKM);
+        if (head) post_info(c, kq, tc.lt, tc.cnt, true, false, base + tK, base + tKM);
+    }
+    ph.add(ph.bar);
+    // phase B: the union pass in 32 bits, carry 0 (the epilogue warp fixes the head)
+    const uint32_t Er = E <= base ? 0u : (E - base > 0xffffffffull ? 0xffffffffu : (uint32_t)(E - base));
+    const int32_t r0 = sm.r[0];
+    const bool decl = declared(p.dev_decl, p.dev_ids, p.m, r0);
+    bool rare = E < base || !decl;
+    uint32_t runK = min(xK, Er), runKM = min(xKM, Er), cK = 0, cKM = 0, ps = 0;
+    if (b == 0) rare = rare || (head && nv > 0 && sm.s[0] < c->prev_start[tc.st]);
+    else ps = S32[2 * (b - 1)] - bl;
+#pragma unroll kUnrollB
+    for (int j = 0; j < kItems; ++j) {
+        if (j < nv) {
+            const uint32_t s0 = S32[2 * (b + j)] - bl, e0 = E32[2 * (b + j)] - bl;
+            const uint8_t kk = sm.k[b + j];
+            rare = rare || ((j > 0 || b > 0) && s0 < ps) || s0 >= e0 || e0 > Er;
+            const uint32_t e = min(e0, Er), s = min(s0, e);
+            const uint32_t loKM = max(runKM, s);
+            runKM = max(runKM, e);
+            cKM += runKM - loKM;
+            if (kk == 0) {
+                const uint32_t loK = max(runK, s);
+                runK = max(runK, e);
+                cK += runK - loK;
+            }
+            ps = s0;
+        }
+    }
+    if (rare) rescan<true>(p, sm, c, tc.st, b, nv, 0, E, (p.mode == kReport || p.mode == kValidate) && p.n >= 1, gi0);
+    ph.add(ph.b);
+    // one piece for the whole tile: warp reductions, one RED per field per warp
+    const u64 sK = warp_sum32(cK), sKM = warp_sum32(cKM);
+    const uint32_t mx = __reduce_max_sync(0xffffffffu, nv > 0 ? runKM : 0u);
+    if (lane == 0 && r0 >= 0 && r0 < p.dev_ids) {
+        if (sK) red_add(p.d_k + r0, sK);
+        if (sKM) red_add(p.d_km + r0, sKM);
+        red_max(p.d_maxend + r0, base + mx);
+    }
+    ph.add(ph.emit);
+    return true;
+}
+
 __device__ __forceinline__ void dev_compute(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
                                             u64 &E_cache, bool &E_known, bool &signalled, int &k, Phases &ph)
 {
+    if (tc.cnt > 0 && sm.r[0] == sm.r[tc.cnt - 1] &&
+        dev_single(p, sm, c, tc, tid, E_cache, E_known, signalled, k, ph))
+        return;
     ph.mark();
     const int warp = tid >> 5, lane = tid & 31;
     const int b = tid * kItems;
@@ -990,14 +1123,7 @@ __device__ __forceinline__ void dev_compute(const Params &p, const StageSmem &sm
     if (lane == 0) { c->w_mn[tc.st][warp] = mn; c->w_mx[tc.st][warp] = mx; }
     ph.add(ph.a);
     bar_compute();
-    if (!E_known) {   // once per warp: E from the host phase (device_window)
-        if (tid == 0 && !signalled) host_phase_done(p);   // every warp of this CTA is past its host tiles
-        signalled = true;
-        u64 E = 0;
-        if (lane == 0) E = device_window(p);
-        E_cache = __shfl_sync(0xffffffffu, E, 0);
-        E_known = true;
-    }
+    device_E(p, tid, lane, E_cache, E_known, signalled);
     const u64 E = E_cache;
     const bool late_check = (p.mode == kReport || p.mode == kValidate) && p.n >= 1;
     const TileView tv = tile_view(c, tc.st, warp, lane, in_f, in0, in1);
