@@ -347,17 +347,18 @@ __device__ __forceinline__ void publish(u64 *slot, uint32_t epoch, u64 v0, u64 v
     }
 }
 
+// 16-byte L2 loads (each 8-byte word is single-copy atomic; validity is per word)
 template <int NV>
 __device__ __forceinline__ bool read_slot(const u64 *slot, uint32_t epoch, u64 &v0, u64 &v1)
 {
-    const u64 a = ld_relaxed(slot + 0), b = ld_relaxed(slot + 1);
-    bool ok = (a >> 32) == epoch && (b >> 32) == epoch;
-    v0 = (a << 32) | (b & 0xffffffffull);
+    const ulonglong2 ab = __ldcg(reinterpret_cast<const ulonglong2 *>(slot));
+    bool ok = (ab.x >> 32) == epoch && (ab.y >> 32) == epoch;
+    v0 = (ab.x << 32) | (ab.y & 0xffffffffull);
     v1 = 0;
     if (NV == 2) {
-        const u64 c = ld_relaxed(slot + 2), d = ld_relaxed(slot + 3);
-        ok = ok && (c >> 32) == epoch && (d >> 32) == epoch;
-        v1 = (c << 32) | (d & 0xffffffffull);
+        const ulonglong2 cd = __ldcg(reinterpret_cast<const ulonglong2 *>(slot + 2));
+        ok = ok && (cd.x >> 32) == epoch && (cd.y >> 32) == epoch;
+        v1 = (cd.x << 32) | (cd.y & 0xffffffffull);
     }
     return ok;
 }
@@ -802,10 +803,21 @@ __device__ __noinline__ u64 host_rare(const Params &p, const StageSmem &sm, cons
         pr = sm.r[b - 1];
         ps = sm.s[b - 1];
     }
-    bool decl = false;
+    bool decl = false, ovl = false;
     int32_t cur = 0;
-    u64 mx = 0, seg = 0;
+    u64 mx = 0, seg = 0, pe = 0;
     int bad = -1;
+    // end of the last usable record before this thread, when at hand (else: conservative)
+    bool pe_known = true;
+    {
+        int q = b - 1;
+        while (q >= 0 && sm.r[q] == sm.r[b] && sm.s[q] >= sm.e[q]) --q;
+        if (q >= 0 && sm.r[q] == sm.r[b]) pe = sm.e[q];
+        else if (q < 0 && hp && pr == sm.r[b]) {
+            if (b == 0 && c->prev_start[st] < c->prev_end[st]) pe = c->prev_end[st];
+            else pe_known = false;
+        }
+    }
     for (int j = 0; j < nv; ++j) {
         const int32_t r = sm.r[b + j];
         const u64 s = sm.s[b + j], e = sm.e[b + j];
@@ -818,9 +830,15 @@ __device__ __noinline__ u64 host_rare(const Params &p, const StageSmem &sm, cons
         }
         if (j == 0 || start) {
             if (j > 0 && seg && cur >= 0 && cur < p.host_ids) red_max(p.h_span + cur, seg);
+            if (start) { pe = 0; pe_known = true; }
             cur = r;
             seg = 0;
             decl = declared(p.host_decl, p.host_ids, p.n, r);
+        }
+        if (s < e) {   // usable: adjacent overlap check against the last usable end
+            if (s < pe || !pe_known) ovl = true;
+            pe = e;
+            pe_known = true;
         }
         const int64_t gi = gi0 + j;
         if (s > e) push(p, 0, gi);
@@ -833,7 +851,52 @@ __device__ __noinline__ u64 host_rare(const Params &p, const StageSmem &sm, cons
     }
     if (nv > 0 && seg && cur >= 0 && cur < p.host_ids) red_max(p.h_span + cur, seg);   // exact span maxima
     if (bad >= 0) contract(p, 1u, gi0 + bad);
+    if (ovl && !*(volatile unsigned *)&p.g->ovl_suspect) atomicOr(&p.g->ovl_suspect, 1u);
     return mx;
+}
+
+// Fast path for a thread whose records all belong to one rank and lie in one
+// aligned 2^32 ns window: every check and sum in 32 bits relative to the
+// window.  Returns false (results unused) if a record leaves the window.
+__device__ __forceinline__ bool host_fast32(const StageSmem &sm, int b, int nv, bool cont, u64 ps64, u64 pe64,
+                                            bool &rare, bool &ovl, u64 &off, u64 &mpi, u64 &last)
+{
+    const u64 base = sm.s[b];
+    const uint32_t bh = (uint32_t)(base >> 32), bl = (uint32_t)base;
+    // the previous record of the same rank (cont): relative start / usable end, clamped into the window
+    uint32_t ps = 0, pe = 0;
+    if (cont) {
+        ps = ps64 >= base ? (uint32_t)(ps64 - base) : 0u;
+        rare = rare || ps64 > base;                                     // order
+        pe = pe64 <= base ? 0u : (pe64 - base > 0xffffffffull ? 0xffffffffu : (uint32_t)(pe64 - base));
+    }
+    const uint32_t *S32 = reinterpret_cast<const uint32_t *>(sm.s);
+    const uint32_t *E32 = reinterpret_cast<const uint32_t *>(sm.e);
+    bool out = false;
+    uint32_t o = 0, m = 0, l = 0;
+#pragma unroll kUnrollB
+    for (int j = 0; j < kItems; ++j) {
+        if (j < nv) {
+            const int i = b + j;
+            const uint32_t sl = S32[2 * i], sh = S32[2 * i + 1], el = E32[2 * i], eh = E32[2 * i + 1];
+            const uint8_t k = sm.k[i];
+            out = out || sh != bh || eh != bh || sl < bl || el < bl;   // outside [base, base + 2^32)
+            const uint32_t s = sl - bl, e = el - bl;
+            rare = rare || (j > 0 && s < ps) || s >= e;   // order / zero-length / malformed
+            const bool usable = s < e;
+            ovl = ovl || (usable && s < pe);
+            pe = usable ? e : pe;
+            l = usable ? e : l;
+            const uint32_t d = e - s;
+            o += k == 1 ? d : 0u;
+            m += k == 2 ? d : 0u;
+            ps = s;
+        }
+    }
+    off = o;
+    mpi = m;
+    last = base + l;
+    return !out;
 }
 
 __device__ __forceinline__ void host_compute(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc,
@@ -873,9 +936,29 @@ __device__ __forceinline__ void host_compute(const Params &p, const StageSmem &s
     uint32_t sfm = 0;
     bool rare = nv > 0 && !P.cur_decl;
     u64 off = 0, mpi = 0, last = 0, tmax = 0;
+    // one rank inside the thread (and in one 2^32 window): the 32-bit fast path
+    bool done = false;
+    if (nv > 0 && sm.r[b] == sm.r[b + nv - 1]) {
+        const bool cont = hp && pr == sm.r[b];
+        bool r2 = rare, o2 = ovl;
+        u64 of2, mp2, la2;
+        if (host_fast32(sm, b, nv, cont, ps, pe, r2, o2, of2, mp2, la2)) {
+            if (!cont) {
+                sfm = 1u;
+                P.head_open = false;
+                r2 = r2 || (hp && sm.r[b] < pr);   // rank order across the segment start
+            }
+            rare = r2;
+            ovl = o2;
+            off = of2;
+            mpi = mp2;
+            last = la2;
+            done = true;
+        }
+    }
 #pragma unroll kUnrollB
     for (int j = 0; j < kItems; ++j) {
-        if (j < nv) {
+        if (!done && j < nv) {
             const int32_t r = sm.r[b + j];
             const u64 s = sm.s[b + j], e = sm.e[b + j];
             const uint8_t k = sm.k[b + j];
@@ -1502,10 +1585,11 @@ __global__ void __launch_bounds__(kThreads, 1) analyze_kernel(const __grid_const
             o[8] = pa; o[9] = pb; o[12] = pn;
         }
 #endif
-    } else if (warp == kComputeWarps + 1) {
-        // ---------------- epilogue warp: look-back + carry fix-up of device tiles ----------------
+    } else if (warp > kComputeWarps) {
+        // ---------------- epilogue warps: look-back + carry fix-up of device tiles ----------------
+        // descriptor k goes to epilogue warp k % kEpiWarps
         PROF_DECL(pc); PROF_DECL(pw);
-        for (int k = 0;; ++k) {
+        for (int k = warp - kComputeWarps - 1;; k += kEpiWarps) {
             const int slot = k % kRing;
             long long t0 = PROF_NOW();
             mbar_wait(&c->info_full[slot], (uint32_t)((k / kRing) & 1));
@@ -1520,7 +1604,7 @@ __global__ void __launch_bounds__(kThreads, 1) analyze_kernel(const __grid_const
             (void)t0;
         }
 #ifdef HB_PROF
-        if (lane == 0) {
+        if (lane == 0 && warp == kComputeWarps + 1) {
             unsigned long long *o = hb_prof_buf + blockIdx.x * kProfSlots;
             o[10] = pc; o[11] = pw;
         }
@@ -1558,8 +1642,9 @@ __global__ void __launch_bounds__(kThreads, 1) analyze_kernel(const __grid_const
 #endif
             (void)t0;
         }
+        bar_compute();   // every compute warp is done with its last tile (incl. host max-end REDs)
         if (tid == 0) {
-            post_info(c, k, -1, 0, false, false, 0, 0);     // end of the epilogue stream
+            for (int e = 0; e < kEpiWarps; ++e) post_info(c, k, -1, 0, false, false, 0, 0);   // end of stream
             if (!signalled) host_phase_done(p);             // CTAs without device tiles
         }
 #ifdef HB_PROF

@@ -9,7 +9,10 @@ typedef unsigned long long u64;
 
 // tile geometry (compile-time knobs, see tools/build_variants.sh)
 #ifndef HB_WARPS
-#define HB_WARPS 14
+#define HB_WARPS 13
+#endif
+#ifndef HB_EPI
+#define HB_EPI 2
 #endif
 #ifndef HB_ITEMS
 #define HB_ITEMS 11
@@ -19,7 +22,8 @@ typedef unsigned long long u64;
 #endif
 constexpr int kComputeWarps = HB_WARPS;
 constexpr int kComputeThreads = kComputeWarps * 32;
-constexpr int kThreads = kComputeThreads + 64;         // + TMA warp + look-back/epilogue warp
+constexpr int kEpiWarps = HB_EPI;                      // look-back / carry fix-up warps
+constexpr int kThreads = kComputeThreads + 32 * (1 + kEpiWarps);   // + TMA warp + epilogue warps
 constexpr int kItems = HB_ITEMS;                       // odd: conflict-free blocked smem reads
 constexpr int kTile = kComputeThreads * kItems;        // records per tile (multiple of 16)
 constexpr int kStages = HB_STAGES;
