@@ -108,9 +108,17 @@ typedef struct {
     uint64_t host_elapsed_floor;/* max end of host records kept out of the SoA (0 if none) */
 } heteff_trace;
 
+/* heteff_options.flags bits */
+enum {
+    /* records not in canonical order are sorted on the GPU (K3, heteff_sort_records)
+       and the analysis re-run, instead of returning HETEFF_CONTRACT; list indices
+       still refer to the caller's input positions */
+    HETEFF_FLAG_SORT_IF_NEEDED = 1
+};
+
 typedef struct {
     int32_t mode;               /* heteff_mode */
-    int32_t reserved;
+    int32_t flags;              /* HETEFF_FLAG_* */
     uint64_t elapsed;           /* SUMMARIZE_DEVICE: the explicit elapsed window */
     int64_t list_capacity;      /* capacity of each heteff_outputs list (0 = counts only) */
 } heteff_options;
@@ -152,6 +160,31 @@ int heteff_analyze(heteff_ctx *ctx, const heteff_trace *trace, const heteff_opti
 /* trace columns in host memory (pinned for full PCIe rate); H2D inside */
 int heteff_analyze_host(heteff_ctx *ctx, const heteff_trace *trace, const heteff_options *opt,
                         heteff_result *result, const heteff_outputs *out, void *stream);
+
+/* K3: stable GPU radix sort of one record set (device memory) into the canonical
+ * order the analysis expects -- grouped by res ascending, start ascending within
+ * a resource, ties kept in input order.  Replaces the canonical sort of
+ * Trace.__post_init__ (model.py:74-80, 99-107) for columns that arrive unsorted
+ * (e.g. per-stream device activity concatenated).  `out` columns must not alias
+ * `in`; perm (optional, device memory, int64[count]) receives the input position
+ * of every output record. */
+typedef struct {
+    uint64_t *start;
+    uint64_t *end;
+    int32_t *res;
+    uint8_t *kind;
+} heteff_columns;
+
+typedef struct {
+    int32_t key_bits;           /* bits of the compressed (res, start) key */
+    int32_t passes;             /* onesweep digit passes */
+    int32_t wide;               /* 1: key did not fit 64 bits (two stable stages) */
+    int32_t start_sorted;       /* 1: input was start-ordered: sorted by res alone */
+    double ms;                  /* device time of the sort (CUDA events) */
+} heteff_sort_info;
+
+int heteff_sort_records(heteff_ctx *ctx, const heteff_records *in, const heteff_columns *out, int64_t *perm,
+                        heteff_sort_info *info, void *stream);
 
 /* overlap errors: cover index of each listed record (model.py:208-215), host memory */
 int heteff_overlap_covers(heteff_ctx *ctx, const heteff_trace *trace, int host_columns_on_host,

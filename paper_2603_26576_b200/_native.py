@@ -42,7 +42,7 @@ class TraceABI(C.Structure):
 
 
 class Options(C.Structure):
-    _fields_ = [("mode", C.c_int32), ("reserved", C.c_int32), ("elapsed", C.c_uint64),
+    _fields_ = [("mode", C.c_int32), ("flags", C.c_int32), ("elapsed", C.c_uint64),
                 ("list_capacity", C.c_int64)]
 
 
@@ -60,6 +60,19 @@ class Outputs(C.Structure):
     _fields_ = [("host_summaries", _p), ("device_summaries", _p), ("lists", _p * NUM_LISTS)]
 
 
+class Columns(C.Structure):
+    _fields_ = [("start", _p), ("end", _p), ("res", _p), ("kind", _p)]
+
+
+class SortInfo(C.Structure):
+    _fields_ = [("key_bits", C.c_int32), ("passes", C.c_int32), ("wide", C.c_int32), ("start_sorted", C.c_int32),
+                ("ms", C.c_double)]
+
+
+FLAG_SORT_IF_NEEDED = 1
+CONTRACT_HOST_ORDER, CONTRACT_DEV_ORDER, CONTRACT_HOST_KIND, CONTRACT_DEV_KIND = 1, 2, 4, 8
+
+
 class GenSide(C.Structure):
     _fields_ = [
         ("seed", C.c_uint64), ("n_res", C.c_int32), ("res_base", C.c_int32),
@@ -75,6 +88,7 @@ EXPORTED = (
     "heteff_abi_version", "heteff_create", "heteff_destroy", "heteff_last_error",
     "heteff_analyze", "heteff_analyze_host", "heteff_overlap_covers",
     "heteff_host_metrics", "heteff_device_metrics", "heteff_generate", "heteff_prof_read",
+    "heteff_sort_records",
 )
 
 _lib = None
@@ -107,6 +121,8 @@ def load() -> C.CDLL:
         f.argtypes = [_p, _p, C.c_int32, C.c_uint64, _p, C.POINTER(C.c_uint32), _p]
     lib.heteff_prof_read.restype = C.c_int
     lib.heteff_prof_read.argtypes = [_p, C.c_int]
+    lib.heteff_sort_records.restype = C.c_int
+    lib.heteff_sort_records.argtypes = [_p, C.POINTER(Records), C.POINTER(Columns), _p, C.POINTER(SortInfo), _p]
     lib.heteff_generate.restype = C.c_int
     lib.heteff_generate.argtypes = [_p, C.POINTER(GenSide), _p, _p, _p, _p, _p]
     _lib = lib

@@ -41,6 +41,8 @@ struct heteff_ctx {
     // staging for heteff_analyze_host / metrics; scratch of the overlap error path
     DevBuf stage, aux;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // K3 sort: workspace, sorted columns + permutations
+    DevBuf sort_ws, sorted;
 };
 
 static int fail(heteff_ctx *ctx, int code, const std::string &msg)
@@ -106,8 +108,8 @@ heteff_ctx *heteff_create(int device)
 void heteff_destroy(heteff_ctx *ctx)
 {
     if (!ctx) return;
-    DevBuf *bufs[] = {&ctx->host_acc, &ctx->dev_acc, &ctx->host_tiles, &ctx->dev_tiles,
-                      &ctx->host_out, &ctx->dev_out, &ctx->lists, &ctx->stage, &ctx->aux};
+    DevBuf *bufs[] = {&ctx->host_acc, &ctx->dev_acc, &ctx->host_tiles, &ctx->dev_tiles, &ctx->host_out,
+                      &ctx->dev_out, &ctx->lists, &ctx->stage, &ctx->aux, &ctx->sort_ws, &ctx->sorted};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->g) cudaFree(ctx->g);
@@ -122,8 +124,8 @@ const char *heteff_last_error(const heteff_ctx *ctx) { return ctx ? ctx->err.c_s
 
 static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-static int run_analysis(heteff_ctx *ctx, const heteff_trace *t, const heteff_options *opt, heteff_result *result,
-                        const heteff_outputs *out, cudaStream_t s)
+static int run_once(heteff_ctx *ctx, const heteff_trace *t, const heteff_options *opt, heteff_result *result,
+                    const heteff_outputs *out, cudaStream_t s, const int64_t *const perms[2] = nullptr)
 {
     if (!ctx || !t || !opt || !result) return fail(ctx, HETEFF_BAD_ARG, "null argument");
     if (t->host.count < 0 || t->dev.count < 0 || t->host_ids < 0 || t->dev_ids < 0 || t->n < 0 || t->m < 0 ||
@@ -230,6 +232,13 @@ static int run_analysis(heteff_ctx *ctx, const heteff_trace *t, const heteff_opt
         CK(cudaStreamSynchronize(s), "overlap pass");
     }
     const hb::ResultDev &r = *ctx->res_h;
+    if (perms && opt->list_capacity > 0) {   // sorted re-run: list entries back to input positions
+        for (int i = 0; i < 8; ++i) {
+            const int64_t k = r.counts[i] < opt->list_capacity ? r.counts[i] : opt->list_capacity;
+            const int64_t *pm = perms[i < 4 ? 0 : 1];
+            if (k > 0 && pm) CK(hb::launch_remap(p.lists[i], k, pm, s), "launch remap");
+        }
+    }
     if (out && opt->list_capacity > 0) {
         for (int i = 0; i < 8; ++i) {
             int64_t k = r.counts[i] < opt->list_capacity ? r.counts[i] : opt->list_capacity;
@@ -257,6 +266,105 @@ static int run_analysis(heteff_ctx *ctx, const heteff_trace *t, const heteff_opt
     result->kernel_ms = ms;
     ctx->err.clear();
     return r.status;
+}
+
+// sort one record set into ctx-owned columns (K3)
+static int sort_side(heteff_ctx *ctx, const heteff_records &in, heteff_columns &out, int64_t *perm,
+                     heteff_sort_info *info, cudaStream_t s)
+{
+    const int64_t n = in.count;
+    if (n <= 0) return HETEFF_OK;
+    const size_t need = hb::sort_workspace_bytes(n);
+    CK(ensure(ctx->sort_ws, need, false), "alloc sort workspace");
+    hb::SortStats st{};
+    CK(cudaEventRecord(ctx->ev0, s), "event");
+    CK(hb::sort_records((const u64 *)in.start, (const u64 *)in.end, in.res, in.kind, n, (u64 *)out.start,
+                        (u64 *)out.end, out.res, out.kind, perm,
+                        ctx->sort_ws.p, ctx->sort_ws.bytes, s, &st),
+       "sort records");
+    CK(cudaEventRecord(ctx->ev1, s), "event");
+    if (info) {
+        CK(cudaEventSynchronize(ctx->ev1), "sort");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        info->key_bits = st.key_bits;
+        info->passes = st.passes;
+        info->wide = st.wide;
+        info->start_sorted = st.start_sorted;
+        info->ms = ms;
+    }
+    return HETEFF_OK;
+}
+
+static int run_analysis(heteff_ctx *ctx, const heteff_trace *t, const heteff_options *opt, heteff_result *result,
+                        const heteff_outputs *out, cudaStream_t s)
+{
+    int rc = run_once(ctx, t, opt, result, out, s);
+    const int order = HETEFF_CONTRACT_HOST_ORDER | HETEFF_CONTRACT_DEV_ORDER;
+    if (rc != HETEFF_CONTRACT || !(opt->flags & HETEFF_FLAG_SORT_IF_NEEDED) || !(result->contract_flags & order))
+        return rc;
+    // K3: sort the offending side(s) into ctx-owned columns and analyze again
+    const bool sh = result->contract_flags & HETEFF_CONTRACT_HOST_ORDER;
+    const bool sd = result->contract_flags & HETEFF_CONTRACT_DEV_ORDER;
+    auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const int64_t hn = sh ? t->host.count : 0, dn = sd ? t->dev.count : 0;
+    const size_t bytes = up((size_t)hn * 29) + up((size_t)hn * 8) + up((size_t)dn * 29) + up((size_t)dn * 8) + 2048;
+    CK(ensure(ctx->sorted, bytes, false), "alloc sorted columns");
+    uint8_t *b = static_cast<uint8_t *>(ctx->sorted.p);
+    size_t o = 0;
+    auto take = [&](size_t x) { void *q = b + o; o += up(x); return q; };
+    heteff_trace ts = *t;
+    int64_t *perm[2] = {nullptr, nullptr};
+    const int64_t *perms[2] = {nullptr, nullptr};
+    const heteff_records *src[2] = {&t->host, &t->dev};
+    heteff_records *dst[2] = {&ts.host, &ts.dev};
+    const bool doit[2] = {sh, sd};
+    for (int side = 0; side < 2; ++side) {
+        if (!doit[side]) continue;
+        const int64_t n = src[side]->count;
+        heteff_columns c;
+        c.start = static_cast<uint64_t *>(take((size_t)n * 8));
+        c.end = static_cast<uint64_t *>(take((size_t)n * 8));
+        c.res = static_cast<int32_t *>(take((size_t)n * 4));
+        c.kind = static_cast<uint8_t *>(take((size_t)n));
+        perm[side] = static_cast<int64_t *>(take((size_t)n * 8));
+        perms[side] = perm[side];
+        if ((rc = sort_side(ctx, *src[side], c, perm[side], nullptr, s)) != HETEFF_OK) return rc;
+        dst[side]->start = c.start;
+        dst[side]->end = c.end;
+        dst[side]->res = c.res;
+        dst[side]->kind = c.kind;
+    }
+    rc = run_once(ctx, &ts, opt, result, out, s, perms);
+    if (result->contract_index >= 0 && result->contract_index < LLONG_MAX) {
+        const int side = (result->contract_flags & (HETEFF_CONTRACT_HOST_ORDER | HETEFF_CONTRACT_HOST_KIND)) ? 0 : 1;
+        if (perm[side]) {
+            int64_t orig = 0;
+            CK(cudaMemcpyAsync(&orig, perm[side] + result->contract_index, 8, cudaMemcpyDeviceToHost, s), "d2h");
+            CK(cudaStreamSynchronize(s), "sync");
+            result->contract_index = orig;
+        }
+    }
+    return rc;
+}
+
+int heteff_sort_records(heteff_ctx *ctx, const heteff_records *in, const heteff_columns *out, int64_t *perm,
+                        heteff_sort_info *info, void *stream)
+{
+    if (!ctx || !in || !out || in->count < 0) return fail(ctx, HETEFF_BAD_ARG, "bad argument");
+    if (in->count > 0 && (!in->start || !in->end || !in->res || !in->kind || !out->start || !out->end ||
+                          !out->res || !out->kind))
+        return fail(ctx, HETEFF_BAD_ARG, "null column");
+    if (in->count >= (int64_t)0xffffffffll) return fail(ctx, HETEFF_BAD_ARG, "record set too large for one sort");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    heteff_columns c = *out;
+    heteff_sort_info local{};
+    const int rc = sort_side(ctx, *in, c, perm, info ? info : &local, s);
+    if (rc != HETEFF_OK) return rc;
+    CK(cudaStreamSynchronize(s), "sort");
+    ctx->err.clear();
+    return HETEFF_OK;
 }
 
 int heteff_analyze(heteff_ctx *ctx, const heteff_trace *trace, const heteff_options *opt, heteff_result *result,

@@ -107,4 +107,14 @@ cudaError_t launch_metrics(const u64 *summaries, int32_t k, u64 elapsed, int hos
 cudaError_t launch_overlap_pass(const Params &p, u64 *scratch, cudaStream_t s);
 cudaError_t launch_covers(const Params &p, const int64_t *err_idx, int64_t count, int64_t *cover, cudaStream_t s);
 
+// K3 (sort.cu): stable radix sort of one record set by (res, start)
+struct SortStats {
+    int key_bits, passes, wide, start_sorted;
+};
+size_t sort_workspace_bytes(int64_t n);
+cudaError_t sort_records(const u64 *S, const u64 *E, const int32_t *R, const uint8_t *KD, int64_t n, u64 *os, u64 *oe,
+                         int32_t *orr, uint8_t *ok, int64_t *perm, void *ws, size_t ws_bytes, cudaStream_t s,
+                         SortStats *stats);
+cudaError_t launch_remap(int64_t *list, int64_t k, const int64_t *perm, cudaStream_t s);
+
 }  // namespace hb

@@ -1,0 +1,550 @@
+// sort.cu -- K3: stable LSD radix sort of one record set into the canonical
+// order the analysis kernel expects: grouped by resource id, start-sorted
+// within a resource (reference: Trace.__post_init__'s canonical sort,
+// model.py:74-80,99-107, and flatten's items.sort(), intervals.py:53).
+//
+// Keys are compressed before sorting: with s' = start - min(start) and
+// r' = flip(res) - min(flip(res)) (flip = sign-bit flip so negative ids order
+// first), a record's key is (r' << bt) | s' where bt = bits(max s').  When
+// bits(r') + bt <= 64 (the normal case) one u64 key carries both, and the
+// sorted key alone reconstructs start and res -- only end and kind are
+// gathered through the permutation at the end.  Otherwise the sort runs in two
+// stable stages (by s', then by r').
+//
+// Each digit pass is reduce-then-scan: an upsweep kernel counts the digits of
+// every tile (digit-major count matrix), a three-kernel scan turns the matrix
+// into the global position of every (digit, tile) run, and the downsweep
+// kernel ranks its tile's keys stably with warp-level match/popc (warp-striped
+// items, warps in order), reorders the tile in shared memory and writes digit
+// runs back coalesced.  No inter-CTA chain: every tile is independent, so the
+// passes stay bandwidth-bound (a decoupled look-back variant measured 2-4x
+// slower here -- its per-tile chain, not HBM, was the limit).
+//
+// Ties (equal res and start) keep their input order.  Summaries and metrics
+// do not depend on tie order (the union and the sums are order-free;
+// SURVEY.md appendix A.5).
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "engine.cuh"
+#include "ptx.cuh"
+
+namespace hb {
+namespace rsort {
+
+constexpr int kT = 512;                 // threads per CTA (2 CTAs / SM)
+constexpr int kW = kT / 32;
+constexpr int kI = 15;                  // keys per thread
+constexpr int kTileKeys = kT * kI;      // 7680 keys per tile
+constexpr int kBins = 256;              // <= 8-bit digits
+
+struct Range {
+    u64 smin, smax;
+    unsigned int rmin, rmax;            // flipped domain
+    unsigned int start_desc;            // some start is below its predecessor's
+    unsigned int pad;
+};
+
+__device__ __forceinline__ unsigned int flip(int32_t r) { return (unsigned int)r ^ 0x80000000u; }
+__device__ __forceinline__ int32_t unflip(unsigned int r) { return (int32_t)(r ^ 0x80000000u); }
+
+// ---------------------------------------------------------------------------
+// range of start / res
+// ---------------------------------------------------------------------------
+__global__ void range_init(Range *g)
+{
+    g->smin = ~0ull;
+    g->smax = 0;
+    g->rmin = 0xffffffffu;
+    g->rmax = 0;
+    g->start_desc = 0;
+}
+
+__global__ void __launch_bounds__(512) range_kernel(const u64 *__restrict__ S, const int32_t *__restrict__ R,
+                                                    int64_t n, Range *g)
+{
+    u64 smin = ~0ull, smax = 0;
+    unsigned int rmin = 0xffffffffu, rmax = 0;
+    bool desc = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const u64 s = __ldg(S + i);
+        if (i > 0) desc = desc || __ldg(S + i - 1) > s;
+        const unsigned int r = flip(__ldcs(R + i));
+        smin = umin(smin, s);
+        smax = umax(smax, s);
+        rmin = min(rmin, r);
+        rmax = max(rmax, r);
+    }
+    // 64-bit warp reductions by shuffles (the kernel is bandwidth-bound)
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        smin = umin(smin, __shfl_xor_sync(0xffffffffu, smin, d));
+        smax = umax(smax, __shfl_xor_sync(0xffffffffu, smax, d));
+    }
+    rmin = __reduce_min_sync(0xffffffffu, rmin);
+    rmax = __reduce_max_sync(0xffffffffu, rmax);
+    desc = __any_sync(0xffffffffu, desc);
+    if ((threadIdx.x & 31) == 0) {
+        if (desc) atomicOr(&g->start_desc, 1u);
+        atomicMin(&g->smin, smin);
+        atomicMax(&g->smax, smax);
+        atomicMin(&g->rmin, rmin);
+        atomicMax(&g->rmax, rmax);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// key building + every pass's global digit histogram
+// ---------------------------------------------------------------------------
+struct KeyPlan {
+    u64 smin;
+    unsigned int rmin;
+    int bt;            // bits of the start offset
+    int wide;          // 1: stage 1 keys are s' only (res sorted in stage 2)
+    int res_only;      // 1: input already start-sorted: one stable sort by r' suffices
+    int passes;        // digit passes of this stage
+    int dbits;         // bits per digit
+};
+
+__device__ __forceinline__ u64 make_key(const KeyPlan &kp, u64 s, int32_t r)
+{
+    const u64 so = s - kp.smin;
+    if (kp.res_only) return (u64)(flip(r) - kp.rmin);
+    if (kp.wide || kp.bt >= 64) return so;
+    return ((u64)(flip(r) - kp.rmin) << kp.bt) | so;
+}
+
+__global__ void __launch_bounds__(512) build_keys(const u64 *__restrict__ S, const int32_t *__restrict__ R, int64_t n,
+                                                  KeyPlan kp, u64 *__restrict__ K, uint32_t *__restrict__ V)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        K[i] = make_key(kp, __ldcs(S + i), __ldcs(R + i));
+        V[i] = (uint32_t)i;
+    }
+}
+
+// wide keys, stage 2: r' of each record in stage-1 order
+__global__ void __launch_bounds__(512) build_res_keys(const int32_t *__restrict__ R, const uint32_t *__restrict__ V,
+                                                      int64_t n, KeyPlan kp, u64 *__restrict__ K)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        K[i] = (u64)(flip(__ldg(R + V[i])) - kp.rmin);
+}
+
+// ---------------------------------------------------------------------------
+// one digit pass
+// ---------------------------------------------------------------------------
+struct PassSmem {
+    u64 k[kTileKeys];
+    uint32_t v[kTileKeys];
+    uint32_t whist[kW][kBins];   // per-warp digit counts -> warp-exclusive offsets
+    uint32_t bexcl[kBins];       // tile-local exclusive digit offsets
+    uint32_t gbase[kBins];       // destination of the tile's first key of each digit
+    uint32_t wsum[kW];
+};
+
+// exclusive scan of one value per thread t < kBins (all threads must call)
+__device__ __forceinline__ uint32_t block_excl_scan_bins(uint32_t x, uint32_t *wsum, int tid)
+{
+    const int lane = tid & 31, warp = tid >> 5;
+    uint32_t inc = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+    }
+    __syncthreads();
+    if (tid < kBins && lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    uint32_t off = 0;
+    if (tid < kBins)
+        for (int w = 0; w < warp; ++w) off += wsum[w];
+    return off + inc - x;
+}
+
+// per-tile digit counts of one pass, digit-major: counts[d * tiles + t].
+// Warp-private shared counters (atomics conflict only inside a warp); a
+// 256-thread CTA per tile keeps more tiles' loads in flight per SM.
+constexpr int kUT = 256, kUW = kUT / 32, kUI = kTileKeys / kUT;
+__global__ void __launch_bounds__(kUT) upsweep(const u64 *__restrict__ kin, int64_t n, int shift, int dbits,
+                                               uint32_t *__restrict__ counts, int64_t tiles)
+{
+    __shared__ uint32_t h[kUW][kBins];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t bins = 1u << dbits;
+    const u64 mask = bins - 1;
+    for (int i = tid; i < kUW * kBins; i += kUT) (&h[0][0])[i] = 0;
+    __syncthreads();
+    const int64_t tile = blockIdx.x;
+    const int64_t base = tile * kTileKeys;
+    const int cnt = (int)((n - base) < kTileKeys ? (n - base) : kTileKeys);
+    const u64 *kt = kin + base;
+    if (cnt == kTileKeys) {
+        u64 k[kUI];
+#pragma unroll
+        for (int j = 0; j < kUI; ++j) k[j] = __ldcs(kt + j * kUT + tid);
+#pragma unroll
+        for (int j = 0; j < kUI; ++j) atomicAdd(&h[warp][(uint32_t)((k[j] >> shift) & mask)], 1u);
+    } else {
+        for (int i = tid; i < cnt; i += kUT) atomicAdd(&h[warp][(uint32_t)((__ldcs(kt + i) >> shift) & mask)], 1u);
+    }
+    __syncthreads();
+    for (int d = tid; d < (int)bins; d += kUT) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int w = 0; w < kUW; ++w) c += h[w][d];
+        counts[(int64_t)d * tiles + tile] = c;
+    }
+}
+
+// exclusive scan of the digit-major count matrix (global positions of every
+// (digit, tile) run): block sums, a one-block scan of those, then the blocks
+constexpr int kScanT = 1024, kScanI = 4, kScanBlock = kScanT * kScanI;
+
+__device__ __forceinline__ uint32_t block_scan_excl_1024(uint32_t x, uint32_t *ws, uint32_t &total)
+{
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t inc = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+    }
+    if (lane == 31) ws[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t v = ws[lane], vi = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, vi, d);
+            if (lane >= d) vi += o;
+        }
+        ws[lane] = vi - v;
+        if (lane == 31) ws[32] = vi;
+    }
+    __syncthreads();
+    const uint32_t r = ws[warp] + inc - x;
+    total = ws[32];
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(kScanT) scan_sums(const uint32_t *__restrict__ c, int64_t m, uint32_t *__restrict__ bsum)
+{
+    __shared__ uint32_t ws[33];
+    const int64_t b0 = (int64_t)blockIdx.x * kScanBlock;
+    uint32_t acc = 0;
+#pragma unroll
+    for (int q = 0; q < kScanI; ++q) {
+        const int64_t i = b0 + (int64_t)q * kScanT + threadIdx.x;
+        acc += i < m ? c[i] : 0u;
+    }
+    uint32_t total;
+    block_scan_excl_1024(acc, ws, total);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kScanT) scan_top(uint32_t *bsum, int64_t nb)
+{
+    __shared__ uint32_t ws[33];
+    uint32_t carry = 0;
+    for (int64_t b0 = 0; b0 < nb; b0 += kScanT) {
+        const int64_t i = b0 + threadIdx.x;
+        const uint32_t x = i < nb ? bsum[i] : 0u;
+        uint32_t total;
+        const uint32_t ex = block_scan_excl_1024(x, ws, total);
+        if (i < nb) bsum[i] = carry + ex;
+        carry += total;
+    }
+}
+
+__global__ void __launch_bounds__(kScanT) scan_blocks(uint32_t *c, int64_t m, const uint32_t *__restrict__ bsum)
+{
+    __shared__ uint32_t ws[33];
+    const int64_t b0 = (int64_t)blockIdx.x * kScanBlock + (int64_t)threadIdx.x * kScanI;   // blocked
+    uint32_t v[kScanI], acc = 0;
+#pragma unroll
+    for (int q = 0; q < kScanI; ++q) {
+        v[q] = b0 + q < m ? c[b0 + q] : 0u;
+        acc += v[q];
+    }
+    uint32_t total;
+    uint32_t run = bsum[blockIdx.x] + block_scan_excl_1024(acc, ws, total);
+#pragma unroll
+    for (int q = 0; q < kScanI; ++q) {
+        if (b0 + q < m) c[b0 + q] = run;
+        run += v[q];
+    }
+}
+
+// lanes holding the same digit as this lane, from dbits ballots (faster than
+// match.any on this part, measured: the upsweep went 348 -> 61 us without it)
+__device__ __forceinline__ uint32_t peers_of(uint32_t d, int dbits, uint32_t valid_mask)
+{
+    uint32_t m = valid_mask;
+#pragma unroll 8
+    for (int b = 0; b < 8; ++b) {
+        if (b < dbits) {
+            const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+            m &= ((d >> b) & 1u) ? bb : ~bb;
+        }
+    }
+    return m;
+}
+
+// one digit pass: stable rank of the tile's keys, reorder in shared memory,
+// coalesced digit runs to their scanned global positions
+__global__ void __launch_bounds__(kT, 2) downsweep(const u64 *__restrict__ kin, const uint32_t *__restrict__ vin,
+                                                   u64 *__restrict__ kout, uint32_t *__restrict__ vout, int64_t n,
+                                                   int shift, int dbits, const uint32_t *__restrict__ offs,
+                                                   int64_t tiles)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    PassSmem &sm = *reinterpret_cast<PassSmem *>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t bins = 1u << dbits;
+    const u64 mask = bins - 1;
+    const int64_t tile = blockIdx.x;
+    for (int i = tid; i < kW * kBins; i += kT) (&sm.whist[0][0])[i] = 0;
+    for (int d = tid; d < (int)bins; d += kT) sm.gbase[d] = offs[(int64_t)d * tiles + tile];
+    __syncthreads();
+    const int64_t base = tile * kTileKeys;
+    const int64_t wbase = base + (int64_t)warp * 32 * kI;
+    const int64_t wrem64 = n - wbase;   // records of this warp's slice still in range
+    const int wrem = wrem64 <= 0 ? 0 : (wrem64 > 32 * kI ? 32 * kI : (int)wrem64);
+    const u64 *kw = kin + wbase;
+
+    u64 k[kI];
+    uint32_t rk[(kI + 1) / 2];   // warp ranks (< 2^9), two per register
+#pragma unroll
+    for (int j = 0; j < kI; ++j) {
+        const int o = j * 32 + lane;
+        k[j] = o < wrem ? __ldcs(kw + o) : 0ull;
+    }
+    // stable warp-level ranking (items j, then lanes, are in input order);
+    // invalid lanes carry a digit no valid lane has, so the match never diverges
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int j = 0; j < (kI + 1) / 2; ++j) rk[j] = 0;
+#pragma unroll
+    for (int j = 0; j < kI; ++j) {
+        const bool valid = j * 32 + lane < wrem;
+        const uint32_t dj = (uint32_t)((k[j] >> shift) & mask);
+        const uint32_t pm = peers_of(dj, dbits, __ballot_sync(0xffffffffu, valid));
+        const int leader = __ffs(pm) - 1;
+        const uint32_t b = valid ? sm.whist[warp][dj] : 0u;
+        __syncwarp();
+        if (valid && lane == leader) sm.whist[warp][dj] = b + __popc(pm);
+        __syncwarp();
+        rk[j >> 1] |= (b + __popc(pm & lt)) << (16 * (j & 1));
+    }
+    __syncthreads();
+    // per digit: warp-exclusive offsets and the tile total
+    uint32_t total = 0;
+    if (tid < (int)bins) {
+        uint32_t run = 0;
+#pragma unroll
+        for (int w = 0; w < kW; ++w) {
+            const uint32_t c = sm.whist[w][tid];
+            sm.whist[w][tid] = run;
+            run += c;
+        }
+        total = run;
+    }
+    {
+        const uint32_t ex = block_excl_scan_bins(total, sm.wsum, tid);
+        if (tid < kBins) sm.bexcl[tid] = ex;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kI; ++j) {
+        const int o = j * 32 + lane;
+        if (o < wrem) {
+            const uint32_t dj = (uint32_t)((k[j] >> shift) & mask);
+            const uint32_t pos = sm.bexcl[dj] + sm.whist[warp][dj] + ((rk[j >> 1] >> (16 * (j & 1))) & 0xffffu);
+            sm.k[pos] = k[j];
+            sm.v[pos] = __ldcs(vin + wbase + o);
+        }
+    }
+    __syncthreads();
+    const int cnt = (int)((n - base) < kTileKeys ? (n - base) : kTileKeys);
+    for (int i = tid; i < cnt; i += kT) {
+        const u64 key = sm.k[i];
+        const uint32_t dd = (uint32_t)((key >> shift) & mask);
+        const u64 dst = (u64)sm.gbase[dd] + (u64)(i - (int)sm.bexcl[dd]);
+        kout[dst] = key;
+        vout[dst] = sm.v[i];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// output columns
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) finish_narrow(const u64 *__restrict__ K, const uint32_t *__restrict__ V,
+                                                     int64_t n, KeyPlan kp, const u64 *__restrict__ E,
+                                                     const uint8_t *__restrict__ KD, u64 *__restrict__ os,
+                                                     u64 *__restrict__ oe, int32_t *__restrict__ orr,
+                                                     uint8_t *__restrict__ ok, int64_t *__restrict__ perm)
+{
+    const u64 tmask = kp.bt >= 64 ? ~0ull : ((1ull << kp.bt) - 1);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const u64 key = __ldcs(K + i);
+        const uint32_t v = __ldcs(V + i);
+        os[i] = (key & tmask) + kp.smin;
+        orr[i] = unflip((kp.bt >= 64 ? 0u : (unsigned int)(key >> kp.bt)) + kp.rmin);
+        oe[i] = __ldg(E + v);
+        ok[i] = __ldg(KD + v);
+        if (perm) perm[i] = v;
+    }
+}
+
+__global__ void __launch_bounds__(512) finish_gather(const uint32_t *__restrict__ V, int64_t n,
+                                                     const u64 *__restrict__ S, const u64 *__restrict__ E,
+                                                     const int32_t *__restrict__ R, const uint8_t *__restrict__ KD,
+                                                     u64 *__restrict__ os, u64 *__restrict__ oe,
+                                                     int32_t *__restrict__ orr, uint8_t *__restrict__ ok,
+                                                     int64_t *__restrict__ perm)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = __ldcs(V + i);
+        os[i] = __ldg(S + v);
+        oe[i] = __ldg(E + v);
+        orr[i] = __ldg(R + v);
+        ok[i] = __ldg(KD + v);
+        if (perm) perm[i] = v;
+    }
+}
+
+__global__ void remap_kernel(int64_t *list, int64_t k, const int64_t *__restrict__ perm)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+        list[i] = perm[list[i]];
+}
+
+}  // namespace rsort
+
+cudaError_t launch_remap(int64_t *list, int64_t k, const int64_t *perm, cudaStream_t s)
+{
+    const int64_t g = (k + 255) / 256;
+    rsort::remap_kernel<<<(unsigned)(g > 4096 ? 4096 : g), 256, 0, s>>>(list, k, perm);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------
+static size_t up256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static int64_t tiles_of(int64_t n) { return (n + rsort::kTileKeys - 1) / rsort::kTileKeys; }
+
+size_t sort_workspace_bytes(int64_t n)
+{
+    const int64_t m = tiles_of(n) * rsort::kBins;
+    return 2 * up256((size_t)n * 8) + 2 * up256((size_t)n * 4) + up256((size_t)m * 4) +
+           up256((size_t)(m / rsort::kScanBlock + 1) * 4) + up256(sizeof(rsort::Range));
+}
+
+static int bits_of(u64 x) { return x ? 64 - __builtin_clzll(x) : 0; }
+
+static int grid_for(int64_t n, int sms)
+{
+    int64_t g = (n + 511) / 512;
+    const int64_t cap = (int64_t)sms * 8;
+    if (g > cap) g = cap;
+    return g < 1 ? 1 : (int)g;
+}
+
+cudaError_t sort_records(const u64 *S, const u64 *E, const int32_t *R, const uint8_t *KD, int64_t n, u64 *os, u64 *oe,
+                         int32_t *orr, uint8_t *ok, int64_t *perm, void *ws, size_t ws_bytes, cudaStream_t s,
+                         SortStats *stats)
+{
+    using namespace rsort;
+    if (n <= 0) return cudaSuccess;
+    if (n >= (int64_t)0xffffffffll) return cudaErrorInvalidValue;          // 32-bit permutation indices
+    if (ws_bytes < sort_workspace_bytes(n)) return cudaErrorInvalidValue;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(downsweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sizeof(PassSmem));
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    const int64_t tiles = tiles_of(n);
+    const int64_t m = tiles * kBins;
+    const int64_t nb = (m + kScanBlock - 1) / kScanBlock;
+    uint8_t *b = static_cast<uint8_t *>(ws);
+    size_t o = 0;
+    auto take = [&](size_t bytes) { void *p = b + o; o += up256(bytes); return p; };
+    u64 *K0 = static_cast<u64 *>(take((size_t)n * 8));
+    u64 *K1 = static_cast<u64 *>(take((size_t)n * 8));
+    uint32_t *V0 = static_cast<uint32_t *>(take((size_t)n * 4));
+    uint32_t *V1 = static_cast<uint32_t *>(take((size_t)n * 4));
+    uint32_t *counts = static_cast<uint32_t *>(take((size_t)m * 4));
+    uint32_t *bsum = static_cast<uint32_t *>(take((size_t)(m / kScanBlock + 1) * 4));
+    Range *range = static_cast<Range *>(take(sizeof(Range)));
+    cudaError_t e;
+
+    // 1. key range (one D2H of 32 bytes decides the key layout)
+    range_init<<<1, 1, 0, s>>>(range);
+    range_kernel<<<grid_for(n, sms), 512, 0, s>>>(S, R, n, range);
+    Range rg;
+    if ((e = cudaMemcpyAsync(&rg, range, sizeof(Range), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    const int bt = bits_of(rg.smax - rg.smin);
+    const int br = bits_of((u64)(rg.rmax - rg.rmin));
+    KeyPlan kp;
+    kp.smin = rg.smin;
+    kp.rmin = rg.rmin;
+    kp.bt = bt;
+    // input already ordered by start (e.g. a globally time-ordered event log):
+    // a stable sort by resource alone yields the canonical order
+    kp.res_only = rg.start_desc ? 0 : 1;
+    kp.wide = (!kp.res_only && bt + br > 64) ? 1 : 0;
+    const int stage_bits[2] = {kp.res_only ? br : (kp.wide ? bt : bt + br), kp.wide ? br : 0};
+
+    u64 *kin = K0, *kout = K1;
+    uint32_t *vin = V0, *vout = V1;
+    int total_passes = 0;
+    for (int stage = 0; stage < 2; ++stage) {
+        const int bits = stage_bits[stage];
+        if (stage == 1 && !kp.wide) break;
+        const int passes = bits == 0 ? 0 : (bits + 7) / 8;
+        kp.passes = passes;
+        kp.dbits = passes ? (bits + passes - 1) / passes : 1;
+        if (stage == 0) build_keys<<<grid_for(n, sms), 512, 0, s>>>(S, R, n, kp, kin, vin);
+        else build_res_keys<<<grid_for(n, sms), 512, 0, s>>>(R, vin, n, kp, kin);
+        for (int p = 0; p < passes; ++p) {
+            const int shift = p * kp.dbits;
+            const int64_t mm = ((int64_t)1 << kp.dbits) * tiles;   // this pass's matrix (digit-major)
+            const int64_t nbb = (mm + kScanBlock - 1) / kScanBlock;
+            upsweep<<<(unsigned)tiles, kUT, 0, s>>>(kin, n, shift, kp.dbits, counts, tiles);
+            scan_sums<<<(unsigned)nbb, kScanT, 0, s>>>(counts, mm, bsum);
+            scan_top<<<1, kScanT, 0, s>>>(bsum, nbb);
+            scan_blocks<<<(unsigned)nbb, kScanT, 0, s>>>(counts, mm, bsum);
+            downsweep<<<(unsigned)tiles, kT, sizeof(PassSmem), s>>>(kin, vin, kout, vout, n, shift, kp.dbits, counts,
+                                                                    tiles);
+            u64 *tk = kin; kin = kout; kout = tk;
+            uint32_t *tv = vin; vin = vout; vout = tv;
+            ++total_passes;
+        }
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    (void)nb;
+    if (!kp.wide && !kp.res_only) {
+        finish_narrow<<<grid_for(n, sms), 512, 0, s>>>(kin, vin, n, kp, E, KD, os, oe, orr, ok, perm);
+    } else {
+        finish_gather<<<grid_for(n, sms), 512, 0, s>>>(vin, n, S, E, R, KD, os, oe, orr, ok, perm);
+    }
+    if (stats) {
+        stats->key_bits = kp.res_only ? br : bt + br;
+        stats->passes = total_passes;
+        stats->wide = kp.wide;
+        stats->start_sorted = kp.res_only;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace hb

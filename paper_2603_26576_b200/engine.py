@@ -64,7 +64,7 @@ def _check(ctx, rc):
 
 
 def analyze_packed(packed: PackedTrace, mode: int, elapsed: int = 0, want_lists: bool = True,
-                   capacity: int = 1 << 14, device: int | None = None) -> Findings:
+                   capacity: int = 1 << 14, device: int | None = None, sort_if_needed: bool = False) -> Findings:
     """Run the engine on a host-resident packed trace (copies inside the call)."""
     ctx = N.context(device)
     lib = N.load()
@@ -81,7 +81,7 @@ def analyze_packed(packed: PackedTrace, mode: int, elapsed: int = 0, want_lists:
         out = N.Outputs(_ptr(host_sum), _ptr(dev_sum),
                         (C.c_void_p * N.NUM_LISTS)(*[_ptr(x) for x in lists]) if cap
                         else (C.c_void_p * N.NUM_LISTS)())
-        opt = N.Options(mode, 0, elapsed, cap)
+        opt = N.Options(mode, N.FLAG_SORT_IF_NEEDED if sort_if_needed else 0, elapsed, cap)
         res = N.Result()
         rc = lib.heteff_analyze_host(ctx, C.byref(t), C.byref(opt), C.byref(res), C.byref(out), None)
         _check(ctx, rc)
@@ -164,8 +164,12 @@ def device_trace_abi(dt: DeviceTrace) -> N.TraceABI:
 
 def analyze_device(dt: DeviceTrace, mode: int = N.MODE_REPORT, elapsed: int = 0, stream: int | None = None,
                    device: int | None = None, host_sum: np.ndarray | None = None,
-                   dev_sum: np.ndarray | None = None) -> Findings:
-    """Analyze HBM-resident columns (counts only, no per-record lists)."""
+                   dev_sum: np.ndarray | None = None, sort_if_needed: bool = False) -> Findings:
+    """Analyze HBM-resident columns (counts only, no per-record lists).
+
+    ``sort_if_needed``: columns that are not in canonical order are sorted on the
+    GPU (K3, :func:`sort_records`) and analyzed again instead of failing with
+    ``CONTRACT``."""
     ctx = N.context(device)
     lib = N.load()
     t = device_trace_abi(dt)
@@ -174,7 +178,7 @@ def analyze_device(dt: DeviceTrace, mode: int = N.MODE_REPORT, elapsed: int = 0,
     if dev_sum is None:
         dev_sum = np.zeros((max(dt.m, 1), 4), dtype=np.uint64)
     out = N.Outputs(_ptr(host_sum), _ptr(dev_sum), (C.c_void_p * N.NUM_LISTS)())
-    opt = N.Options(mode, 0, elapsed, 0)
+    opt = N.Options(mode, N.FLAG_SORT_IF_NEEDED if sort_if_needed else 0, elapsed, 0)
     res = N.Result()
     rc = lib.heteff_analyze(ctx, C.byref(t), C.byref(opt), C.byref(res), C.byref(out), stream)
     _check(ctx, rc)
@@ -182,7 +186,7 @@ def analyze_device(dt: DeviceTrace, mode: int = N.MODE_REPORT, elapsed: int = 0,
 
 
 def analyze_host_columns(dt: DeviceTrace, mode: int = N.MODE_REPORT, stream: int | None = None,
-                         device: int | None = None) -> Findings:
+                         device: int | None = None, sort_if_needed: bool = False) -> Findings:
     """Same as :func:`analyze_device` but the columns are HOST tensors (pinned); H2D inside."""
     ctx = N.context(device)
     lib = N.load()
@@ -190,8 +194,49 @@ def analyze_host_columns(dt: DeviceTrace, mode: int = N.MODE_REPORT, stream: int
     host_sum = np.zeros((max(dt.n, 1), 4), dtype=np.uint64)
     dev_sum = np.zeros((max(dt.m, 1), 4), dtype=np.uint64)
     out = N.Outputs(_ptr(host_sum), _ptr(dev_sum), (C.c_void_p * N.NUM_LISTS)())
-    opt = N.Options(mode, 0, 0, 0)
+    opt = N.Options(mode, N.FLAG_SORT_IF_NEEDED if sort_if_needed else 0, 0, 0)
     res = N.Result()
     rc = lib.heteff_analyze_host(ctx, C.byref(t), C.byref(opt), C.byref(res), C.byref(out), stream)
     _check(ctx, rc)
     return _findings(res, host_sum[: dt.n], dev_sum[: dt.m], [])
+
+
+@dataclass
+class SortResult:
+    start: object
+    end: object
+    res: object
+    kind: object
+    perm: object           # int64: input position of each output record
+    key_bits: int
+    passes: int
+    wide: bool
+    start_sorted: bool     # input was start-ordered: sorted by res alone
+    ms: float
+
+
+def sort_records(start, end, res, kind, stream: int | None = None, device: int | None = None) -> SortResult:
+    """K3: stable GPU sort of one record set (CUDA tensors) by (res, start).
+
+    The canonical order of ``Trace.__post_init__`` (``model.py:74-80,99-107``)
+    for columns that arrive unsorted; ties keep their input order."""
+    import torch
+
+    ctx = N.context(device)
+    lib = N.load()
+    n = int(start.numel())
+    dev = start.device
+    os_ = torch.empty(n, dtype=torch.int64, device=dev)   # u64 bits
+    oe = torch.empty(n, dtype=torch.int64, device=dev)
+    orr = torch.empty(n, dtype=torch.int32, device=dev)
+    ok = torch.empty(n, dtype=torch.uint8, device=dev)
+    perm = torch.empty(n, dtype=torch.int64, device=dev)
+    rec = N.Records(_dptr(start), _dptr(end), _dptr(res), _dptr(kind), n)
+    cols = N.Columns(_dptr(os_), _dptr(oe), _dptr(orr), _dptr(ok))
+    info = N.SortInfo()
+    rc = lib.heteff_sort_records(ctx, C.byref(rec), C.byref(cols), _dptr(perm), C.byref(info), stream)
+    _check(ctx, rc)
+    if rc != N.OK:
+        raise N.NativeError(f"sort failed ({rc}): {N.last_error(ctx)}")
+    return SortResult(os_, oe, orr, ok, perm, info.key_bits, info.passes, bool(info.wide),
+                      bool(info.start_sorted), info.ms)
