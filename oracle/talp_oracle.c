@@ -503,3 +503,123 @@ double orc_div_exact_u64x2(uint64_t a_hi, uint64_t a_lo, uint64_t b_hi, uint64_t
 
 size_t orc_in_size(void) { return sizeof(orc_in); }
 size_t orc_out_size(void) { return sizeof(orc_out); }
+
+/* ------------------------------------------------------------------ */
+/* EXTENSIONS (not in the reference)      */
+/*                                                                     */
+/* Monitoring regions: region j is a window [a_j, b_j).  Its trace is   */
+/* the full trace with every record intersected with the window         */
+/* (intervals.py:98-105 semantics: empty results dropped) and shifted   */
+/* by -a_j; a zero-length record is kept iff a_j <= s < b_j.  The       */
+/* region's metric tree is compute_report (metrics.py:125-154) of that  */
+/* trace -- restated here by literally building it and calling          */
+/* orc_analyze.                                                         */
+/*                                                                     */
+/* Offload-wait / device-busy overlap, per device g with owner rank p:  */
+/*   busy_g = |A_p  ∩  B_g|, A_p = flatten(offload records of p)        */
+/*   ∩ [0,E), B_g = flatten(records of g) ∩ [0,E), computed as          */
+/*   |A| - |subtract(A, B)| with the intervals.py:40-105 restatements;  */
+/*   fraction = sum_g busy_g / sum_g d_offload(owner(g)).               */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    const uint64_t *win_start, *win_end;
+    int32_t count;
+    const int32_t *dev_owner;            /* [d_ids] dense host id owning the device, -1 none */
+} orc_regions_in;
+
+typedef struct {
+    int32_t *status;                     /* [R] ORC_OK / ORC_ANALYSIS (E == 0) / ... */
+    uint64_t *elapsed;                   /* [R] */
+    uint64_t *host_sum;                  /* [R][n][4] */
+    uint64_t *dev_sum;                   /* [R][m][4] */
+    uint64_t *busy;                      /* [R][m] */
+    double *host_m; uint32_t *host_mask; /* [R][5], [R] */
+    double *dev_m; uint32_t *dev_mask;   /* [R][4], [R] */
+    double *busy_frac; uint32_t *busy_mask; /* [R], [R] */
+} orc_regions_out;
+
+/* clip one record set to [a, b), shifted; returns the kept count */
+static int64_t clip_records(const uint64_t *s, const uint64_t *e, const int32_t *r, const uint8_t *k, int64_t n,
+                            uint64_t a, uint64_t b, uint64_t *os, uint64_t *oe, int32_t *orr, uint8_t *ok)
+{
+    int64_t w = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        uint64_t cs, ce;
+        if (s[i] == e[i]) {
+            if (!(s[i] >= a && s[i] < b)) continue;
+            cs = ce = s[i];
+        } else {
+            cs = s[i] > a ? s[i] : a;
+            ce = e[i] < b ? e[i] : b;
+            if (!(cs < ce)) continue;
+        }
+        os[w] = cs - a; oe[w] = ce - a; orr[w] = r[i]; ok[w] = k[i]; ++w;
+    }
+    return w;
+}
+
+/* records of dense id `id` in a canonical (res-grouped) set, optionally one kind, as intervals */
+static int64_t gather_ivs(const uint64_t *s, const uint64_t *e, const int32_t *r, const uint8_t *k, int64_t n,
+                          int32_t id, int kind, iv_t *out)
+{
+    int64_t w = 0;
+    for (int64_t i = 0; i < n; ++i)
+        if (r[i] == id && (kind < 0 || k[i] == kind)) { out[w].s = s[i]; out[w].e = e[i]; ++w; }
+    return w;
+}
+
+int orc_regions(const orc_in *in, const orc_regions_in *rg, orc_regions_out *o)
+{
+    const int64_t hn = in->h_count, dn = in->d_count;
+    const int32_t n = in->n, m = in->m;
+    uint64_t *hs = malloc(8 * (size_t)(hn + 1)), *he = malloc(8 * (size_t)(hn + 1));
+    int32_t *hr = malloc(4 * (size_t)(hn + 1)); uint8_t *hk = malloc((size_t)hn + 1);
+    uint64_t *ds = malloc(8 * (size_t)(dn + 1)), *de = malloc(8 * (size_t)(dn + 1));
+    int32_t *dr = malloc(4 * (size_t)(dn + 1)); uint8_t *dk = malloc((size_t)dn + 1);
+    iv_t *A = malloc(sizeof(iv_t) * (size_t)(hn + 1)), *B = malloc(sizeof(iv_t) * (size_t)(dn + 1));
+    iv_t *D = malloc(sizeof(iv_t) * (size_t)(hn + dn + 1));
+    if (!hs || !he || !hr || !hk || !ds || !de || !dr || !dk || !A || !B || !D) return ORC_NOMEM;
+    for (int32_t j = 0; j < rg->count; ++j) {
+        const uint64_t a = rg->win_start[j], b = rg->win_end[j];
+        const int64_t kh = clip_records(in->h_start, in->h_end, in->h_res, in->h_kind, hn, a, b, hs, he, hr, hk);
+        const int64_t kd = clip_records(in->d_start, in->d_end, in->d_res, in->d_kind, dn, a, b, ds, de, dr, dk);
+        orc_in ri = *in;
+        ri.h_start = hs; ri.h_end = he; ri.h_res = hr; ri.h_kind = hk; ri.h_count = kh;
+        ri.d_start = ds; ri.d_end = de; ri.d_res = dr; ri.d_kind = dk; ri.d_count = kd;
+        ri.mode = MODE_REPORT; ri.cap = 0; ri.host_elapsed_floor = 0;
+        orc_out ro; memset(&ro, 0, sizeof(ro));
+        ro.host_sum = o->host_sum + (size_t)j * (size_t)(n > 0 ? n : 1) * 4;
+        ro.dev_sum = o->dev_sum + (size_t)j * (size_t)(m > 0 ? m : 1) * 4;
+        o->status[j] = orc_analyze(&ri, &ro);
+        o->elapsed[j] = ro.elapsed;
+        for (int q = 0; q < 5; ++q) o->host_m[5 * j + q] = ro.host_m[q];
+        for (int q = 0; q < 4; ++q) o->dev_m[4 * j + q] = ro.dev_m[q];
+        o->host_mask[j] = ro.host_mask; o->dev_mask[j] = ro.dev_mask;
+        o->busy_mask[j] = 0; o->busy_frac[j] = 0.0;
+        uint64_t *busy = o->busy + (size_t)j * (size_t)(m > 0 ? m : 1);
+        for (int32_t q = 0; q < m; ++q) busy[q] = 0;
+        if (o->status[j] != ORC_OK) continue;
+        const uint64_t E = ro.elapsed;
+        u128 num = 0, den = 0;
+        for (int32_t did = 0; did < in->d_ids; ++did) {
+            const int32_t q = in->d_decl ? in->d_decl[did] : did;     /* declaration position */
+            if (q < 0 || q >= m) continue;
+            const int32_t hid = rg->dev_owner ? rg->dev_owner[did] : -1;
+            if (hid < 0 || hid >= in->h_ids) continue;
+            const int32_t p = in->h_decl ? in->h_decl[hid] : hid;
+            if (p < 0 || p >= n) continue;
+            int64_t ka = gather_ivs(hs, he, hr, hk, kh, hid, 1, A);
+            ka = iv_flatten(A, ka); ka = iv_intersect(A, ka, 0, E);
+            int64_t kb = gather_ivs(ds, de, dr, dk, kd, did, -1, B);
+            kb = iv_flatten(B, kb); kb = iv_intersect(B, kb, 0, E);
+            const int64_t kdiff = iv_subtract(A, ka, B, kb, D);
+            const u128 ov = iv_total(A, ka) - iv_total(D, kdiff);
+            busy[q] = (uint64_t)ov;
+            num += ov;
+            den += o->host_sum[((size_t)j * (size_t)n + (size_t)p) * 4 + 1];
+        }
+        if (den > 0) { o->busy_frac[j] = orc_div_exact(num, den); o->busy_mask[j] = 1; }
+    }
+    free(hs); free(he); free(hr); free(hk); free(ds); free(de); free(dr); free(dk); free(A); free(B); free(D);
+    return ORC_OK;
+}

@@ -173,3 +173,19 @@ def columns(start, end, res, kind) -> RecordColumns:
                          np.ascontiguousarray(end, dtype=np.uint64),
                          np.ascontiguousarray(res, dtype=np.int32),
                          np.ascontiguousarray(kind, dtype=np.uint8))
+
+
+def dev_owner_table(trace: Trace, packed: PackedTrace) -> np.ndarray:
+    """int32 [len(dev_ids)]: dense host id of each device's ``owner_rank``, -1 when it
+    has none or the owner is not a declared rank (``DeviceDecl.owner_rank``, model.py:66-71)."""
+    host_dense = {rank: i for i, rank in enumerate(packed.host_ids)}
+    declared = set(trace.host_processes)
+    owner_of = {}
+    for d in trace.devices:
+        owner_of.setdefault(d.device_id, d.owner_rank)
+    out = np.full(len(packed.dev_ids), -1, dtype=np.int32)
+    for i, dev in enumerate(packed.dev_ids):
+        o = owner_of.get(dev)
+        if o is not None and o in declared and o in host_dense:
+            out[i] = host_dense[o]
+    return out

@@ -20,6 +20,11 @@ reference's own corpus generator ``random_valid_trace``
     (metrics.py:66-122, exact int/int division),
   * config-shaped traces from oracle/gen.py: C1 in full and rank shards of
     C2, C3, C5,
+  * EXTENSIONS (not in the reference): monitoring-region
+    reports = the reference's compute_report on the window-clipped trace, and
+    offload-wait / device-busy overlap = the reference's flatten / intersect /
+    subtract / total_duration (intervals.py:40-105) on the owner's offload
+    records and the device's records,
 
 and writes the inputs plus the reference's outputs (floats as float.hex) to
 tests/golden/*.json.gz.  Nothing on the GPU box reads /root/reference.
@@ -294,13 +299,108 @@ def config_shards() -> list:
     return out
 
 
+# ---------------------------------------------------------------------------
+# extensions: regions (window-clipped traces) and offload / busy overlap
+# ---------------------------------------------------------------------------
+from heteff.intervals import flatten, intersect, subtract, total_duration  # noqa: E402
+
+
+def clip_interval(iv: Interval, a: int, b: int):
+    """The region clip (DESIGN.md section 9): intersect with [a, b), shift by -a;
+    zero-length records survive iff a <= start < b."""
+    if iv.start == iv.end:
+        return Interval(iv.start - a, iv.start - a) if a <= iv.start < b else None
+    s, e = max(iv.start, a), min(iv.end, b)
+    return Interval(s - a, e - a) if s < e else None
+
+
+def region_trace(t: Trace, a: int, b: int) -> Trace:
+    hr = [HostRecord(r.rank, r.state, c) for r in t.host_records if (c := clip_interval(r.interval, a, b))]
+    dr = [DeviceRecord(r.device_id, r.kind, c, r.stream) for r in t.device_records
+          if (c := clip_interval(r.interval, a, b))]
+    return Trace(host_processes=t.host_processes, devices=t.devices, host_records=tuple(hr),
+                 device_records=tuple(dr), time_unit=t.time_unit)
+
+
+def region_overlap(rt: Trace, E: int):
+    """Per declared device: |flatten(owner offload) ∩ flatten(device) ∩ [0,E)|, plus the fraction."""
+    bounds = Interval(0, E)
+    busy, num, den = [], 0, 0
+    offload_by_rank = {}
+    for s in compute_report(rt).host_summaries if rt.n else ():
+        offload_by_rank[s.rank] = s.d_offload
+    for d in rt.devices:
+        o = d.owner_rank
+        if o is None or o not in rt.host_processes:
+            busy.append(0)
+            continue
+        A = intersect(flatten(r.interval for r in rt.host_records
+                              if r.rank == o and r.state == HostState.OFFLOAD), bounds)
+        B = intersect(flatten(r.interval for r in rt.device_records if r.device_id == d.device_id), bounds)
+        ov = total_duration(A) - total_duration(subtract(A, B))
+        busy.append(ov)
+        num += ov
+        den += offload_by_rank[o]
+    return busy, (fx(num / den) if den else None)
+
+
+def region_case(t: Trace, windows, tag: str) -> dict:
+    regs = []
+    for a, b in windows:
+        rt = region_trace(t, a, b)
+        rep = enc_report(rt)
+        ov = region_overlap(rt, rep["E"]) if "E" in rep else None
+        regs.append({"report": rep, "busy": ov[0] if ov else None, "frac": ov[1] if ov else None})
+    return {"tag": tag, "trace": enc_trace(t), "windows": [list(w) for w in windows], "regions": regs}
+
+
+def random_windows(rng: random.Random, span: int, k: int):
+    out = [(0, span + 1000), (0, 1), (span + 5, span + 50)]          # whole trace, tiny, past the end
+    lo, hi = 0, span + rng.randint(0, 30)
+    for _ in range(k):                                                # nested
+        out.append((lo, hi))
+        w = hi - lo
+        lo += rng.randint(0, max(1, w // 6))
+        hi -= rng.randint(0, max(1, w // 6))
+        if hi <= lo:
+            break
+    for _ in range(3):                                                # arbitrary
+        a = rng.randint(0, span + 10)
+        out.append((a, a + rng.randint(0, span // 2 + 1)))
+    return out
+
+
+def regions_corpus() -> list:
+    out = []
+    rng = random.Random(0x5EED40)
+    for i in range(300):
+        t = random_valid_trace(rng, max_ranks=4, max_devices=4, max_segments=12)
+        span = max([r.interval.end for r in t.host_records] + [r.interval.end for r in t.device_records] + [1])
+        out.append(region_case(t, random_windows(rng, span, 6), f"rand{i}"))
+    # config-shaped shards (owners = rank of each device)
+    for name, r0, r1 in (("c1", 0, 4), ("c4", 0, 1), ("c3", 0, 1)):
+        cfg = CONFIGS[name]
+        (hs, he, hr, hk), (ds, de, dr, dk) = ogen.generate(cfg, r0, r1)
+        t = config_trace(cfg, r0, r1)
+        span = int(max(he.max(), de.max()))
+        nw = 4 if name == "c3" else 16
+        win = [(k * span // 40, span - k * span // 40) for k in range(nw)]
+        c = region_case(t, win, f"{name}[{r0}:{r1}]")
+        del c["trace"]                       # regenerated by the tests from oracle/gen.py
+        c.update({"config": name, "r0": r0, "r1": r1})
+        out.append(c)
+        print(f"  regions {name}[{r0}:{r1}] {len(t.host_records) + len(t.device_records)} records")
+    return out
+
+
 def main() -> None:
-    write("presets", presets())
-    write("acceptance", acceptance_corpora())
-    write("invalid", invalid_corpus())
-    write("summarize_device", summarize_device_corpus())
-    write("metrics", metrics_corpus())
-    write("config_shards", config_shards())
+    only = sys.argv[sys.argv.index("--only") + 1].split(",") if "--only" in sys.argv else None
+    jobs = {"presets": presets, "acceptance": acceptance_corpora, "invalid": invalid_corpus,
+            "summarize_device": summarize_device_corpus, "metrics": metrics_corpus,
+            "config_shards": config_shards, "regions": regions_corpus}
+    for name, fn in jobs.items():
+        if only is None or name in only:
+            write(name, fn())
 
 
 if __name__ == "__main__":
