@@ -186,6 +186,51 @@ typedef struct {
 int heteff_sort_records(heteff_ctx *ctx, const heteff_records *in, const heteff_columns *out, int64_t *perm,
                         heteff_sort_info *info, void *stream);
 
+/* ---- EXTENSIONS (not in the reference) ----
+ * Monitoring regions (K5) and offload-wait / device-busy overlap (K6).
+ * Region j is a window [start_j, end_j).  Its report is compute_report
+ * (metrics.py:125-154) of the trace whose records are intersected with the
+ * window (intervals.py:98-105 semantics) and shifted by -start_j, zero-length
+ * records kept iff start_j <= s < end_j.  offload_busy[j][g] is
+ * |offload(owner(g)) ∩ busy(g) ∩ [start_j, start_j + E_j)| where busy(g) is
+ * the union of the device's kernel and memory records; the fraction is
+ * sum_g offload_busy / sum_g d_offload(owner(g)).  The trace must be valid and
+ * canonical: the call runs the full analysis first and returns its status
+ * (INVALID_TRACE / CONTRACT) without computing regions otherwise.  All
+ * windows are evaluated in one pass over the records per 16 windows. */
+typedef struct {
+    const uint64_t *start;      /* [count] window starts (host memory) */
+    const uint64_t *end;        /* [count] window ends (exclusive; end <= start = empty window) */
+    int32_t count;
+    int32_t reserved;
+    const int32_t *dev_owner;   /* [dev_ids] dense host id owning each device, -1 none (host memory; NULL = none) */
+} heteff_regions;
+
+typedef struct {
+    int32_t status;             /* HETEFF_OK, or HETEFF_ANALYSIS_ERROR: the region records no activity */
+    int32_t reserved;
+    uint64_t elapsed;           /* E of the region trace */
+    double host_metrics[5];
+    uint32_t host_mask;
+    uint32_t device_mask;
+    double device_metrics[4];
+    double offload_busy_fraction;
+    uint32_t offload_busy_defined;
+    uint32_t reserved2;
+} heteff_region_result;
+
+typedef struct {
+    heteff_region_result *results;  /* [count] (host memory) */
+    uint64_t *host_summaries;       /* [count][n][4] useful, offload, mpi, span_end, or NULL */
+    uint64_t *device_summaries;     /* [count][m][4] kernel, memory, idle, clamped, or NULL */
+    uint64_t *offload_busy;         /* [count][m], or NULL */
+    double kernel_ms;               /* device time of the region passes (out) */
+} heteff_region_outputs;
+
+/* trace columns in device memory */
+int heteff_analyze_regions(heteff_ctx *ctx, const heteff_trace *trace, const heteff_regions *regions,
+                           heteff_region_outputs *out, void *stream);
+
 /* overlap errors: cover index of each listed record (model.py:208-215), host memory */
 int heteff_overlap_covers(heteff_ctx *ctx, const heteff_trace *trace, int host_columns_on_host,
                           const int64_t *error_idx, int64_t count, int64_t *cover_idx, void *stream);

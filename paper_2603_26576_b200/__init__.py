@@ -16,9 +16,11 @@ from .api import (
     HostMetrics,
     HostSummary,
     MetricsReport,
+    RegionReport,
     compute_report,
     device_metrics,
     host_metrics,
+    region_reports,
     summarize_device,
     summarize_host,
     validate,
@@ -40,7 +42,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "AnalysisError", "DeviceMetrics", "DeviceSummary", "HostMetrics", "HostSummary", "MetricsReport",
-    "compute_report", "device_metrics", "host_metrics", "summarize_device", "summarize_host", "validate",
+    "RegionReport", "region_reports", "compute_report", "device_metrics", "host_metrics", "summarize_device", "summarize_host", "validate",
     "U64_MAX", "DeviceActivityKind", "DeviceDecl", "DeviceRecord", "HostRecord", "HostState", "Interval",
     "InvalidTraceError", "Trace", "ValidationReport",
 ]

@@ -69,6 +69,24 @@ class SortInfo(C.Structure):
                 ("ms", C.c_double)]
 
 
+class RegionsABI(C.Structure):
+    _fields_ = [("start", _p), ("end", _p), ("count", C.c_int32), ("reserved", C.c_int32), ("dev_owner", _p)]
+
+
+class RegionResult(C.Structure):
+    _fields_ = [
+        ("status", C.c_int32), ("reserved", C.c_int32), ("elapsed", C.c_uint64),
+        ("host_metrics", C.c_double * 5), ("host_mask", C.c_uint32), ("device_mask", C.c_uint32),
+        ("device_metrics", C.c_double * 4), ("offload_busy_fraction", C.c_double),
+        ("offload_busy_defined", C.c_uint32), ("reserved2", C.c_uint32),
+    ]
+
+
+class RegionOutputs(C.Structure):
+    _fields_ = [("results", _p), ("host_summaries", _p), ("device_summaries", _p), ("offload_busy", _p),
+                ("kernel_ms", C.c_double)]
+
+
 FLAG_SORT_IF_NEEDED = 1
 CONTRACT_HOST_ORDER, CONTRACT_DEV_ORDER, CONTRACT_HOST_KIND, CONTRACT_DEV_KIND = 1, 2, 4, 8
 
@@ -88,7 +106,7 @@ EXPORTED = (
     "heteff_abi_version", "heteff_create", "heteff_destroy", "heteff_last_error",
     "heteff_analyze", "heteff_analyze_host", "heteff_overlap_covers",
     "heteff_host_metrics", "heteff_device_metrics", "heteff_generate", "heteff_prof_read",
-    "heteff_sort_records",
+    "heteff_sort_records", "heteff_analyze_regions",
 )
 
 _lib = None
@@ -123,6 +141,9 @@ def load() -> C.CDLL:
     lib.heteff_prof_read.argtypes = [_p, C.c_int]
     lib.heteff_sort_records.restype = C.c_int
     lib.heteff_sort_records.argtypes = [_p, C.POINTER(Records), C.POINTER(Columns), _p, C.POINTER(SortInfo), _p]
+    lib.heteff_analyze_regions.restype = C.c_int
+    lib.heteff_analyze_regions.argtypes = [_p, C.POINTER(TraceABI), C.POINTER(RegionsABI),
+                                           C.POINTER(RegionOutputs), _p]
     lib.heteff_generate.restype = C.c_int
     lib.heteff_generate.argtypes = [_p, C.POINTER(GenSide), _p, _p, _p, _p, _p]
     _lib = lib

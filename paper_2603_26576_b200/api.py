@@ -26,7 +26,7 @@ from . import _native as N
 from .engine import Findings, analyze_packed, metrics_from_summaries
 from .messages import clamp_warnings, declaration_messages, validation_report
 from .model import U64_MAX, InvalidTraceError, Trace, ValidationReport
-from .packing import PackedTrace, pack_trace
+from .packing import PackedTrace, dev_owner_table, pack_trace
 
 
 class AnalysisError(Exception):
@@ -192,3 +192,66 @@ def compute_report(trace: Trace) -> MetricsReport:
         host_summaries=tuple(_host_summaries(trace, f)),
         device_summaries=tuple(_device_summaries(trace, f, E)) if trace.m >= 1 else (),
         warnings=tuple(warnings))
+
+
+# ---------------------------------------------------------------------------
+# EXTENSIONS beyond the reference: monitoring regions and
+# the offload-wait / device-busy overlap.  Not part of the reference API.
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True)
+class RegionReport:
+    """One monitoring region: ``report`` is the reference's compute_report of the
+    window-clipped trace (``None`` when the region records no activity, where the
+    reference raises AnalysisError); ``offload_busy[g]`` is the owner's offload
+    time during which device g was busy, inside the region."""
+
+    window: tuple[int, int]
+    report: MetricsReport | None
+    offload_busy: tuple[int, ...]
+    offload_busy_fraction: float | None
+
+
+def region_reports(trace: Trace, windows) -> list[RegionReport]:
+    """Region metric trees for ``windows`` = ``[(start, end), ...]`` (K5 + K6 kernels).
+
+    Raises InvalidTraceError for an invalid trace (validation runs first).
+    Region reports carry summaries and metrics; their ``warnings`` are empty."""
+    import torch
+
+    from .engine import DeviceTrace, analyze_regions
+
+    packed = pack_trace(trace)
+    windows = [(int(a), int(b)) for a, b in windows]
+    dev = torch.device("cuda", int(__import__("os").environ.get("HETEFF_DEVICE", "0")))
+
+    def up(a):
+        a = np.ascontiguousarray(a)
+        if a.dtype == np.uint64:
+            a = a.view(np.int64)
+        return torch.from_numpy(a).to(dev)
+
+    H, D = packed.host, packed.dev
+    dt = DeviceTrace(up(H.start), up(H.end), up(H.res), up(H.kind), up(D.start), up(D.end), up(D.res),
+                     up(D.kind), packed.n_unique, packed.m_unique, packed.host_elapsed_floor)
+    owner = dev_owner_table(trace, packed)
+    run = analyze_regions(dt, windows, owner, host_decl=up(packed.host_decl), dev_decl=up(packed.dev_decl),
+                          host_ids=len(packed.host_ids), dev_ids=len(packed.dev_ids))
+    if run.status not in (N.OK, N.ANALYSIS_ERROR) or packed.host_q or packed.dev_q:
+        _, f = _run(trace, N.MODE_VALIDATE)
+        _raise_invalid(trace, packed, f)
+    out = []
+    for w, r in zip(windows, run.regions):
+        if r.status != N.OK:
+            out.append(RegionReport(w, None, tuple(int(x) for x in r.offload_busy), None))
+            continue
+        hs = tuple(HostSummary(rank, *(int(x) for x in r.host_sum[pos]))
+                   for pos, rank in enumerate(trace.host_processes))
+        ds = tuple(DeviceSummary(d.device_id, *(int(x) for x in r.dev_sum[pos][:3]))
+                   for pos, d in enumerate(trace.devices)) if trace.m >= 1 else ()
+        rep = MetricsReport(
+            elapsed_ns=r.elapsed, n=trace.n, m=trace.m,
+            host=HostMetrics(*r.host_metrics) if trace.n >= 1 else None,
+            device=DeviceMetrics(*r.device_metrics) if trace.m >= 1 else None,
+            host_summaries=hs, device_summaries=ds, warnings=())
+        out.append(RegionReport(w, rep, tuple(int(x) for x in r.offload_busy), r.offload_busy_fraction))
+    return out

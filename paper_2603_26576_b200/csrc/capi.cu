@@ -43,6 +43,8 @@ struct heteff_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // K3 sort: workspace, sorted columns + permutations
     DevBuf sort_ws, sorted;
+    // K5/K6 regions: accumulators, carries, outputs
+    DevBuf reg_ws, reg_out;
 };
 
 static int fail(heteff_ctx *ctx, int code, const std::string &msg)
@@ -109,7 +111,7 @@ void heteff_destroy(heteff_ctx *ctx)
 {
     if (!ctx) return;
     DevBuf *bufs[] = {&ctx->host_acc, &ctx->dev_acc, &ctx->host_tiles, &ctx->dev_tiles, &ctx->host_out,
-                      &ctx->dev_out, &ctx->lists, &ctx->stage, &ctx->aux, &ctx->sort_ws, &ctx->sorted};
+                      &ctx->dev_out, &ctx->lists, &ctx->stage, &ctx->aux, &ctx->sort_ws, &ctx->sorted, &ctx->reg_ws, &ctx->reg_out};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->g) cudaFree(ctx->g);
@@ -346,6 +348,121 @@ static int run_analysis(heteff_ctx *ctx, const heteff_trace *t, const heteff_opt
         }
     }
     return rc;
+}
+
+int heteff_analyze_regions(heteff_ctx *ctx, const heteff_trace *t, const heteff_regions *rg,
+                           heteff_region_outputs *out, void *stream)
+{
+    if (!ctx || !t || !rg || !out || rg->count < 0) return fail(ctx, HETEFF_BAD_ARG, "bad argument");
+    if (rg->count > 0 && (!rg->start || !rg->end || !out->results)) return fail(ctx, HETEFF_BAD_ARG, "null argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    // the whole trace first: validity and canonical order are preconditions
+    heteff_options o0{};
+    o0.mode = HETEFF_MODE_REPORT;
+    heteff_result r0{};
+    int rc = run_analysis(ctx, t, &o0, &r0, nullptr, s);
+    if (rc != HETEFF_OK && rc != HETEFF_ANALYSIS_ERROR) return rc;
+    out->kernel_ms = 0.0;
+    if (rg->count == 0) return HETEFF_OK;
+
+    const int W = hb::kMaxWindows;
+    const int64_t hid = t->host_ids > 0 ? t->host_ids : 1, did = t->dev_ids > 0 ? t->dev_ids : 1;
+    const int64_t tiles = (int64_t)hb::region_tiles(t->dev.count);
+    const int64_t nn = t->n > 0 ? t->n : 1, mm = t->m > 0 ? t->m : 1;
+    auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t b_hseg = up((size_t)(hid + 1) * 8), b_hacc = up((size_t)W * hid * 24), b_dacc = up((size_t)W * did * 32);
+    const size_t b_E = up(W * 8), b_dmax = up(W * 8), b_tagg = up((size_t)(tiles + 1) * 24);
+    const size_t b_tcar = up((size_t)(tiles + 1) * 16), b_own = up((size_t)did * 4);
+    CK(ensure(ctx->reg_ws, b_hseg + b_hacc + b_dacc + b_E + b_dmax + b_tagg + b_tcar + b_own, false), "alloc regions");
+    const size_t b_ho = up((size_t)W * nn * 32), b_do = up((size_t)W * mm * 32), b_bo = up((size_t)W * mm * 8);
+    const size_t b_res = up(W * sizeof(hb::RegionResultDev));
+    CK(ensure(ctx->reg_out, 2 * (b_ho + b_do + b_bo + b_res), false), "alloc region outputs");
+    uint8_t *w = static_cast<uint8_t *>(ctx->reg_ws.p);
+    hb::RegParams p;
+    memset(&p, 0, sizeof(p));
+    p.hs = (const u64 *)t->host.start; p.he = (const u64 *)t->host.end; p.hr = t->host.res; p.hk = t->host.kind;
+    p.hn = t->host.count;
+    p.ds = (const u64 *)t->dev.start; p.de = (const u64 *)t->dev.end; p.dr = t->dev.res; p.dk = t->dev.kind;
+    p.dn = t->dev.count;
+    p.host_ids = t->host_ids; p.dev_ids = t->dev_ids;
+    p.host_decl = t->host_decl; p.dev_decl = t->dev_decl;
+    p.n = t->n; p.m = t->m;
+    size_t o = 0;
+    p.hseg = reinterpret_cast<int64_t *>(w + o); o += b_hseg;
+    p.h_acc = reinterpret_cast<u64 *>(w + o); o += b_hacc;
+    p.d_acc = reinterpret_cast<u64 *>(w + o); o += b_dacc;
+    p.E = reinterpret_cast<u64 *>(w + o); o += b_E;
+    p.dmax = reinterpret_cast<u64 *>(w + o); o += b_dmax;
+    p.tagg = reinterpret_cast<u64 *>(w + o); o += b_tagg;
+    p.tcarry = reinterpret_cast<u64 *>(w + o); o += b_tcar;
+    int32_t *own = reinterpret_cast<int32_t *>(w + o); o += b_own;
+    p.tiles = tiles;
+    if (rg->dev_owner && t->dev_ids > 0) {
+        CK(cudaMemcpyAsync(own, rg->dev_owner, (size_t)t->dev_ids * 4, cudaMemcpyHostToDevice, s), "h2d owners");
+        p.owner = own;
+    }
+    uint8_t *ob = static_cast<uint8_t *>(ctx->reg_out.p);
+    p.host_out = reinterpret_cast<u64 *>(ob);
+    p.dev_out = reinterpret_cast<u64 *>(ob + b_ho);
+    p.busy_out = reinterpret_cast<u64 *>(ob + b_ho + b_do);
+    p.res = reinterpret_cast<hb::RegionResultDev *>(ob + b_ho + b_do + b_bo);
+    // pinned staging of a pass's results (the second half of reg_out is not used on the device)
+    hb::RegionResultDev rh[hb::kMaxWindows];
+    float total_ms = 0.f;
+    for (int32_t j0 = 0; j0 < rg->count; j0 += W) {
+        const int R = rg->count - j0 < W ? rg->count - j0 : W;
+        p.R = R;
+        for (int j = 0; j < W; ++j) {
+            const bool live = j < R;
+            const uint64_t a = live ? rg->start[j0 + j] : 0, b = live ? rg->end[j0 + j] : 0;
+            p.wlo[j] = a;
+            p.whi[j] = b > a ? b : a;
+            p.wtop[j] = a;
+        }
+        CK(cudaMemsetAsync(p.h_acc, 0, b_hacc, s), "memset");
+        CK(cudaMemsetAsync(p.d_acc, 0, b_dacc, s), "memset");
+        CK(cudaMemsetAsync(p.E, 0, b_E + b_dmax, s), "memset");
+        CK(cudaEventRecord(ctx->ev0, s), "event");
+        CK(hb::launch_regions_phase1(p, s), "launch regions phase 1");
+        u64 Eh[hb::kMaxWindows];
+        CK(cudaMemcpyAsync(Eh, p.E, sizeof(Eh), cudaMemcpyDeviceToHost, s), "d2h E");
+        CK(cudaStreamSynchronize(s), "regions phase 1");
+        for (int j = 0; j < R; ++j) p.wtop[j] = p.wlo[j] + Eh[j];
+        CK(hb::launch_regions_phase2(p, s), "launch regions phase 2");
+        CK(cudaEventRecord(ctx->ev1, s), "event");
+        CK(cudaMemcpyAsync(rh, p.res, sizeof(hb::RegionResultDev) * R, cudaMemcpyDeviceToHost, s), "d2h results");
+        if (out->host_summaries && t->n > 0)
+            CK(cudaMemcpyAsync(out->host_summaries + (size_t)j0 * t->n * 4, p.host_out, (size_t)R * t->n * 32,
+                               cudaMemcpyDeviceToHost, s), "d2h host summaries");
+        if (out->device_summaries && t->m > 0)
+            CK(cudaMemcpyAsync(out->device_summaries + (size_t)j0 * t->m * 4, p.dev_out, (size_t)R * t->m * 32,
+                               cudaMemcpyDeviceToHost, s), "d2h device summaries");
+        if (out->offload_busy && t->m > 0)
+            CK(cudaMemcpyAsync(out->offload_busy + (size_t)j0 * t->m, p.busy_out, (size_t)R * t->m * 8,
+                               cudaMemcpyDeviceToHost, s), "d2h busy");
+        CK(cudaStreamSynchronize(s), "regions");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        total_ms += ms;
+        for (int j = 0; j < R; ++j) {
+            heteff_region_result &x = out->results[j0 + j];
+            const hb::RegionResultDev &y = rh[j];
+            x.status = y.status;
+            x.reserved = 0;
+            x.elapsed = y.elapsed;
+            for (int i = 0; i < 5; ++i) x.host_metrics[i] = y.host_metrics[i];
+            for (int i = 0; i < 4; ++i) x.device_metrics[i] = y.device_metrics[i];
+            x.host_mask = y.host_mask;
+            x.device_mask = y.device_mask;
+            x.offload_busy_fraction = y.busy_fraction;
+            x.offload_busy_defined = y.busy_mask;
+            x.reserved2 = 0;
+        }
+    }
+    out->kernel_ms = total_ms;
+    ctx->err.clear();
+    return HETEFF_OK;
 }
 
 int heteff_sort_records(heteff_ctx *ctx, const heteff_records *in, const heteff_columns *out, int64_t *perm,

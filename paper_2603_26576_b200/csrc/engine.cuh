@@ -107,6 +107,56 @@ cudaError_t launch_metrics(const u64 *summaries, int32_t k, u64 elapsed, int hos
 cudaError_t launch_overlap_pass(const Params &p, u64 *scratch, cudaStream_t s);
 cudaError_t launch_covers(const Params &p, const int64_t *err_idx, int64_t count, int64_t *cover, cudaStream_t s);
 
+// K5/K6 (regions.cu, EXTENSIONS): monitoring regions + offload / busy overlap
+constexpr int kMaxWindows = 16;      // windows per region pass
+
+struct RegionResultDev {
+    int32_t status;
+    int32_t reserved;
+    u64 elapsed;
+    double host_metrics[5];
+    uint32_t host_mask;
+    uint32_t device_mask;
+    double device_metrics[4];
+    double busy_fraction;
+    uint32_t busy_mask;
+    uint32_t reserved2;
+};
+
+struct RegParams {
+    const u64 *hs, *he;
+    const int32_t *hr;
+    const uint8_t *hk;
+    int64_t hn;
+    const u64 *ds, *de;
+    const int32_t *dr;
+    const uint8_t *dk;
+    int64_t dn;
+    int32_t host_ids, dev_ids;
+    const int32_t *host_decl, *dev_decl;   // null = identity
+    int32_t n, m;
+    int32_t R;                              // windows of this pass (<= kMaxWindows)
+    u64 wlo[kMaxWindows], whi[kMaxWindows]; // window bounds, padded with empty [0, 0)
+    u64 wtop[kMaxWindows];                  // phase 2: wlo + E (the region's clamp end)
+    const int32_t *owner;                   // [dev_ids] dense host id or -1 (null = none)
+    int64_t *hseg;                          // [host_ids + 1] host CSR offsets
+    u64 *h_acc;                             // [R][host_ids][3] offload, mpi, span
+    u64 *d_acc;                             // [R][dev_ids][4] kernel, kernel|memory, clamped, busy
+    u64 *E;                                 // [R]
+    u64 *dmax;                              // [R] max clipped device end (device-only traces)
+    u64 *tagg;                              // [tiles][3]
+    u64 *tcarry;                            // [tiles][2]
+    int64_t tiles;
+    u64 *host_out;                          // [R][n][4]
+    u64 *dev_out;                           // [R][m][4]
+    u64 *busy_out;                          // [R][m]
+    RegionResultDev *res;                   // [R]
+};
+
+size_t region_tiles(int64_t dn);
+cudaError_t launch_regions_phase1(const RegParams &p, cudaStream_t s);
+cudaError_t launch_regions_phase2(const RegParams &p, cudaStream_t s);
+
 // K3 (sort.cu): stable radix sort of one record set by (res, start)
 struct SortStats {
     int key_bits, passes, wide, start_sorted;

@@ -240,3 +240,62 @@ def sort_records(start, end, res, kind, stream: int | None = None, device: int |
         raise N.NativeError(f"sort failed ({rc}): {N.last_error(ctx)}")
     return SortResult(os_, oe, orr, ok, perm, info.key_bits, info.passes, bool(info.wide),
                       bool(info.start_sorted), info.ms)
+
+
+# ---------------------------------------------------------------------------
+# EXTENSIONS: monitoring regions (K5) + offload-wait / device-busy overlap (K6)
+# ---------------------------------------------------------------------------
+@dataclass
+class RegionFindings:
+    status: int                 # OK, or ANALYSIS_ERROR when the region records no activity
+    elapsed: int
+    host_metrics: tuple         # 5 floats or None
+    device_metrics: tuple       # 4 floats or None
+    offload_busy_fraction: float | None
+    host_sum: np.ndarray        # uint64 [n][4] useful, offload, mpi, span_end
+    dev_sum: np.ndarray         # uint64 [m][4] kernel, memory, idle, clamped
+    offload_busy: np.ndarray    # uint64 [m]
+
+
+@dataclass
+class RegionsRun:
+    status: int                 # status of the whole-trace analysis that precedes the regions
+    regions: list
+    kernel_ms: float
+
+
+def analyze_regions(dt: DeviceTrace, windows, dev_owner=None, stream: int | None = None,
+                    device: int | None = None, host_decl=None, dev_decl=None, host_ids: int | None = None,
+                    dev_ids: int | None = None) -> RegionsRun:
+    """Region reports for ``windows`` (``[(start, end), ...]``) of HBM-resident columns.
+
+    ``dev_owner``: int32 [dev_ids] dense host id owning each device (-1 none)."""
+    ctx = N.context(device)
+    lib = N.load()
+    t = device_trace_abi(dt)
+    if host_ids is not None:
+        t.host_ids, t.dev_ids = host_ids, dev_ids
+        t.host_decl, t.dev_decl = _dptr(host_decl), _dptr(dev_decl)
+    w = np.ascontiguousarray(np.asarray(windows, dtype=np.uint64).reshape(-1, 2))
+    ws, we = np.ascontiguousarray(w[:, 0]), np.ascontiguousarray(w[:, 1])
+    R = w.shape[0]
+    owner = None if dev_owner is None else np.ascontiguousarray(dev_owner, dtype=np.int32)
+    n, m = t.n, t.m
+    results = (N.RegionResult * max(R, 1))()
+    hs = np.zeros((max(R, 1), max(n, 1), 4), dtype=np.uint64)
+    ds = np.zeros((max(R, 1), max(m, 1), 4), dtype=np.uint64)
+    busy = np.zeros((max(R, 1), max(m, 1)), dtype=np.uint64)
+    rg = N.RegionsABI(_ptr(ws), _ptr(we), R, 0, _ptr(owner))
+    out = N.RegionOutputs(C.cast(results, C.c_void_p), hs.ctypes.data, ds.ctypes.data, busy.ctypes.data, 0.0)
+    rc = lib.heteff_analyze_regions(ctx, C.byref(t), C.byref(rg), C.byref(out), stream)
+    _check(ctx, rc)
+    regs = []
+    if rc in (N.OK, N.ANALYSIS_ERROR):
+        for j in range(R):
+            x = results[j]
+            regs.append(RegionFindings(
+                int(x.status), int(x.elapsed), _metrics(x.host_metrics, x.host_mask, 5),
+                _metrics(x.device_metrics, x.device_mask, 4),
+                float(x.offload_busy_fraction) if x.offload_busy_defined else None,
+                hs[j, :n], ds[j, :m], busy[j, :m]))
+    return RegionsRun(rc, regs, float(out.kernel_ms))
