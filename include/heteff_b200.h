@@ -186,6 +186,26 @@ typedef struct {
 int heteff_sort_records(heteff_ctx *ctx, const heteff_records *in, const heteff_columns *out, int64_t *perm,
                         heteff_sort_info *info, void *stream);
 
+/* ---- interval algebra (intervals.py:40-105) over device arrays of [start, end) ----
+ * flatten   <- flatten (intervals.py:40-61): HETEFF_VALUE_ERROR with *malformed_index
+ *              = first input index with start > end ("malformed interval at index i");
+ *              out capacity n.
+ * subtract  <- subtract (intervals.py:64-81): a, b flat sets (sorted, disjoint,
+ *              non-adjacent, no empties); out capacity na + nb.
+ * intersect <- intersect (intervals.py:98-105): clip to [lo, hi); out capacity n.
+ * total     <- total_duration (intervals.py:93-95): exact u128 sum, out[0] low
+ *              word, out[1] high word (host memory).
+ * complement (intervals.py:84-90) is subtract([bounds], a), as in the reference. */
+int heteff_flatten(heteff_ctx *ctx, const uint64_t *start, const uint64_t *end, int64_t n, uint64_t *out_start,
+                   uint64_t *out_end, int64_t *out_n, int64_t *malformed_index, void *stream);
+int heteff_subtract(heteff_ctx *ctx, const uint64_t *a_start, const uint64_t *a_end, int64_t na,
+                    const uint64_t *b_start, const uint64_t *b_end, int64_t nb, uint64_t *out_start,
+                    uint64_t *out_end, int64_t *out_n, void *stream);
+int heteff_intersect(heteff_ctx *ctx, const uint64_t *start, const uint64_t *end, int64_t n, uint64_t lo,
+                     uint64_t hi, uint64_t *out_start, uint64_t *out_end, int64_t *out_n, void *stream);
+int heteff_total_duration(heteff_ctx *ctx, const uint64_t *start, const uint64_t *end, int64_t n, uint64_t out[2],
+                          void *stream);
+
 /* ---- EXTENSIONS (not in the reference) ----
  * Monitoring regions (K5) and offload-wait / device-busy overlap (K6).
  * Region j is a window [start_j, end_j).  Its report is compute_report

@@ -623,3 +623,50 @@ int orc_regions(const orc_in *in, const orc_regions_in *rg, orc_regions_out *o)
     free(hs); free(he); free(hr); free(hk); free(ds); free(de); free(dr); free(dk); free(A); free(B); free(D);
     return ORC_OK;
 }
+
+/* ------------------------------------------------------------------ */
+/* exported interval algebra restatements (tests pin them to fixtures  */
+/* generated from the reference's intervals.py)                        */
+/* ------------------------------------------------------------------ */
+int64_t orc_iv_flatten(const uint64_t *s, const uint64_t *e, int64_t n, uint64_t *os, uint64_t *oe, int64_t *bad)
+{
+    *bad = -1;
+    for (int64_t i = 0; i < n; ++i) if (s[i] > e[i]) { *bad = i; return -1; }   /* intervals.py:49-51 */
+    iv_t *v = malloc(sizeof(iv_t) * (size_t)(n + 1));
+    for (int64_t i = 0; i < n; ++i) { v[i].s = s[i]; v[i].e = e[i]; }
+    int64_t k = iv_flatten(v, n);
+    for (int64_t i = 0; i < k; ++i) { os[i] = v[i].s; oe[i] = v[i].e; }
+    free(v);
+    return k;
+}
+
+int64_t orc_iv_subtract(const uint64_t *as, const uint64_t *ae, int64_t na, const uint64_t *bs, const uint64_t *be,
+                        int64_t nb, uint64_t *os, uint64_t *oe)
+{
+    iv_t *a = malloc(sizeof(iv_t) * (size_t)(na + 1)), *b = malloc(sizeof(iv_t) * (size_t)(nb + 1));
+    iv_t *o = malloc(sizeof(iv_t) * (size_t)(na + nb + 1));
+    for (int64_t i = 0; i < na; ++i) { a[i].s = as[i]; a[i].e = ae[i]; }
+    for (int64_t i = 0; i < nb; ++i) { b[i].s = bs[i]; b[i].e = be[i]; }
+    int64_t k = iv_subtract(a, na, b, nb, o);
+    for (int64_t i = 0; i < k; ++i) { os[i] = o[i].s; oe[i] = o[i].e; }
+    free(a); free(b); free(o);
+    return k;
+}
+
+int64_t orc_iv_intersect(const uint64_t *s, const uint64_t *e, int64_t n, uint64_t lo, uint64_t hi, uint64_t *os,
+                         uint64_t *oe)
+{
+    iv_t *v = malloc(sizeof(iv_t) * (size_t)(n + 1));
+    for (int64_t i = 0; i < n; ++i) { v[i].s = s[i]; v[i].e = e[i]; }
+    int64_t k = iv_intersect(v, n, lo, hi);
+    for (int64_t i = 0; i < k; ++i) { os[i] = v[i].s; oe[i] = v[i].e; }
+    free(v);
+    return k;
+}
+
+void orc_iv_total(const uint64_t *s, const uint64_t *e, int64_t n, uint64_t out[2])
+{
+    u128 t = 0;
+    for (int64_t i = 0; i < n; ++i) t += e[i] - s[i];
+    out[0] = (uint64_t)t; out[1] = (uint64_t)(t >> 64);
+}

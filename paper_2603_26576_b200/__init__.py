@@ -25,6 +25,7 @@ from .api import (
     summarize_host,
     validate,
 )
+from .intervals import EMPTY, FlatSet, complement, flatten, intersect, subtract, total_duration
 from .model import (
     U64_MAX,
     DeviceActivityKind,
@@ -41,6 +42,7 @@ from .model import (
 __version__ = "0.1.0"
 
 __all__ = [
+    "EMPTY", "FlatSet", "complement", "flatten", "intersect", "subtract", "total_duration",
     "AnalysisError", "DeviceMetrics", "DeviceSummary", "HostMetrics", "HostSummary", "MetricsReport",
     "RegionReport", "region_reports", "compute_report", "device_metrics", "host_metrics", "summarize_device", "summarize_host", "validate",
     "U64_MAX", "DeviceActivityKind", "DeviceDecl", "DeviceRecord", "HostRecord", "HostState", "Interval",

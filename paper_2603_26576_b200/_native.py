@@ -107,6 +107,7 @@ EXPORTED = (
     "heteff_analyze", "heteff_analyze_host", "heteff_overlap_covers",
     "heteff_host_metrics", "heteff_device_metrics", "heteff_generate", "heteff_prof_read",
     "heteff_sort_records", "heteff_analyze_regions",
+    "heteff_flatten", "heteff_subtract", "heteff_intersect", "heteff_total_duration",
 )
 
 _lib = None
@@ -144,6 +145,15 @@ def load() -> C.CDLL:
     lib.heteff_analyze_regions.restype = C.c_int
     lib.heteff_analyze_regions.argtypes = [_p, C.POINTER(TraceABI), C.POINTER(RegionsABI),
                                            C.POINTER(RegionOutputs), _p]
+    lib.heteff_flatten.restype = C.c_int
+    lib.heteff_flatten.argtypes = [_p, _p, _p, C.c_int64, _p, _p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), _p]
+    lib.heteff_subtract.restype = C.c_int
+    lib.heteff_subtract.argtypes = [_p, _p, _p, C.c_int64, _p, _p, C.c_int64, _p, _p, C.POINTER(C.c_int64), _p]
+    lib.heteff_intersect.restype = C.c_int
+    lib.heteff_intersect.argtypes = [_p, _p, _p, C.c_int64, C.c_uint64, C.c_uint64, _p, _p, C.POINTER(C.c_int64),
+                                     _p]
+    lib.heteff_total_duration.restype = C.c_int
+    lib.heteff_total_duration.argtypes = [_p, _p, _p, C.c_int64, _p, _p]
     lib.heteff_generate.restype = C.c_int
     lib.heteff_generate.argtypes = [_p, C.POINTER(GenSide), _p, _p, _p, _p, _p]
     _lib = lib

@@ -45,6 +45,8 @@ struct heteff_ctx {
     DevBuf sort_ws, sorted;
     // K5/K6 regions: accumulators, carries, outputs
     DevBuf reg_ws, reg_out;
+    // interval algebra scratch
+    DevBuf iv_ws;
 };
 
 static int fail(heteff_ctx *ctx, int code, const std::string &msg)
@@ -111,7 +113,7 @@ void heteff_destroy(heteff_ctx *ctx)
 {
     if (!ctx) return;
     DevBuf *bufs[] = {&ctx->host_acc, &ctx->dev_acc, &ctx->host_tiles, &ctx->dev_tiles, &ctx->host_out,
-                      &ctx->dev_out, &ctx->lists, &ctx->stage, &ctx->aux, &ctx->sort_ws, &ctx->sorted, &ctx->reg_ws, &ctx->reg_out};
+                      &ctx->dev_out, &ctx->lists, &ctx->stage, &ctx->aux, &ctx->sort_ws, &ctx->sorted, &ctx->reg_ws, &ctx->reg_out, &ctx->iv_ws};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->g) cudaFree(ctx->g);
@@ -461,6 +463,65 @@ int heteff_analyze_regions(heteff_ctx *ctx, const heteff_trace *t, const heteff_
         }
     }
     out->kernel_ms = total_ms;
+    ctx->err.clear();
+    return HETEFF_OK;
+}
+
+int heteff_flatten(heteff_ctx *ctx, const uint64_t *start, const uint64_t *end, int64_t n, uint64_t *out_start,
+                   uint64_t *out_end, int64_t *out_n, int64_t *malformed_index, void *stream)
+{
+    if (!ctx || n < 0 || !out_n || !malformed_index || (n > 0 && (!start || !end || !out_start || !out_end)))
+        return fail(ctx, HETEFF_BAD_ARG, "bad argument");
+    if (n >= (int64_t)0xffffffffll) return fail(ctx, HETEFF_BAD_ARG, "too many intervals for one call");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    CK(ensure(ctx->iv_ws, hb::iv_flatten_ws(n), false), "alloc interval scratch");
+    const cudaError_t e = hb::iv_flatten((const u64 *)start, (const u64 *)end, n, (u64 *)out_start, (u64 *)out_end,
+                                         out_n, malformed_index, ctx->iv_ws.p, ctx->iv_ws.bytes,
+                                         static_cast<cudaStream_t>(stream));
+    if (*malformed_index >= 0) return fail(ctx, HETEFF_VALUE_ERROR, "malformed interval");
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "flatten");
+    ctx->err.clear();
+    return HETEFF_OK;
+}
+
+int heteff_subtract(heteff_ctx *ctx, const uint64_t *a_start, const uint64_t *a_end, int64_t na,
+                    const uint64_t *b_start, const uint64_t *b_end, int64_t nb, uint64_t *out_start,
+                    uint64_t *out_end, int64_t *out_n, void *stream)
+{
+    if (!ctx || na < 0 || nb < 0 || !out_n) return fail(ctx, HETEFF_BAD_ARG, "bad argument");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    CK(ensure(ctx->iv_ws, hb::iv_subtract_ws(na, nb), false), "alloc interval scratch");
+    CK(hb::iv_subtract((const u64 *)a_start, (const u64 *)a_end, na, (const u64 *)b_start, (const u64 *)b_end, nb,
+                       (u64 *)out_start, (u64 *)out_end, out_n, ctx->iv_ws.p, ctx->iv_ws.bytes,
+                       static_cast<cudaStream_t>(stream)),
+       "subtract");
+    ctx->err.clear();
+    return HETEFF_OK;
+}
+
+int heteff_intersect(heteff_ctx *ctx, const uint64_t *start, const uint64_t *end, int64_t n, uint64_t lo,
+                     uint64_t hi, uint64_t *out_start, uint64_t *out_end, int64_t *out_n, void *stream)
+{
+    if (!ctx || n < 0 || !out_n) return fail(ctx, HETEFF_BAD_ARG, "bad argument");
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    CK(ensure(ctx->iv_ws, hb::iv_intersect_ws(n), false), "alloc interval scratch");
+    CK(hb::iv_intersect((const u64 *)start, (const u64 *)end, n, lo, hi, (u64 *)out_start, (u64 *)out_end, out_n,
+                        ctx->iv_ws.p, ctx->iv_ws.bytes, static_cast<cudaStream_t>(stream)),
+       "intersect");
+    ctx->err.clear();
+    return HETEFF_OK;
+}
+
+int heteff_total_duration(heteff_ctx *ctx, const uint64_t *start, const uint64_t *end, int64_t n, uint64_t out[2],
+                          void *stream)
+{
+    if (!ctx || n < 0 || !out) return fail(ctx, HETEFF_BAD_ARG, "bad argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    CK(ensure(ctx->iv_ws, 256, false), "alloc interval scratch");
+    CK(hb::iv_total((const u64 *)start, (const u64 *)end, n, static_cast<u64 *>(ctx->iv_ws.p), s), "total");
+    CK(cudaMemcpyAsync(out, ctx->iv_ws.p, 16, cudaMemcpyDeviceToHost, s), "d2h");
+    CK(cudaStreamSynchronize(s), "total");
     ctx->err.clear();
     return HETEFF_OK;
 }

@@ -157,6 +157,18 @@ size_t region_tiles(int64_t dn);
 cudaError_t launch_regions_phase1(const RegParams &p, cudaStream_t s);
 cudaError_t launch_regions_phase2(const RegParams &p, cudaStream_t s);
 
+// interval algebra (intervals.cu): the reference's intervals.py:40-105
+size_t iv_flatten_ws(int64_t n);
+cudaError_t iv_flatten(const u64 *s, const u64 *e, int64_t n, u64 *os, u64 *oe, int64_t *out_n, int64_t *bad,
+                       void *ws, size_t ws_bytes, cudaStream_t st);
+size_t iv_subtract_ws(int64_t na, int64_t nb);
+cudaError_t iv_subtract(const u64 *as, const u64 *ae, int64_t na, const u64 *bs, const u64 *be, int64_t nb, u64 *os,
+                        u64 *oe, int64_t *out_n, void *ws, size_t ws_bytes, cudaStream_t st);
+size_t iv_intersect_ws(int64_t n);
+cudaError_t iv_intersect(const u64 *s, const u64 *e, int64_t n, u64 lo, u64 hi, u64 *os, u64 *oe, int64_t *out_n,
+                         void *ws, size_t ws_bytes, cudaStream_t st);
+cudaError_t iv_total(const u64 *s, const u64 *e, int64_t n, u64 *out2_dev, cudaStream_t st);
+
 // K3 (sort.cu): stable radix sort of one record set by (res, start)
 struct SortStats {
     int key_bits, passes, wide, start_sorted;

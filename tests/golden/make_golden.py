@@ -393,11 +393,59 @@ def regions_corpus() -> list:
     return out
 
 
+# ---------------------------------------------------------------------------
+# interval algebra (intervals.py:40-105), acceptance criterion 2 shapes
+# ---------------------------------------------------------------------------
+def _enc_flat(f):
+    return [[iv.start, iv.end] for iv in f]
+
+
+def intervals_corpus() -> list:
+    from heteff.intervals import complement
+
+    rng = random.Random(0x5EED02)
+    out = []
+    for i in range(400):
+        k = rng.randint(0, 40)
+        hi = rng.choice([30, 200, 10_000])
+        raw_a = []
+        for _ in range(k):
+            s = rng.randint(0, hi)
+            raw_a.append((s, s + rng.choice([0, 0, 1, 2, rng.randint(0, hi // 3 + 1)])))
+        raw_b = []
+        for _ in range(rng.randint(0, 40)):
+            s = rng.randint(0, hi)
+            raw_b.append((s, s + rng.randint(0, hi // 4 + 1)))
+        case = {"a": raw_a, "b": raw_b}
+        if i % 25 == 7 and raw_a:                       # malformed input
+            j = rng.randrange(len(raw_a))
+            raw_a[j] = (raw_a[j][0] + 5, raw_a[j][0])
+            case["a"] = raw_a
+            try:
+                flatten(Interval(s, e) for s, e in raw_a)
+                case["flat_a"] = None
+            except ValueError as exc:
+                case["error"] = str(exc)
+            out.append(case)
+            continue
+        fa = flatten(Interval(s, e) for s, e in raw_a)
+        fb = flatten(Interval(s, e) for s, e in raw_b)
+        b0 = rng.randint(0, hi)
+        bounds = (b0, b0 + rng.randint(0, hi))
+        case.update({
+            "flat_a": _enc_flat(fa), "flat_b": _enc_flat(fb), "sub": _enc_flat(subtract(fa, fb)),
+            "bounds": list(bounds), "comp": _enc_flat(complement(fa, Interval(*bounds))),
+            "inter": _enc_flat(intersect(fa, Interval(*bounds))), "total": total_duration(fa),
+        })
+        out.append(case)
+    return out
+
+
 def main() -> None:
     only = sys.argv[sys.argv.index("--only") + 1].split(",") if "--only" in sys.argv else None
     jobs = {"presets": presets, "acceptance": acceptance_corpora, "invalid": invalid_corpus,
             "summarize_device": summarize_device_corpus, "metrics": metrics_corpus,
-            "config_shards": config_shards, "regions": regions_corpus}
+            "config_shards": config_shards, "regions": regions_corpus, "intervals": intervals_corpus}
     for name, fn in jobs.items():
         if only is None or name in only:
             write(name, fn())
