@@ -371,15 +371,24 @@ int heteff_analyze_regions(heteff_ctx *ctx, const heteff_trace *t, const heteff_
     const int W = hb::kMaxWindows;
     const int64_t hid = t->host_ids > 0 ? t->host_ids : 1, did = t->dev_ids > 0 ? t->dev_ids : 1;
     const int64_t tiles = (int64_t)hb::region_tiles(t->dev.count);
+    const int64_t hch = (int64_t)hb::region_hchunks(t->host.count);
     const int64_t nn = t->n > 0 ? t->n : 1, mm = t->m > 0 ? t->m : 1;
     auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
-    const size_t b_hseg = up((size_t)(hid + 1) * 8), b_hacc = up((size_t)W * hid * 24), b_dacc = up((size_t)W * did * 32);
-    const size_t b_E = up(W * 8), b_dmax = up(W * 8), b_tagg = up((size_t)(tiles + 1) * 24);
-    const size_t b_tcar = up((size_t)(tiles + 1) * 16), b_own = up((size_t)did * 4);
-    CK(ensure(ctx->reg_ws, b_hseg + b_hacc + b_dacc + b_E + b_dmax + b_tagg + b_tcar + b_own, false), "alloc regions");
+    const int64_t scan_blocks = ((hch > tiles ? hch : tiles) + 1023) / 1024 + 1;   // per seg_scan
+    const size_t b_hseg = up((size_t)(hid + 1) * 8), b_dseg = up((size_t)(did + 1) * 8);
+    const size_t b_hagg = up((size_t)(hch + 1) * 48), b_hck = up((size_t)(hch + 1) * 40);
+    const size_t b_dagg = up((size_t)(tiles + 1) * 24), b_drun = up((size_t)(tiles + 1) * 16);
+    const size_t b_dsum = up((size_t)(tiles + 1) * 32), b_dck = up((size_t)(tiles + 1) * 24);
+    const size_t b_scan = up((size_t)scan_blocks * 64), b_tst = up((size_t)(tiles + 1) * 16);
+    const size_t b_dsub = up((size_t)(tiles + 1) * 8 * 64);
+    const size_t b_hacc = up((size_t)W * hid * 24), b_dacc = up((size_t)W * did * 32);
+    const size_t b_E = up(W * 8), b_dmax = up(W * 8), b_own = up((size_t)did * 4);
+    CK(ensure(ctx->reg_ws, b_hseg + b_dseg + b_hagg + b_hck + b_dagg + b_drun + b_dsum + b_dck + b_scan + b_tst + b_dsub + b_hacc +
+                               b_dacc + b_E + b_dmax + b_own, false),
+       "alloc regions");
     const size_t b_ho = up((size_t)W * nn * 32), b_do = up((size_t)W * mm * 32), b_bo = up((size_t)W * mm * 8);
     const size_t b_res = up(W * sizeof(hb::RegionResultDev));
-    CK(ensure(ctx->reg_out, 2 * (b_ho + b_do + b_bo + b_res), false), "alloc region outputs");
+    CK(ensure(ctx->reg_out, b_ho + b_do + b_bo + b_res, false), "alloc region outputs");
     uint8_t *w = static_cast<uint8_t *>(ctx->reg_ws.p);
     hb::RegParams p;
     memset(&p, 0, sizeof(p));
@@ -391,15 +400,25 @@ int heteff_analyze_regions(heteff_ctx *ctx, const heteff_trace *t, const heteff_
     p.host_decl = t->host_decl; p.dev_decl = t->dev_decl;
     p.n = t->n; p.m = t->m;
     size_t o = 0;
-    p.hseg = reinterpret_cast<int64_t *>(w + o); o += b_hseg;
-    p.h_acc = reinterpret_cast<u64 *>(w + o); o += b_hacc;
-    p.d_acc = reinterpret_cast<u64 *>(w + o); o += b_dacc;
-    p.E = reinterpret_cast<u64 *>(w + o); o += b_E;
-    p.dmax = reinterpret_cast<u64 *>(w + o); o += b_dmax;
-    p.tagg = reinterpret_cast<u64 *>(w + o); o += b_tagg;
-    p.tcarry = reinterpret_cast<u64 *>(w + o); o += b_tcar;
-    int32_t *own = reinterpret_cast<int32_t *>(w + o); o += b_own;
+    auto take = [&](size_t b) { void *q = w + o; o += b; return q; };
+    p.hseg = static_cast<int64_t *>(take(b_hseg));
+    p.dseg = static_cast<int64_t *>(take(b_dseg));
+    p.hagg = static_cast<u64 *>(take(b_hagg));
+    p.hck = static_cast<u64 *>(take(b_hck));
+    p.dagg = static_cast<u64 *>(take(b_dagg));
+    p.drun = static_cast<u64 *>(take(b_drun));
+    p.dsum = static_cast<u64 *>(take(b_dsum));
+    p.dck = static_cast<u64 *>(take(b_dck));
+    p.scan_tmp = static_cast<u64 *>(take(b_scan));
+    p.tstage = static_cast<int64_t *>(take(b_tst));
+    p.dsub = static_cast<u64 *>(take(b_dsub));
+    p.h_acc = static_cast<u64 *>(take(b_hacc));
+    p.d_acc = static_cast<u64 *>(take(b_dacc));
+    p.E = static_cast<u64 *>(take(b_E));
+    p.dmax = static_cast<u64 *>(take(b_dmax));
+    int32_t *own = static_cast<int32_t *>(take(b_own));
     p.tiles = tiles;
+    p.hchunks = hch;
     if (rg->dev_owner && t->dev_ids > 0) {
         CK(cudaMemcpyAsync(own, rg->dev_owner, (size_t)t->dev_ids * 4, cudaMemcpyHostToDevice, s), "h2d owners");
         p.owner = own;
@@ -409,9 +428,18 @@ int heteff_analyze_regions(heteff_ctx *ctx, const heteff_trace *t, const heteff_
     p.dev_out = reinterpret_cast<u64 *>(ob + b_ho);
     p.busy_out = reinterpret_cast<u64 *>(ob + b_ho + b_do);
     p.res = reinterpret_cast<hb::RegionResultDev *>(ob + b_ho + b_do + b_bo);
-    // pinned staging of a pass's results (the second half of reg_out is not used on the device)
     hb::RegionResultDev rh[hb::kMaxWindows];
     float total_ms = 0.f;
+    // window-independent checkpoints, once
+    CK(cudaEventRecord(ctx->ev0, s), "event");
+    CK(hb::launch_regions_prepare(p, s), "launch regions prepare");
+    CK(cudaEventRecord(ctx->ev1, s), "event");
+    CK(cudaEventSynchronize(ctx->ev1), "regions prepare");
+    {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        total_ms += ms;
+    }
     for (int32_t j0 = 0; j0 < rg->count; j0 += W) {
         const int R = rg->count - j0 < W ? rg->count - j0 : W;
         p.R = R;
@@ -422,8 +450,6 @@ int heteff_analyze_regions(heteff_ctx *ctx, const heteff_trace *t, const heteff_
             p.whi[j] = b > a ? b : a;
             p.wtop[j] = a;
         }
-        CK(cudaMemsetAsync(p.h_acc, 0, b_hacc, s), "memset");
-        CK(cudaMemsetAsync(p.d_acc, 0, b_dacc, s), "memset");
         CK(cudaMemsetAsync(p.E, 0, b_E + b_dmax, s), "memset");
         CK(cudaEventRecord(ctx->ev0, s), "event");
         CK(hb::launch_regions_phase1(p, s), "launch regions phase 1");

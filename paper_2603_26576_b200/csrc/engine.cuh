@@ -139,21 +139,28 @@ struct RegParams {
     u64 wlo[kMaxWindows], whi[kMaxWindows]; // window bounds, padded with empty [0, 0)
     u64 wtop[kMaxWindows];                  // phase 2: wlo + E (the region's clamp end)
     const int32_t *owner;                   // [dev_ids] dense host id or -1 (null = none)
-    int64_t *hseg;                          // [host_ids + 1] host CSR offsets
+    int64_t *hseg, *dseg;                   // [ids + 1] CSR offsets per dense id
+    // window-independent checkpoints (prefix of the resource's segment at each chunk start)
+    int64_t hchunks, tiles;
+    u64 *hagg, *hck;                        // host chunks: [c][6] f,off,mpi,max end,max off end,max mpi end / [c+1][5]
+    u64 *dagg, *drun;                       // device tiles: [t][3] f,max K end,max end / [t+1][2]
+    u64 *dsum, *dck;                        // device tiles: [t][4] f,U_K,U_KM,busy / [t+1][3]
+    int64_t *tstage;                        // device tiles: [t][2] owner host index range to stage
+    u64 *dsub;                              // device tiles: [t][8 sub-checkpoints][8] in-tile prefixes
+    u64 *scan_tmp;                          // [blocks][8] scan scratch
     u64 *h_acc;                             // [R][host_ids][3] offload, mpi, span
     u64 *d_acc;                             // [R][dev_ids][4] kernel, kernel|memory, clamped, busy
     u64 *E;                                 // [R]
     u64 *dmax;                              // [R] max clipped device end (device-only traces)
-    u64 *tagg;                              // [tiles][3]
-    u64 *tcarry;                            // [tiles][2]
-    int64_t tiles;
     u64 *host_out;                          // [R][n][4]
     u64 *dev_out;                           // [R][m][4]
     u64 *busy_out;                          // [R][m]
     RegionResultDev *res;                   // [R]
 };
 
+size_t region_hchunks(int64_t hn);
 size_t region_tiles(int64_t dn);
+cudaError_t launch_regions_prepare(const RegParams &p, cudaStream_t s);
 cudaError_t launch_regions_phase1(const RegParams &p, cudaStream_t s);
 cudaError_t launch_regions_phase2(const RegParams &p, cudaStream_t s);
 
