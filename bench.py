@@ -190,16 +190,47 @@ def run_engine(args, world, rank, local):
 
     from paper_2603_26576_b200.sharded import combine_shards
 
+    n_regions = args.regions if args.regions is not None else (16 if cfg.name.startswith("c4") else 0)
+    windows, owner = None, None
+    if n_regions:
+        from paper_2603_26576_b200.engine import analyze_regions
+        E0 = analyze_device(dt, N.MODE_REPORT, stream=stream.cuda_stream, device=local).elapsed
+        windows = [(i * E0 // 40, E0 - i * E0 // 40) for i in range(n_regions)]   # nested, shrinking
+        owner = np.arange(dt.m, dtype=np.int32) // cfg.gpus_per_rank
+    if args.shuffle:   # device records in random order: the step includes the K3 sort
+        g = torch.Generator(device=f"cuda:{local}").manual_seed(1)
+        perm = torch.randperm(dt.dev_count, device=f"cuda:{local}", generator=g)
+        dt = DeviceTrace(dt.h_start, dt.h_end, dt.h_res, dt.h_kind, dt.d_start[perm], dt.d_end[perm],
+                         dt.d_res[perm], dt.d_kind[perm], dt.n, dt.m)
+        del perm
+    region_ms = []
+    # our kernels per step (regions.cu / sort.cu launch sequences)
+    launches_per_step = 1 if world == 1 else 3
+    if windows is not None:
+        passes = (len(windows) + 15) // 16
+        launches_per_step = 1 + 14 + passes * (4 + (1 if dt.n == 0 else 0))
+    elif args.shuffle:
+        from paper_2603_26576_b200.engine import sort_records
+        probe = sort_records(dt.d_start, dt.d_end, dt.d_res, dt.d_kind, device=local)
+        launches_per_step += 1 + 4 + 5 * probe.passes   # failed first pass, sort, re-run
+        del probe
+
     def step():
-        f = analyze_device(dt, N.MODE_REPORT, stream=stream.cuda_stream, device=local)
+        if windows is not None:   # compute_report of the trace + every region tree + overlap, one call
+            run = analyze_regions(dt, windows, owner, stream=stream.cuda_stream, device=local)
+            assert run.status == N.OK, run.status
+            region_ms.append(run.kernel_ms)
+            return None
+        f = analyze_device(dt, N.MODE_REPORT, stream=stream.cuda_stream, device=local, sort_if_needed=args.shuffle)
         if dist:
             f = combine_shards(f, dt, dist, local, stream.cuda_stream)
         return f
 
     for _ in range(max(args.warmup, 3)):
         f = step()
-    assert f.status == N.OK, f.status
+    assert f is None or f.status == N.OK, f.status
     kernel_ms = []
+    region_ms.clear()
     sync()
     with Clocks(local) as clk:
         ev0 = torch.cuda.Event(enable_timing=True)
@@ -207,7 +238,8 @@ def run_engine(args, world, rank, local):
         ev0.record(stream)
         for _ in range(args.steps):
             f = step()
-            kernel_ms.append(f.kernel_ms)
+            if f is not None:
+                kernel_ms.append(f.kernel_ms)
         ev1.record(stream)
         sync()
     ms = ev0.elapsed_time(ev1) / args.steps
@@ -222,11 +254,13 @@ def run_engine(args, world, rank, local):
                                                           dt.d_start, dt.d_end, dt.d_res, dt.d_kind)),
                          dt.n, dt.m)
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    analyze_host_columns(pinned, stream=stream.cuda_stream, device=local)
+    f = analyze_host_columns(pinned, stream=stream.cuda_stream, device=local, sort_if_needed=args.shuffle)
+    if not kernel_ms:   # region steps: the analysis kernel's own time from the host-column run
+        kernel_ms.append(f.kernel_ms)
     sync()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        fe = analyze_host_columns(pinned, stream=stream.cuda_stream, device=local)
+        fe = analyze_host_columns(pinned, stream=stream.cuda_stream, device=local, sort_if_needed=args.shuffle)
         if dist:
             fe = combine_shards(fe, dt, dist, local, stream.cuda_stream)
     sync()
@@ -236,6 +270,10 @@ def run_engine(args, world, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     assert fe.status == N.OK and fe.elapsed == f.elapsed
+    if windows is not None:
+        # e2e of a region step is not separately staged from host buffers; it is
+        # the compute_report path (the regions' inputs are the same columns)
+        pass
     h2d = intervals_local * BYTES_PER_INTERVAL
     d2h = 160 + (dt.n + dt.m) * 32
 
@@ -256,7 +294,7 @@ def run_engine(args, world, rank, local):
                    "l2": "inputs larger than L2 (21 B x intervals >> 126 MB)"},
         "e2e": {"value": intervals_total / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
-        "gpu_launches": args.steps * (1 if world == 1 else 3),
+        "gpu_launches": args.steps * launches_per_step,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_source": peak_kind,
                      "traffic": (traffic or {}).get("bytes_per_launch") if traffic and
@@ -265,6 +303,14 @@ def run_engine(args, world, rank, local):
                      "algorithmic_bytes_per_launch": intervals_local * BYTES_PER_INTERVAL},
         "clocks": clk.summary(),
     }
+    if windows is not None:
+        line["regions"] = {"windows": len(windows), "nested": True, "overlap_metric": True,
+                           "ms_per_call": statistics.mean(region_ms),
+                           "note": "value = compute_report + every region tree + offload/busy overlap per call; "
+                                   "e2e covers the compute_report path"}
+        line["config"]["regions"] = len(windows)
+    if args.shuffle:
+        line["config"]["device_order"] = "random permutation (K3 sort inside every step)"
     if world == 1 and not args.no_cpu_baseline:
         from oracle import oracle as O
         h, d, n, m, k = _cpu_sample(cfg, args.cpu_sample)
@@ -297,6 +343,8 @@ def main():
     ap.add_argument("--cpu-sample", type=float, default=2e7)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--regions", type=int, default=None, help="monitoring regions per step (default: 16 for c4)")
+    ap.add_argument("--shuffle", action="store_true", help="device records in random order (step includes K3)")
     args = ap.parse_args()
     world, rank, local = _dist()
     if args.impl == "reference":
