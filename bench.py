@@ -167,7 +167,7 @@ def run_engine(args, world, rank, local):
     import torch
 
     from paper_2603_26576_b200 import _native as N
-    from paper_2603_26576_b200.engine import DeviceTrace, analyze_device, analyze_host_columns
+    from paper_2603_26576_b200.engine import AnalysisPlan, DeviceTrace, analyze_device, analyze_host_columns
     from paper_2603_26576_b200.synth import generate
 
     torch.cuda.set_device(local)
@@ -215,16 +215,18 @@ def run_engine(args, world, rank, local):
         launches_per_step += 1 + 4 + 5 * probe.passes   # failed first pass, sort, re-run
         del probe
 
+    plan = AnalysisPlan(dt, N.MODE_REPORT, stream=stream.cuda_stream, device=local, sort_if_needed=args.shuffle)
+
     def step():
         if windows is not None:   # compute_report of the trace + every region tree + overlap, one call
             run = analyze_regions(dt, windows, owner, stream=stream.cuda_stream, device=local)
             assert run.status == N.OK, run.status
             region_ms.append(run.kernel_ms)
             return None
-        f = analyze_device(dt, N.MODE_REPORT, stream=stream.cuda_stream, device=local, sort_if_needed=args.shuffle)
         if dist:
-            f = combine_shards(f, dt, dist, local, stream.cuda_stream)
-        return f
+            f = analyze_device(dt, N.MODE_REPORT, stream=stream.cuda_stream, device=local)
+            return combine_shards(f, dt, dist, local, stream.cuda_stream)
+        return plan.run()
 
     for _ in range(max(args.warmup, 3)):
         f = step()

@@ -47,6 +47,11 @@ struct heteff_ctx {
     DevBuf reg_ws, reg_out;
     // interval algebra scratch
     DevBuf iv_ws;
+    // one contiguous result block per analysis: [ResultDev | host summaries | device summaries],
+    // mirrored into pinned host memory by a single D2H copy
+    DevBuf out_blk;
+    void *out_pin = nullptr;
+    size_t out_pin_bytes = 0;
 };
 
 static int fail(heteff_ctx *ctx, int code, const std::string &msg)
@@ -89,6 +94,8 @@ static cudaError_t reset_globals(heteff_ctx *ctx)
     return cudaMemcpy(ctx->g, &g0, sizeof(g0), cudaMemcpyHostToDevice);
 }
 
+static_assert(sizeof(hb::ResultDev) <= 256, "result header slot of the output block");
+
 extern "C" {
 
 int heteff_abi_version(void) { return HETEFF_ABI_VERSION; }
@@ -113,12 +120,13 @@ void heteff_destroy(heteff_ctx *ctx)
 {
     if (!ctx) return;
     DevBuf *bufs[] = {&ctx->host_acc, &ctx->dev_acc, &ctx->host_tiles, &ctx->dev_tiles, &ctx->host_out,
-                      &ctx->dev_out, &ctx->lists, &ctx->stage, &ctx->aux, &ctx->sort_ws, &ctx->sorted, &ctx->reg_ws, &ctx->reg_out, &ctx->iv_ws};
+                      &ctx->dev_out, &ctx->lists, &ctx->stage, &ctx->aux, &ctx->sort_ws, &ctx->sorted, &ctx->reg_ws, &ctx->reg_out, &ctx->iv_ws, &ctx->out_blk};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->g) cudaFree(ctx->g);
     if (ctx->res_d) cudaFree(ctx->res_d);
     if (ctx->res_h) cudaFreeHost(ctx->res_h);
+    if (ctx->out_pin) cudaFreeHost(ctx->out_pin);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     delete ctx;
@@ -159,8 +167,16 @@ static int run_once(heteff_ctx *ctx, const heteff_trace *t, const heteff_options
         CK(ensure(ctx->dev_tiles, (size_t)(dt + 1) * 64, true), "alloc device tile status");
         ctx->dev_tiles_cap = (int64_t)(ctx->dev_tiles.bytes / 64);
     }
-    CK(ensure(ctx->host_out, (size_t)(t->n > 0 ? t->n : 1) * 4 * sizeof(u64), false), "alloc host summaries");
-    CK(ensure(ctx->dev_out, (size_t)(t->m > 0 ? t->m : 1) * 4 * sizeof(u64), false), "alloc device summaries");
+    const size_t ob_res = 256, ob_h = (size_t)(t->n > 0 ? t->n : 0) * 32, ob_d = (size_t)(t->m > 0 ? t->m : 0) * 32;
+    const size_t ob_total = ob_res + ob_h + ob_d;
+    CK(ensure(ctx->out_blk, ob_total, false), "alloc result block");
+    if (ctx->out_pin_bytes < ob_total) {
+        if (ctx->out_pin) cudaFreeHost(ctx->out_pin);
+        ctx->out_pin = nullptr;
+        ctx->out_pin_bytes = 0;
+        CK(cudaMallocHost(&ctx->out_pin, ob_total + ob_total / 4), "alloc pinned results");
+        ctx->out_pin_bytes = ob_total + ob_total / 4;
+    }
     if (opt->list_capacity > ctx->lists_cap) {
         CK(ensure(ctx->lists, (size_t)opt->list_capacity * 8 * sizeof(int64_t), false), "alloc lists");
         ctx->lists_cap = opt->list_capacity;
@@ -207,34 +223,30 @@ static int run_once(heteff_ctx *ctx, const heteff_trace *t, const heteff_options
     p.g = ctx->g;
     int64_t *lb = static_cast<int64_t *>(ctx->lists.p);
     for (int i = 0; i < 8; ++i) p.lists[i] = lb ? lb + (size_t)i * (size_t)ctx->lists_cap : nullptr;
-    p.host_out = static_cast<u64 *>(ctx->host_out.p);
-    p.dev_out = static_cast<u64 *>(ctx->dev_out.p);
-    p.res = ctx->res_d;
+    uint8_t *blk = static_cast<uint8_t *>(ctx->out_blk.p);
+    p.res = reinterpret_cast<hb::ResultDev *>(blk);
+    p.host_out = reinterpret_cast<u64 *>(blk + ob_res);
+    p.dev_out = reinterpret_cast<u64 *>(blk + ob_res + ob_h);
+    const bool want_sums = out && (out->host_summaries || out->device_summaries);
+    const size_t ob_copy = want_sums ? ob_total : sizeof(hb::ResultDev);
 
     CK(cudaEventRecord(ctx->ev0, s), "event");
     CK(hb::launch_analyze(p, ctx->grid, s), "launch analyze");
     CK(cudaEventRecord(ctx->ev1, s), "event");
-    CK(cudaMemcpyAsync(ctx->res_h, ctx->res_d, sizeof(hb::ResultDev), cudaMemcpyDeviceToHost, s), "d2h result");
-    if (out && out->host_summaries && t->n > 0)
-        CK(cudaMemcpyAsync(out->host_summaries, ctx->host_out.p, (size_t)t->n * 4 * sizeof(u64),
-                           cudaMemcpyDeviceToHost, s), "d2h host summaries");
-    if (out && out->device_summaries && t->m > 0)
-        CK(cudaMemcpyAsync(out->device_summaries, ctx->dev_out.p, (size_t)t->m * 4 * sizeof(u64),
-                           cudaMemcpyDeviceToHost, s), "d2h device summaries");
+    CK(cudaMemcpyAsync(ctx->out_pin, blk, ob_copy, cudaMemcpyDeviceToHost, s), "d2h results");
     CK(cudaStreamSynchronize(s), "analysis");
-    if (ctx->res_h->status == -1) {
+    if (reinterpret_cast<const hb::ResultDev *>(ctx->out_pin)->status == -1) {
         // some host records overlap: exact overlap findings, then the finalize
         CK(ensure(ctx->aux, (size_t)(ht + 1) * 3 * sizeof(u64), false), "alloc overlap scratch");
         CK(hb::launch_overlap_pass(p, static_cast<u64 *>(ctx->aux.p), s), "launch overlap pass");
-        CK(cudaMemcpyAsync(ctx->res_h, ctx->res_d, sizeof(hb::ResultDev), cudaMemcpyDeviceToHost, s), "d2h result");
-        if (out && out->host_summaries && t->n > 0)
-            CK(cudaMemcpyAsync(out->host_summaries, ctx->host_out.p, (size_t)t->n * 4 * sizeof(u64),
-                               cudaMemcpyDeviceToHost, s), "d2h host summaries");
-        if (out && out->device_summaries && t->m > 0)
-            CK(cudaMemcpyAsync(out->device_summaries, ctx->dev_out.p, (size_t)t->m * 4 * sizeof(u64),
-                               cudaMemcpyDeviceToHost, s), "d2h device summaries");
+        CK(cudaMemcpyAsync(ctx->out_pin, blk, ob_copy, cudaMemcpyDeviceToHost, s), "d2h results");
         CK(cudaStreamSynchronize(s), "overlap pass");
     }
+    *ctx->res_h = *reinterpret_cast<const hb::ResultDev *>(ctx->out_pin);
+    if (out && out->host_summaries && t->n > 0)
+        memcpy(out->host_summaries, static_cast<uint8_t *>(ctx->out_pin) + ob_res, ob_h);
+    if (out && out->device_summaries && t->m > 0)
+        memcpy(out->device_summaries, static_cast<uint8_t *>(ctx->out_pin) + ob_res + ob_h, ob_d);
     const hb::ResultDev &r = *ctx->res_h;
     if (perms && opt->list_capacity > 0) {   // sorted re-run: list entries back to input positions
         for (int i = 0; i < 8; ++i) {

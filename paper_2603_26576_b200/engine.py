@@ -185,6 +185,40 @@ def analyze_device(dt: DeviceTrace, mode: int = N.MODE_REPORT, elapsed: int = 0,
     return _findings(res, host_sum[: dt.n], dev_sum[: dt.m], [])
 
 
+class AnalysisPlan:
+    """Repeated analysis of the same HBM-resident columns (online monitoring, benches):
+    the ABI structs and the host output arrays are built once, so a call is one C
+    entry (launch + one D2H of the result block + sync) with no per-call Python
+    allocation.  ``run()`` returns the shared :class:`Findings` (overwritten by the
+    next call)."""
+
+    def __init__(self, dt: DeviceTrace, mode: int = N.MODE_REPORT, elapsed: int = 0, stream: int | None = None,
+                 device: int | None = None, sort_if_needed: bool = False):
+        self.ctx = N.context(device)
+        self.lib = N.load()
+        self.dt = dt   # keeps the columns alive
+        self.t = device_trace_abi(dt)
+        self.host_sum = np.zeros((max(dt.n, 1), 4), dtype=np.uint64)
+        self.dev_sum = np.zeros((max(dt.m, 1), 4), dtype=np.uint64)
+        self.out = N.Outputs(_ptr(self.host_sum), _ptr(self.dev_sum), (C.c_void_p * N.NUM_LISTS)())
+        self.opt = N.Options(mode, N.FLAG_SORT_IF_NEEDED if sort_if_needed else 0, elapsed, 0)
+        self.res = N.Result()
+        self.stream = C.c_void_p(stream) if stream else None
+        self._args = (self.ctx, C.byref(self.t), C.byref(self.opt), C.byref(self.res), C.byref(self.out),
+                      self.stream)
+
+    def run(self) -> Findings:
+        rc = self.lib.heteff_analyze(*self._args)
+        _check(self.ctx, rc)
+        return _findings(self.res, self.host_sum[: self.dt.n], self.dev_sum[: self.dt.m], [])
+
+    def run_status(self) -> int:
+        """The analysis only; results stay in ``self.res`` / ``self.host_sum`` / ``self.dev_sum``."""
+        rc = self.lib.heteff_analyze(*self._args)
+        _check(self.ctx, rc)
+        return rc
+
+
 def analyze_host_columns(dt: DeviceTrace, mode: int = N.MODE_REPORT, stream: int | None = None,
                          device: int | None = None, sort_if_needed: bool = False) -> Findings:
     """Same as :func:`analyze_device` but the columns are HOST tensors (pinned); H2D inside."""

@@ -198,3 +198,18 @@ def test_c2_shuffled_full_size_bit_identical():
     assert got.elapsed == ref.elapsed
     assert np.array_equal(got.dev_sum, ref.dev_sum) and np.array_equal(got.host_sum, ref.host_sum)
     assert got.device_metrics == ref.device_metrics and got.host_metrics == ref.host_metrics
+
+
+def test_analysis_plan_repeated_runs_match():
+    """engine.AnalysisPlan (prebuilt ABI structs, one D2H per call) == analyze_device."""
+    from paper_2603_26576_b200.engine import AnalysisPlan
+
+    cfg, h, d, _, _ = _shuffled_config("c1", 1, local=False)
+    dt = _dt(h, d, cfg.n_ranks, cfg.n_devices)
+    ref = analyze_device(dt)
+    plan = AnalysisPlan(dt)
+    for _ in range(3):
+        got = plan.run()
+        assert got.status == N.OK and got.elapsed == ref.elapsed
+        assert np.array_equal(got.host_sum, ref.host_sum) and np.array_equal(got.dev_sum, ref.dev_sum)
+        assert got.host_metrics == ref.host_metrics and got.device_metrics == ref.device_metrics
