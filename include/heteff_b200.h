@@ -57,7 +57,8 @@ typedef enum {
     HETEFF_CONTRACT = 4,        /* input not in canonical order / bad kind code */
     HETEFF_CUDA_ERROR = 5,
     HETEFF_NOMEM = 6,
-    HETEFF_BAD_ARG = 7
+    HETEFF_BAD_ARG = 7,
+    HETEFF_PARSE_FALLBACK = 8   /* heteff_parse_trace: not decided by the fast path (see below) */
 } heteff_status;
 
 typedef enum {
@@ -205,6 +206,35 @@ int heteff_intersect(heteff_ctx *ctx, const uint64_t *start, const uint64_t *end
                      uint64_t hi, uint64_t *out_start, uint64_t *out_end, int64_t *out_n, void *stream);
 int heteff_total_duration(heteff_ctx *ctx, const uint64_t *start, const uint64_t *end, int64_t n, uint64_t out[2],
                           void *stream);
+
+/* ---- native trace documents (docs/formats.md:9-85) -> record columns ----
+ * heteff_parse_trace <- read_trace (trace_io.py:96-158).  Host memory only; a
+ * string-aware skip scan finds every hosts[] / devices[] entry, then the
+ * entries are parsed in parallel (nthreads, 0 = all cores).  Records come out in
+ * FILE order with the document's own rank / device ids.  Documents the fast path
+ * cannot decide exactly (schema errors, integers beyond u64, duplicate keys,
+ * non-integer numbers, escaped keys) return HETEFF_PARSE_FALLBACK with the byte
+ * offset; the caller re-parses them with a strict reader for the reference's
+ * exact TraceFormatError text. */
+typedef struct heteff_parsed heteff_parsed;
+
+typedef struct {
+    int64_t n_hosts, n_devices, n_host_records, n_dev_records;
+    const uint64_t *host_rank;  /* [n_hosts] */
+    const int64_t *host_off;    /* [n_hosts + 1] record offsets per host entry */
+    const uint64_t *dev_id;     /* [n_devices] */
+    const int64_t *dev_owner;   /* [n_devices] owner_rank, -1 when absent / null */
+    const int64_t *dev_off;     /* [n_devices + 1] */
+    const uint8_t *h_kind;      /* 0 useful 1 offload 2 mpi */
+    const uint64_t *h_start, *h_end;
+    const uint8_t *d_kind;      /* 0 kernel 1 memory */
+    const int64_t *d_stream;    /* -1 when absent / null */
+    const uint64_t *d_start, *d_end;
+} heteff_parsed_view;
+
+int heteff_parse_trace(const char *data, size_t len, int nthreads, heteff_parsed **out, int64_t *fail_offset);
+void heteff_parsed_info(const heteff_parsed *parsed, heteff_parsed_view *view);
+void heteff_parsed_free(heteff_parsed *parsed);
 
 /* ---- EXTENSIONS (not in the reference) ----
  * Monitoring regions (K5) and offload-wait / device-busy overlap (K6).

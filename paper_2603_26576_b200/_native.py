@@ -16,7 +16,7 @@ from pathlib import Path
 LIB_PATH = Path(os.environ.get("HETEFF_LIB", Path(__file__).resolve().parent / "libheteff_b200.so"))
 
 # status codes (heteff_status)
-OK, INVALID_TRACE, ANALYSIS_ERROR, VALUE_ERROR, CONTRACT, CUDA_ERROR, NOMEM, BAD_ARG = range(8)
+OK, INVALID_TRACE, ANALYSIS_ERROR, VALUE_ERROR, CONTRACT, CUDA_ERROR, NOMEM, BAD_ARG, PARSE_FALLBACK = range(9)
 # modes (heteff_mode)
 MODE_REPORT, MODE_SUMMARIZE_DEVICE, MODE_VALIDATE, MODE_SUMMARIZE_HOST = range(4)
 # list classes
@@ -108,6 +108,7 @@ EXPORTED = (
     "heteff_host_metrics", "heteff_device_metrics", "heteff_generate", "heteff_prof_read",
     "heteff_sort_records", "heteff_analyze_regions",
     "heteff_flatten", "heteff_subtract", "heteff_intersect", "heteff_total_duration",
+    "heteff_parse_trace", "heteff_parsed_info", "heteff_parsed_free",
 )
 
 _lib = None
@@ -154,6 +155,12 @@ def load() -> C.CDLL:
                                      _p]
     lib.heteff_total_duration.restype = C.c_int
     lib.heteff_total_duration.argtypes = [_p, _p, _p, C.c_int64, _p, _p]
+    lib.heteff_parse_trace.restype = C.c_int
+    lib.heteff_parse_trace.argtypes = [C.c_char_p, C.c_size_t, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]
+    lib.heteff_parsed_info.restype = None
+    lib.heteff_parsed_info.argtypes = [C.c_void_p, C.c_void_p]
+    lib.heteff_parsed_free.restype = None
+    lib.heteff_parsed_free.argtypes = [C.c_void_p]
     lib.heteff_generate.restype = C.c_int
     lib.heteff_generate.argtypes = [_p, C.POINTER(GenSide), _p, _p, _p, _p, _p]
     _lib = lib

@@ -1,0 +1,456 @@
+// ingest.cpp -- native trace documents (docs/formats.md:9-85, the reference's
+// read_trace, trace_io.py:96-158) parsed straight into record columns.
+//
+// Two phases:
+//   1. one sequential, string-aware skip scan over the document finds the
+//      top-level fields and the byte range of every hosts[] / devices[] entry
+//      (no values are decoded);
+//   2. the entries are parsed in parallel (std::thread, dynamic claiming), each
+//      by a strict recursive-descent parser of exactly the reference schema,
+//      into per-entry column slices; a prefix sum places every slice.
+// Records come out in FILE order with their original rank / device ids; the
+// Python layer assigns dense ids and the canonical order (or hands unsorted
+// columns to the K3 GPU sort).
+//
+// Anything the fast path does not decide exactly -- a schema error (whose
+// message carries a JSON path), an integer beyond u64, a duplicate key, a
+// non-integer number -- returns HETEFF_PARSE_FALLBACK with the byte offset;
+// the Python layer then re-parses with its strict restatement of read_trace,
+// which produces the reference's exact TraceFormatError text.
+#include <atomic>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/heteff_b200.h"
+
+namespace {
+
+struct Cursor {
+    const char *p, *e;
+    bool ok = true;
+    void ws()
+    {
+        while (p < e && (*p == ' ' || *p == '\n' || *p == '\r' || *p == '\t')) ++p;
+    }
+    bool eat(char c)
+    {
+        ws();
+        if (p < e && *p == c) { ++p; return true; }
+        return false;
+    }
+    bool peek(char c)
+    {
+        ws();
+        return p < e && *p == c;
+    }
+};
+
+// a JSON string without escapes (keys and enum values of the schema); escapes -> fallback
+bool plain_string(Cursor &c, const char *&s, size_t &n)
+{
+    c.ws();
+    if (c.p >= c.e || *c.p != '"') return false;
+    const char *q = static_cast<const char *>(memchr(c.p + 1, '"', (size_t)(c.e - c.p - 1)));
+    if (!q) return false;
+    for (const char *t = c.p + 1; t < q; ++t)
+        if (*t == '\\' || (unsigned char)*t < 0x20) return false;
+    s = c.p + 1;
+    n = (size_t)(q - s);
+    c.p = q + 1;
+    return true;
+}
+
+// non-negative integer that fits u64; anything else (sign, fraction, exponent, overflow) -> false
+bool u64_number(Cursor &c, uint64_t &v)
+{
+    c.ws();
+    const char *q = c.p;
+    if (q >= c.e || *q < '0' || *q > '9') return false;
+    if (*q == '0' && q + 1 < c.e && q[1] >= '0' && q[1] <= '9') return false;   // leading zero: invalid JSON
+    uint64_t x = 0;
+    const char *b = q;
+    while (q < c.e && (unsigned)(*q - '0') < 10u) {
+        if (q - b >= 19) {   // a 20th digit may overflow: checked multiply-add
+            unsigned long long y;
+            if (__builtin_mul_overflow((unsigned long long)x, 10ull, &y) ||
+                __builtin_add_overflow(y, (unsigned long long)(*q - '0'), &y))
+                return false;
+            x = y;
+        } else {
+            x = x * 10 + (uint64_t)(*q - '0');
+        }
+        ++q;
+    }
+    if (q < c.e && (*q == '.' || *q == 'e' || *q == 'E')) return false;
+    v = x;
+    c.p = q;
+    return true;
+}
+
+bool is_null(Cursor &c)
+{
+    c.ws();
+    if (c.e - c.p >= 4 && memcmp(c.p, "null", 4) == 0) { c.p += 4; return true; }
+    return false;
+}
+
+template <size_t L>
+inline bool key_is(const char *s, size_t n, const char (&lit)[L])
+{
+    return n == L - 1 && memcmp(s, lit, L - 1) == 0;
+}
+
+// structural-character table for the phase-1 skip scan
+struct Structural {
+    bool t[256];
+    Structural()
+    {
+        memset(t, 0, sizeof(t));
+        t[(unsigned char)'"'] = t[(unsigned char)'{'] = t[(unsigned char)'['] = true;
+        t[(unsigned char)'}'] = t[(unsigned char)']'] = true;
+    }
+};
+const Structural kStruct;
+
+// end of a string body starting at p (just after the opening quote): the closing quote
+inline const char *string_end(const char *p, const char *e)
+{
+    for (;;) {
+        const char *q = static_cast<const char *>(memchr(p, '"', (size_t)(e - p)));
+        if (!q) return nullptr;
+        // count the backslashes right before the quote: an even number means it closes
+        const char *b = q;
+        while (b > p && b[-1] == '\\') --b;
+        if (((q - b) & 1) == 0) return q;
+        p = q + 1;
+    }
+}
+
+// skip any JSON value (string-aware), used only by the phase-1 scan
+bool skip_value(Cursor &c)
+{
+    c.ws();
+    if (c.p >= c.e) return false;
+    const char ch = *c.p;
+    if (ch == '"') {
+        ++c.p;
+        while (c.p < c.e && *c.p != '"') {
+            if (*c.p == '\\') ++c.p;
+            ++c.p;
+        }
+        if (c.p >= c.e) return false;
+        ++c.p;
+        return true;
+    }
+    if (ch == '{' || ch == '[') {
+        int depth = 0;
+        const char *p = c.p, *e = c.e;
+        while (p < e) {
+            while (p < e && !kStruct.t[(unsigned char)*p]) ++p;
+            if (p >= e) break;
+            const char x = *p;
+            if (x == '"') {
+                p = string_end(p + 1, e);
+                if (!p) return false;
+            } else if (x == '{' || x == '[') {
+                ++depth;
+            } else if (--depth == 0) {
+                c.p = p + 1;
+                return true;
+            }
+            ++p;
+        }
+        return false;
+    }
+    while (c.p < c.e && *c.p != ',' && *c.p != '}' && *c.p != ']' && *c.p != ' ' && *c.p != '\n' && *c.p != '\r' &&
+           *c.p != '\t')
+        ++c.p;
+    return true;
+}
+
+struct Entry {
+    const char *b, *e;   // the entry object's bytes
+    bool device;
+};
+
+struct Slice {
+    uint64_t id = 0;
+    int64_t owner = -1;
+    std::vector<uint8_t> kind;
+    std::vector<int64_t> stream;
+    std::vector<uint64_t> start, end;
+    const char *fail = nullptr;   // first byte the fast path could not decide
+};
+
+// { "state": s, "start": a, "end": b } / { "kind": k, ["stream": x,] "start": a, "end": b } in any key order
+bool parse_record(Cursor &c, bool device, Slice &out)
+{
+    if (!c.eat('{')) return false;
+    bool h_state = false, h_start = false, h_end = false, h_stream = false;
+    uint8_t kind = 0;
+    int64_t stream = -1;
+    uint64_t s = 0, e = 0;
+    if (!c.peek('}')) {
+        do {
+            const char *k;
+            size_t kn;
+            if (!plain_string(c, k, kn) || !c.eat(':')) return false;
+            if (!device && key_is(k, kn, "state")) {
+                if (h_state) return false;
+                const char *v;
+                size_t vn;
+                if (!plain_string(c, v, vn)) return false;
+                if (key_is(v, vn, "useful")) kind = 0;
+                else if (key_is(v, vn, "offload")) kind = 1;
+                else if (key_is(v, vn, "mpi")) kind = 2;
+                else return false;
+                h_state = true;
+            } else if (device && key_is(k, kn, "kind")) {
+                if (h_state) return false;
+                const char *v;
+                size_t vn;
+                if (!plain_string(c, v, vn)) return false;
+                if (key_is(v, vn, "kernel")) kind = 0;
+                else if (key_is(v, vn, "memory")) kind = 1;
+                else return false;
+                h_state = true;
+            } else if (device && key_is(k, kn, "stream")) {
+                if (h_stream) return false;
+                if (!is_null(c)) {
+                    uint64_t x;
+                    if (!u64_number(c, x) || x > (uint64_t)INT64_MAX) return false;
+                    stream = (int64_t)x;
+                }
+                h_stream = true;
+            } else if (key_is(k, kn, "start")) {
+                if (h_start || !u64_number(c, s)) return false;
+                h_start = true;
+            } else if (key_is(k, kn, "end")) {
+                if (h_end || !u64_number(c, e)) return false;
+                h_end = true;
+            } else {
+                return false;   // unknown field
+            }
+        } while (c.eat(','));
+    }
+    if (!c.eat('}') || !h_state || !h_start || !h_end) return false;
+    out.kind.push_back(kind);
+    if (device) out.stream.push_back(stream);
+    out.start.push_back(s);
+    out.end.push_back(e);
+    return true;
+}
+
+bool parse_entry(const Entry &en, Slice &out)
+{
+    Cursor c{en.b, en.e};
+    const size_t guess = (size_t)(en.e - en.b) / 40 + 4;
+    out.kind.reserve(guess);
+    out.start.reserve(guess);
+    out.end.reserve(guess);
+    if (en.device) out.stream.reserve(guess);
+    if (!c.eat('{')) { out.fail = c.p; return false; }
+    bool h_id = false, h_owner = false, h_recs = false;
+    if (!c.peek('}')) {
+        do {
+            const char *k;
+            size_t kn;
+            if (!plain_string(c, k, kn) || !c.eat(':')) { out.fail = c.p; return false; }
+            if (!en.device && key_is(k, kn, "rank")) {
+                if (h_id || !u64_number(c, out.id)) { out.fail = c.p; return false; }
+                h_id = true;
+            } else if (en.device && key_is(k, kn, "id")) {
+                if (h_id || !u64_number(c, out.id)) { out.fail = c.p; return false; }
+                h_id = true;
+            } else if (en.device && key_is(k, kn, "owner_rank")) {
+                if (h_owner) { out.fail = c.p; return false; }
+                if (!is_null(c)) {
+                    uint64_t x;
+                    if (!u64_number(c, x) || x > (uint64_t)INT64_MAX) { out.fail = c.p; return false; }
+                    out.owner = (int64_t)x;
+                }
+                h_owner = true;
+            } else if (key_is(k, kn, "records")) {
+                if (h_recs || !c.eat('[')) { out.fail = c.p; return false; }
+                if (!c.peek(']')) {
+                    do {
+                        if (!parse_record(c, en.device, out)) { out.fail = c.p; return false; }
+                    } while (c.eat(','));
+                }
+                if (!c.eat(']')) { out.fail = c.p; return false; }
+                h_recs = true;
+            } else {
+                out.fail = c.p;
+                return false;
+            }
+        } while (c.eat(','));
+    }
+    if (!c.eat('}') || !h_id || !h_recs) { out.fail = c.p; return false; }
+    return true;
+}
+
+}  // namespace
+
+struct heteff_parsed {
+    std::vector<uint64_t> host_rank, dev_id;
+    std::vector<int64_t> dev_owner;
+    std::vector<int64_t> host_off, dev_off;   // [entries + 1] record offsets per entry
+    std::vector<uint8_t> h_kind, d_kind;
+    std::vector<int64_t> d_stream;
+    std::vector<uint64_t> h_start, h_end, d_start, d_end;
+};
+
+extern "C" {
+
+int heteff_parse_trace(const char *data, size_t len, int nthreads, heteff_parsed **out, int64_t *fail_offset)
+{
+    if (!data || !out || !fail_offset) return HETEFF_BAD_ARG;
+    *out = nullptr;
+    *fail_offset = -1;
+    Cursor c{data, data + len};
+    auto fail = [&](const char *at) {
+        *fail_offset = (int64_t)(at - data);
+        return HETEFF_PARSE_FALLBACK;
+    };
+    // ---- phase 1: top level + entry byte ranges
+    if (c.e - c.p >= 3 && (unsigned char)c.p[0] == 0xEF && (unsigned char)c.p[1] == 0xBB) return fail(c.p);   // BOM
+    if (!c.eat('{')) return fail(c.p);
+    bool h_ver = false, h_tu = false, h_hosts = false, h_devs = false;
+    std::vector<Entry> entries;
+    size_t n_hosts = 0;
+    if (!c.peek('}')) {
+        do {
+            const char *k;
+            size_t kn;
+            if (!plain_string(c, k, kn) || !c.eat(':')) return fail(c.p);
+            if (key_is(k, kn, "version")) {
+                uint64_t v;
+                if (h_ver || !u64_number(c, v) || v != 1) return fail(c.p);
+                h_ver = true;
+            } else if (key_is(k, kn, "time_unit")) {
+                const char *v;
+                size_t vn;
+                if (h_tu || !plain_string(c, v, vn) || !key_is(v, vn, "ns")) return fail(c.p);
+                h_tu = true;
+            } else if (key_is(k, kn, "hosts") || key_is(k, kn, "devices")) {
+                const bool dev = key_is(k, kn, "devices");
+                if ((dev ? h_devs : h_hosts) || !c.eat('[')) return fail(c.p);
+                std::vector<Entry> mine;
+                if (!c.peek(']')) {
+                    do {
+                        c.ws();
+                        const char *b = c.p;
+                        if (!c.peek('{') || !skip_value(c)) return fail(b);
+                        mine.push_back(Entry{b, c.p, dev});
+                    } while (c.eat(','));
+                }
+                if (!c.eat(']')) return fail(c.p);
+                if (dev) {
+                    h_devs = true;
+                    entries.insert(entries.end(), mine.begin(), mine.end());
+                } else {
+                    h_hosts = true;
+                    entries.insert(entries.begin(), mine.begin(), mine.end());   // hosts first
+                    n_hosts = mine.size();
+                }
+            } else {
+                return fail(c.p);
+            }
+        } while (c.eat(','));
+    }
+    if (!c.eat('}') || !h_ver || !h_tu || !h_hosts || !h_devs) return fail(c.p);
+    c.ws();
+    if (c.p != c.e) return fail(c.p);
+
+    // ---- phase 2: entries in parallel
+    std::vector<Slice> slices(entries.size());
+    std::atomic<size_t> next{0};
+    int nt = nthreads > 0 ? nthreads : (int)std::thread::hardware_concurrency();
+    if (nt < 1) nt = 1;
+    if ((size_t)nt > entries.size()) nt = entries.size() > 0 ? (int)entries.size() : 1;
+    auto work = [&]() {
+        for (;;) {
+            const size_t i = next.fetch_add(1);
+            if (i >= entries.size()) break;
+            if (!parse_entry(entries[i], slices[i]) && !slices[i].fail) slices[i].fail = entries[i].b;
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+    work();
+    for (auto &th : pool) th.join();
+    for (const Slice &s : slices)
+        if (s.fail) return fail(s.fail);
+
+    // ---- merge in file order
+    heteff_parsed *P = new heteff_parsed();
+    size_t nh = 0, nd = 0;
+    P->host_off.push_back(0);
+    P->dev_off.push_back(0);
+    for (size_t i = 0; i < entries.size(); ++i) {
+        if (i < n_hosts) { nh += slices[i].start.size(); P->host_off.push_back((int64_t)nh); }
+        else { nd += slices[i].start.size(); P->dev_off.push_back((int64_t)nd); }
+    }
+    P->h_kind.resize(nh); P->h_start.resize(nh); P->h_end.resize(nh);
+    P->d_kind.resize(nd); P->d_stream.resize(nd); P->d_start.resize(nd); P->d_end.resize(nd);
+    std::atomic<size_t> nx{0};
+    auto copy = [&]() {
+        for (;;) {
+            const size_t i = nx.fetch_add(1);
+            if (i >= entries.size()) break;
+            const Slice &s = slices[i];
+            const size_t k = s.start.size();
+            if (!k) continue;
+            if (i < n_hosts) {
+                const size_t o = (size_t)P->host_off[i];
+                memcpy(&P->h_kind[o], s.kind.data(), k);
+                memcpy(&P->h_start[o], s.start.data(), 8 * k);
+                memcpy(&P->h_end[o], s.end.data(), 8 * k);
+            } else {
+                const size_t o = (size_t)P->dev_off[i - n_hosts];
+                memcpy(&P->d_kind[o], s.kind.data(), k);
+                memcpy(&P->d_stream[o], s.stream.data(), 8 * k);
+                memcpy(&P->d_start[o], s.start.data(), 8 * k);
+                memcpy(&P->d_end[o], s.end.data(), 8 * k);
+            }
+        }
+    };
+    pool.clear();
+    for (int t = 1; t < nt; ++t) pool.emplace_back(copy);
+    copy();
+    for (auto &th : pool) th.join();
+    for (size_t i = 0; i < entries.size(); ++i) {
+        if (i < n_hosts) P->host_rank.push_back(slices[i].id);
+        else { P->dev_id.push_back(slices[i].id); P->dev_owner.push_back(slices[i].owner); }
+    }
+    *out = P;
+    return HETEFF_OK;
+}
+
+void heteff_parsed_info(const heteff_parsed *P, heteff_parsed_view *v)
+{
+    v->n_hosts = (int64_t)P->host_rank.size();
+    v->n_devices = (int64_t)P->dev_id.size();
+    v->n_host_records = (int64_t)P->h_start.size();
+    v->n_dev_records = (int64_t)P->d_start.size();
+    v->host_rank = P->host_rank.data();
+    v->host_off = P->host_off.data();
+    v->dev_id = P->dev_id.data();
+    v->dev_owner = P->dev_owner.data();
+    v->dev_off = P->dev_off.data();
+    v->h_kind = P->h_kind.data();
+    v->h_start = P->h_start.data();
+    v->h_end = P->h_end.data();
+    v->d_kind = P->d_kind.data();
+    v->d_stream = P->d_stream.data();
+    v->d_start = P->d_start.data();
+    v->d_end = P->d_end.data();
+}
+
+void heteff_parsed_free(heteff_parsed *P) { delete P; }
+
+}  // extern "C"

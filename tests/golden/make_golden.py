@@ -441,11 +441,83 @@ def intervals_corpus() -> list:
     return out
 
 
+# ---------------------------------------------------------------------------
+# native trace documents (trace_io.py:96-193, docs/formats.md:9-85)
+# ---------------------------------------------------------------------------
+def trace_docs_corpus() -> list:
+    from heteff import TraceFormatError, read_trace, write_trace
+
+    out = []
+    rng = random.Random(0x5EED08)
+    for i in range(150):                                   # acceptance criterion 8 shapes
+        t = random_valid_trace(rng, max_ranks=4, max_devices=3, max_segments=8)
+        doc = write_trace(t).decode()
+        out.append({"tag": f"rt{i}", "doc": doc, "trace": enc_trace(read_trace(doc))})
+    for name in ("usecase1", "usecase3", "usecase7b"):
+        doc = write_trace(heteff.build(heteff.preset(name, 7))).decode()
+        out.append({"tag": name, "doc": doc, "trace": enc_trace(read_trace(doc))})
+    base = {"version": 1, "time_unit": "ns",
+            "hosts": [{"rank": 3, "records": [{"state": "mpi", "start": 0, "end": 5},
+                                              {"state": "useful", "start": 5, "end": 9}]},
+                      {"rank": 1, "records": []}],
+            "devices": [{"id": 7, "owner_rank": 3, "records": [{"kind": "kernel", "stream": 2, "start": 1, "end": 4},
+                                                               {"kind": "memory", "start": 0, "end": 2}]},
+                        {"id": 2, "owner_rank": None, "records": []}]}
+    variants = {
+        "compact": json.dumps(base, separators=(",", ":")),
+        "reordered_keys": json.dumps({"devices": base["devices"], "hosts": base["hosts"], "time_unit": "ns",
+                                      "version": 1}),
+        "spaces": json.dumps(base, indent=5).replace(":", " : "),
+        "big_u64": json.dumps({**base, "hosts": [{"rank": 0, "records": [
+            {"state": "offload", "start": 2**64 - 5, "end": 2**64 - 1}]}]}),
+        "beyond_u64": json.dumps({**base, "hosts": [{"rank": 0, "records": [
+            {"state": "offload", "start": 1, "end": 2**64 + 7}]}]}),
+        "dup_key": '{"version": 1, "version": 1, "time_unit": "ns", "hosts": [], "devices": []}',
+        "escaped_key": '{"version": 1, "time_\u0075nit": "ns", "hosts": [], "devices": []}',
+        "float_version": '{"version": 1.0, "time_unit": "ns", "hosts": [], "devices": []}',
+        "bool_version": '{"version": true, "time_unit": "ns", "hosts": [], "devices": []}',
+        "not_json": '{"version": 1,, }',
+        "not_object": '[1, 2]',
+        "bad_version": json.dumps({**base, "version": 2}),
+        "bad_unit": json.dumps({**base, "time_unit": "us"}),
+        "missing_hosts": json.dumps({k: v for k, v in base.items() if k != "hosts"}),
+        "extra_top": json.dumps({**base, "zeta": 1}),
+        "hosts_not_list": json.dumps({**base, "hosts": {}}),
+        "neg_start": json.dumps({**base, "hosts": [{"rank": 0, "records": [{"state": "mpi", "start": -1, "end": 3}]}]}),
+        "float_end": json.dumps({**base, "hosts": [{"rank": 0, "records": [{"state": "mpi", "start": 1, "end": 3.5}]}]}),
+        "bool_rank": json.dumps({**base, "hosts": [{"rank": True, "records": []}]}),
+        "bad_state": json.dumps({**base, "hosts": [{"rank": 0, "records": [{"state": "MPI", "start": 1, "end": 3}]}]}),
+        "bad_kind": json.dumps({**base, "devices": [{"id": 0, "records": [{"kind": "idle", "start": 1, "end": 3}]}]}),
+        "extra_rec": json.dumps({**base, "hosts": [{"rank": 0, "records": [
+            {"state": "mpi", "start": 1, "end": 3, "x": 0}]}]}),
+        "missing_end": json.dumps({**base, "devices": [{"id": 0, "records": [{"kind": "kernel", "start": 1}]}]}),
+        "neg_stream": json.dumps({**base, "devices": [{"id": 0, "records": [
+            {"kind": "kernel", "stream": -2, "start": 1, "end": 3}]}]}),
+        "neg_owner": json.dumps({**base, "devices": [{"id": 0, "owner_rank": -1, "records": []}]}),
+        "rec_not_obj": json.dumps({**base, "hosts": [{"rank": 0, "records": [5]}]}),
+        "entry_not_obj": json.dumps({**base, "devices": [7]}),
+        "trailing": json.dumps(base) + " x",
+        "empty": "",
+        "nan": '{"version": 1, "time_unit": "ns", "hosts": [{"rank": NaN, "records": []}], "devices": []}',
+        "string_brace": json.dumps({**base, "hosts": [{"rank": 0, "records": [{"state": "mp}i", "start": 1, "end": 3}]}]}),
+        "null_stream": json.dumps({**base, "devices": [{"id": 0, "records": [
+            {"kind": "kernel", "stream": None, "start": 1, "end": 3}]}]}),
+    }
+    for tag, doc in variants.items():
+        try:
+            t = read_trace(doc)
+            out.append({"tag": tag, "doc": doc, "trace": enc_trace(t)})
+        except TraceFormatError as e:
+            out.append({"tag": tag, "doc": doc, "error": str(e)})
+    return out
+
+
 def main() -> None:
     only = sys.argv[sys.argv.index("--only") + 1].split(",") if "--only" in sys.argv else None
     jobs = {"presets": presets, "acceptance": acceptance_corpora, "invalid": invalid_corpus,
             "summarize_device": summarize_device_corpus, "metrics": metrics_corpus,
-            "config_shards": config_shards, "regions": regions_corpus, "intervals": intervals_corpus}
+            "config_shards": config_shards, "regions": regions_corpus, "intervals": intervals_corpus,
+            "trace_docs": trace_docs_corpus}
     for name, fn in jobs.items():
         if only is None or name in only:
             write(name, fn())
