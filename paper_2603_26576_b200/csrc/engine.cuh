@@ -9,7 +9,7 @@ typedef unsigned long long u64;
 
 // tile geometry (compile-time knobs, see tools/build_variants.sh)
 #ifndef HB_WARPS
-#define HB_WARPS 13
+#define HB_WARPS 15
 #endif
 #ifndef HB_EPI
 #define HB_EPI 2
