@@ -236,6 +236,42 @@ int heteff_parse_trace(const char *data, size_t len, int nthreads, heteff_parsed
 void heteff_parsed_info(const heteff_parsed *parsed, heteff_parsed_view *view);
 void heteff_parsed_free(heteff_parsed *parsed);
 
+/* ---- Chrome-trace-event documents + mapping rules -> records ----
+ * heteff_import_events <- import_mapped (trace_io.py:263-342, docs/formats.md:87-132).
+ * Only complete-span ("ph": "X") events count; microseconds become nanoseconds
+ * exactly (x 1000; integer-valued floats accepted, fractional ones are the
+ * reference's error); the first matching rule wins.  Matched events come out in
+ * event order; unmapped "X" events are listed (index + name bytes) for the
+ * caller's warnings / MappingError.  Anything the fast path cannot decide
+ * exactly (an error the reference would raise, escaped strings, duplicate
+ * keys) returns HETEFF_PARSE_FALLBACK. */
+typedef struct {
+    int32_t field;              /* 0 name, 1 category */
+    int32_t mode;               /* 0 contains, 1 equals */
+    const char *pattern;        /* UTF-8 bytes */
+    int64_t pattern_len;
+    int32_t target;             /* 0 useful 1 offload 2 mpi 3 kernel 4 memory */
+    int32_t reserved;
+    int64_t resource;           /* >= 0 fixed id, -1 "pid", -2 "tid" */
+} heteff_rule;
+
+typedef struct heteff_imported heteff_imported;
+
+typedef struct {
+    int64_t n_records, n_unmapped;
+    const uint8_t *is_dev;      /* 1: device record */
+    const uint8_t *kind;        /* host: 0 useful 1 offload 2 mpi; device: 0 kernel 1 memory */
+    const uint64_t *res, *start, *end;
+    const int64_t *unmapped;    /* event indices */
+    const int64_t *name_off;    /* byte offset / length of each unmapped event's name */
+    const int64_t *name_len;
+} heteff_imported_view;
+
+int heteff_import_events(const char *data, size_t len, const heteff_rule *rules, int nrules, int nthreads,
+                         heteff_imported **out, int64_t *fail_offset);
+void heteff_imported_info(const heteff_imported *imported, heteff_imported_view *view);
+void heteff_imported_free(heteff_imported *imported);
+
 /* ---- EXTENSIONS (not in the reference) ----
  * Monitoring regions (K5) and offload-wait / device-busy overlap (K6).
  * Region j is a window [start_j, end_j).  Its report is compute_report

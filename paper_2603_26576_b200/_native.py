@@ -109,6 +109,7 @@ EXPORTED = (
     "heteff_sort_records", "heteff_analyze_regions",
     "heteff_flatten", "heteff_subtract", "heteff_intersect", "heteff_total_duration",
     "heteff_parse_trace", "heteff_parsed_info", "heteff_parsed_free",
+    "heteff_import_events", "heteff_imported_info", "heteff_imported_free",
 )
 
 _lib = None
@@ -161,6 +162,13 @@ def load() -> C.CDLL:
     lib.heteff_parsed_info.argtypes = [C.c_void_p, C.c_void_p]
     lib.heteff_parsed_free.restype = None
     lib.heteff_parsed_free.argtypes = [C.c_void_p]
+    lib.heteff_import_events.restype = C.c_int
+    lib.heteff_import_events.argtypes = [C.c_char_p, C.c_size_t, C.c_void_p, C.c_int, C.c_int,
+                                         C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]
+    lib.heteff_imported_info.restype = None
+    lib.heteff_imported_info.argtypes = [C.c_void_p, C.c_void_p]
+    lib.heteff_imported_free.restype = None
+    lib.heteff_imported_free.argtypes = [C.c_void_p]
     lib.heteff_generate.restype = C.c_int
     lib.heteff_generate.argtypes = [_p, C.POINTER(GenSide), _p, _p, _p, _p, _p]
     _lib = lib

@@ -20,6 +20,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdlib>
+#include <climits>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -294,6 +295,304 @@ bool parse_entry(const Entry &en, Slice &out)
 }
 
 }  // namespace
+
+
+// ---------------------------------------------------------------------------
+// Chrome-trace-event documents + mapping rules (import_mapped, trace_io.py:263-342)
+// ---------------------------------------------------------------------------
+namespace {
+
+struct Event {
+    const char *b, *e;
+};
+
+// a JSON number as exact nanoseconds (value * 1000): integers, or floats whose
+// value is an integer (the reference's _us_to_ns); anything else -> false
+bool us_to_ns(Cursor &c, uint64_t &ns)
+{
+    c.ws();
+    const char *q = c.p;
+    if (q >= c.e) return false;
+    if (*q == '-') return false;
+    const char *t = q;
+    bool fl = false;
+    while (t < c.e && ((*t >= '0' && *t <= '9') || *t == '.' || *t == 'e' || *t == 'E' || *t == '+' || *t == '-')) {
+        if (*t == '.' || *t == 'e' || *t == 'E') fl = true;
+        ++t;
+    }
+    if (t == q) return false;
+    uint64_t v = 0;
+    if (!fl) {
+        Cursor d{q, t};
+        if (!u64_number(d, v) || d.p != t) return false;
+    } else {
+        char buf[64];
+        if (t - q >= (long)sizeof(buf)) return false;
+        memcpy(buf, q, (size_t)(t - q));
+        buf[t - q] = 0;
+        char *endp = nullptr;
+        const double x = strtod(buf, &endp);
+        if (endp != buf + (t - q) || !(x >= 0) || x != (double)(uint64_t)x || x >= 1.8e19) return false;
+        v = (uint64_t)x;
+    }
+    if (v > UINT64_MAX / 1000) return false;
+    ns = v * 1000;
+    c.p = t;
+    return true;
+}
+
+struct RawEvent {
+    bool is_x = false;
+    const char *name = nullptr, *cat = nullptr;
+    size_t name_n = 0, cat_n = 0;
+    bool has_cat = false, has_ts = false, has_dur = false, has_pid = false, has_tid = false;
+    uint64_t ts = 0, dur = 0, pid = 0, tid = 0;
+    bool pid_ok = false, tid_ok = false;
+};
+
+// 1: parsed, 0: not an "X" event (skipped), -1: undecided (fallback)
+int parse_event(const Event &ev, RawEvent &r)
+{
+    Cursor c{ev.b, ev.e};
+    c.ws();
+    if (c.p >= c.e || *c.p != '{') return 0;   // not an object: ignored by the reference
+    ++c.p;
+    bool h_ph = false, h_name = false;
+    bool ph_x = false;
+    if (!c.peek('}')) {
+        do {
+            const char *k;
+            size_t kn;
+            if (!plain_string(c, k, kn) || !c.eat(':')) return -1;
+            if (key_is(k, kn, "ph")) {
+                if (h_ph) return -1;
+                h_ph = true;
+                c.ws();
+                if (c.p < c.e && *c.p == '"') {
+                    const char *v;
+                    size_t vn;
+                    if (!plain_string(c, v, vn)) return -1;
+                    ph_x = vn == 1 && v[0] == 'X';
+                } else if (!skip_value(c)) {
+                    return -1;
+                }
+            } else if (key_is(k, kn, "name") || key_is(k, kn, "cat")) {
+                const bool nm = k[0] == 'n';
+                if (nm ? h_name : r.has_cat) return -1;
+                c.ws();
+                if (c.p >= c.e || *c.p != '"') {   // a non-string name / cat is an error if the event is "X"
+                    if (!skip_value(c)) return -1;
+                    if (nm) { h_name = true; r.name = nullptr; }
+                    else { r.has_cat = true; r.cat = nullptr; }
+                    continue;
+                }
+                const char *v;
+                size_t vn;
+                if (!plain_string(c, v, vn)) return -1;
+                if (nm) { h_name = true; r.name = v; r.name_n = vn; }
+                else { r.has_cat = true; r.cat = v; r.cat_n = vn; }
+            } else if (key_is(k, kn, "ts") || key_is(k, kn, "dur")) {
+                const bool ts = k[0] == 't';
+                if (ts ? r.has_ts : r.has_dur) return -1;
+                const char *save = c.p;
+                uint64_t v;
+                if (!us_to_ns(c, v)) { c.p = save; if (!skip_value(c)) return -1; v = UINT64_MAX; }
+                if (ts) { r.has_ts = true; r.ts = v; } else { r.has_dur = true; r.dur = v; }
+            } else if (key_is(k, kn, "pid") || key_is(k, kn, "tid")) {
+                const bool pid = k[0] == 'p';
+                if (pid ? r.has_pid : r.has_tid) return -1;
+                const char *save = c.p;
+                uint64_t v = 0;
+                bool ok = u64_number(c, v);
+                if (!ok) { c.p = save; if (!skip_value(c)) return -1; }
+                if (pid) { r.has_pid = true; r.pid = v; r.pid_ok = ok; }
+                else { r.has_tid = true; r.tid = v; r.tid_ok = ok; }
+            } else {
+                if (!skip_value(c)) return -1;
+            }
+        } while (c.eat(','));
+    }
+    if (!c.eat('}')) return -1;
+    if (!h_ph || !ph_x) return 0;
+    r.is_x = true;
+    // the reference raises for these on an "X" event: leave the exact message to the fallback
+    if (!h_name || !r.name) return -1;
+    if (r.has_cat && !r.cat) return -1;
+    if (!r.has_ts || !r.has_dur || r.ts == UINT64_MAX || r.dur == UINT64_MAX) return -1;
+    if (r.ts > UINT64_MAX - r.dur) return -1;
+    return 1;
+}
+
+bool contains(const char *h, size_t hn, const char *n, size_t nn)
+{
+    if (nn == 0) return true;
+    if (nn > hn) return false;
+    const void *p = memmem(h, hn, n, nn);
+    return p != nullptr;
+}
+
+}  // namespace
+
+struct heteff_imported {
+    std::vector<uint8_t> is_dev, kind;
+    std::vector<uint64_t> res, start, end;
+    std::vector<int64_t> unmapped;            // event indices of unmapped "X" events
+    std::vector<int64_t> name_off;            // byte offset of each unmapped event's name in the document
+    std::vector<int64_t> name_len;
+};
+
+extern "C" {
+
+int heteff_import_events(const char *data, size_t len, const heteff_rule *rules, int nrules, int nthreads,
+                         heteff_imported **out, int64_t *fail_offset)
+{
+    if (!data || !out || !fail_offset || (nrules > 0 && !rules)) return HETEFF_BAD_ARG;
+    *out = nullptr;
+    *fail_offset = -1;
+    Cursor c{data, data + len};
+    auto fail = [&](const char *at) {
+        *fail_offset = (int64_t)(at - data);
+        return HETEFF_PARSE_FALLBACK;
+    };
+    if (c.e - c.p >= 3 && (unsigned char)c.p[0] == 0xEF && (unsigned char)c.p[1] == 0xBB) return fail(c.p);
+    // the events array: a bare array, or the traceEvents field of an object
+    std::vector<Event> events;
+    auto scan_array = [&](Cursor &a) -> bool {
+        if (!a.eat('[')) return false;
+        if (!a.peek(']')) {
+            do {
+                a.ws();
+                const char *b = a.p;
+                if (!skip_value(a)) return false;
+                events.push_back(Event{b, a.p});
+            } while (a.eat(','));
+        }
+        return a.eat(']');
+    };
+    c.ws();
+    if (c.peek('[')) {
+        if (!scan_array(c)) return fail(c.p);
+    } else if (c.eat('{')) {
+        bool found = false;
+        if (!c.peek('}')) {
+            do {
+                const char *k;
+                size_t kn;
+                if (!plain_string(c, k, kn) || !c.eat(':')) return fail(c.p);
+                if (key_is(k, kn, "traceEvents")) {
+                    if (found) return fail(c.p);
+                    found = true;
+                    if (!c.peek('[')) return fail(c.p);
+                    if (!scan_array(c)) return fail(c.p);
+                } else if (!skip_value(c)) {
+                    return fail(c.p);
+                }
+            } while (c.eat(','));
+        }
+        if (!c.eat('}') || !found) return fail(c.p);
+    } else {
+        return fail(c.p);
+    }
+    c.ws();
+    if (c.p != c.e) return fail(c.p);
+
+    // events in parallel: parse + first-match-wins rules
+    const size_t n = events.size();
+    std::vector<int8_t> status(n, 0);   // 1 mapped, 2 unmapped, 0 skipped, -1 fallback
+    std::vector<uint8_t> is_dev(n), kind(n);
+    std::vector<uint64_t> res(n), st(n), en(n);
+    std::vector<int64_t> noff(n), nlen(n);
+    std::atomic<size_t> next{0};
+    std::atomic<int64_t> first_fail{INT64_MAX};
+    const size_t chunk = 4096;
+    auto work = [&]() {
+        for (;;) {
+            const size_t c0 = next.fetch_add(chunk);
+            if (c0 >= n) break;
+            const size_t c1 = c0 + chunk < n ? c0 + chunk : n;
+            for (size_t i = c0; i < c1; ++i) {
+                RawEvent r;
+                const int pr = parse_event(events[i], r);
+                if (pr <= 0) { status[i] = (int8_t)pr; if (pr < 0) { int64_t cur = first_fail.load(); while ((int64_t)i < cur && !first_fail.compare_exchange_weak(cur, (int64_t)i)) {} } continue; }
+                int hit = -1;
+                for (int q = 0; q < nrules && hit < 0; ++q) {
+                    const heteff_rule &R = rules[q];
+                    const char *subj = R.field == 0 ? r.name : (r.has_cat ? r.cat : "");
+                    const size_t sn = R.field == 0 ? r.name_n : (r.has_cat ? r.cat_n : 0);
+                    const bool m = R.mode == 0 ? contains(subj, sn, R.pattern, (size_t)R.pattern_len)
+                                               : ((size_t)R.pattern_len == sn && memcmp(subj, R.pattern, sn) == 0);
+                    if (m) hit = q;
+                }
+                st[i] = r.ts;
+                en[i] = r.ts + r.dur;
+                noff[i] = (int64_t)(r.name - data);
+                nlen[i] = (int64_t)r.name_n;
+                if (hit < 0) { status[i] = 2; continue; }
+                const heteff_rule &R = rules[hit];
+                uint64_t rid = 0;
+                if (R.resource >= 0) {
+                    rid = (uint64_t)R.resource;
+                } else {
+                    const bool pid = R.resource == -1;
+                    const bool has = pid ? r.has_pid : r.has_tid, ok = pid ? r.pid_ok : r.tid_ok;
+                    if (!has || !ok) {   // the reference's _nonneg_int error: exact text from the fallback
+                        status[i] = -1;
+                        int64_t cur = first_fail.load();
+                        while ((int64_t)i < cur && !first_fail.compare_exchange_weak(cur, (int64_t)i)) {}
+                        continue;
+                    }
+                    rid = pid ? r.pid : r.tid;
+                }
+                status[i] = 1;
+                is_dev[i] = R.target >= 3;
+                kind[i] = (uint8_t)(R.target >= 3 ? R.target - 3 : R.target);
+                res[i] = rid;
+            }
+        }
+    };
+    int nt = nthreads > 0 ? nthreads : (int)std::thread::hardware_concurrency();
+    if (nt < 1) nt = 1;
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+    work();
+    for (auto &th : pool) th.join();
+    if (first_fail.load() != INT64_MAX) return fail(events[(size_t)first_fail.load()].b);
+
+    heteff_imported *I = new heteff_imported();
+    for (size_t i = 0; i < n; ++i) {
+        if (status[i] == 1) {
+            I->is_dev.push_back(is_dev[i]);
+            I->kind.push_back(kind[i]);
+            I->res.push_back(res[i]);
+            I->start.push_back(st[i]);
+            I->end.push_back(en[i]);
+        } else if (status[i] == 2) {
+            I->unmapped.push_back((int64_t)i);
+            I->name_off.push_back(noff[i]);
+            I->name_len.push_back(nlen[i]);
+        }
+    }
+    *out = I;
+    return HETEFF_OK;
+}
+
+void heteff_imported_info(const heteff_imported *I, heteff_imported_view *v)
+{
+    v->n_records = (int64_t)I->start.size();
+    v->n_unmapped = (int64_t)I->unmapped.size();
+    v->is_dev = I->is_dev.data();
+    v->kind = I->kind.data();
+    v->res = I->res.data();
+    v->start = I->start.data();
+    v->end = I->end.data();
+    v->unmapped = I->unmapped.data();
+    v->name_off = I->name_off.data();
+    v->name_len = I->name_len.data();
+}
+
+void heteff_imported_free(heteff_imported *I) { delete I; }
+
+}  // extern "C"
 
 struct heteff_parsed {
     std::vector<uint64_t> host_rank, dev_id;

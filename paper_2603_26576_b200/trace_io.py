@@ -264,3 +264,199 @@ def read_trace_packed(data, nthreads: int | None = None):
         tmp[found] = idx[found]
         owner[np.nonzero(ok)[0]] = tmp
     return packed, owner
+
+
+# ---------------------------------------------------------------------------
+# Chrome-trace-event import with mapping rules (trace_io.py:196-342)
+# ---------------------------------------------------------------------------
+from dataclasses import dataclass  # noqa: E402
+
+_TARGETS = {**_HOST_STATES, **_DEVICE_KINDS}
+_MATCH_KEYS = ("name_contains", "name_equals", "category_contains", "category_equals")
+_TARGET_CODE = {HostState.USEFUL: 0, HostState.OFFLOAD: 1, HostState.MPI: 2,
+                DeviceActivityKind.KERNEL: 3, DeviceActivityKind.MEMORY: 4}
+
+
+class MappingError(Exception):
+    """Import failed under default_policy=error: events matched no rule."""
+
+
+@dataclass(frozen=True)
+class MappingRule:
+    """One importer rule; the first matching rule in the list wins."""
+
+    field: str        # "name" | "category"
+    mode: str         # "contains" | "equals"
+    pattern: str
+    target: object    # HostState | DeviceActivityKind
+    resource: object  # fixed id, or "pid" / "tid"
+
+    def matches(self, name: str, category: str) -> bool:
+        subject = name if self.field == "name" else category
+        return self.pattern in subject if self.mode == "contains" else self.pattern == subject
+
+
+@dataclass(frozen=True)
+class CategoryMapping:
+    rules: tuple
+    default_policy: str   # "drop" | "error"
+
+
+def _load_named(data, what):
+    if isinstance(data, bytes):
+        try:
+            data = data.decode("utf-8")
+        except UnicodeDecodeError as e:
+            raise TraceFormatError(f"{what} is not UTF-8: {e}") from e
+    try:
+        return json.loads(data)
+    except json.JSONDecodeError as e:
+        raise TraceFormatError(f"{what} is not valid JSON: {e}") from e
+
+
+def read_mapping(data) -> CategoryMapping:
+    """Parse a mapping document (``trace_io.py:222-260``, ``docs/formats.md:87-132``)."""
+    doc = _expect_obj(_load_named(data, "mapping document"), "$")
+    policy = _pop(doc, "$", "default_policy")
+    if policy not in ("drop", "error"):
+        raise TraceFormatError(f"$.default_policy: expected 'drop' or 'error', got {policy!r}")
+    entries = _expect_list(_pop(doc, "$", "rules"), "$.rules")
+    if not entries:
+        raise TraceFormatError("$.rules: at least one rule is required")
+    rules = []
+    for i, entry in enumerate(entries):
+        path = f"$.rules[{i}]"
+        entry = _expect_obj(entry, path)
+        present = [k for k in _MATCH_KEYS if k in entry]
+        if len(present) != 1:
+            raise TraceFormatError(f"{path}: exactly one of {', '.join(_MATCH_KEYS)} is required")
+        key = present[0]
+        pattern = _pop(entry, path, key)
+        if not isinstance(pattern, str):
+            raise TraceFormatError(f"{path}.{key}: expected string, got {pattern!r}")
+        field, mode = key.rsplit("_", 1)
+        field = "category" if field == "category" else "name"
+        target = _choice(_pop(entry, path, "target"), _TARGETS, f"{path}.target")
+        resource = _pop(entry, path, "resource")
+        if isinstance(resource, bool) or not (isinstance(resource, int) or resource in ("pid", "tid")):
+            raise TraceFormatError(f"{path}.resource: expected non-negative integer, 'pid' or 'tid'; "
+                                   f"got {resource!r}")
+        if isinstance(resource, int) and resource < 0:
+            raise TraceFormatError(f"{path}.resource: negative value {resource}")
+        _done(entry, path)
+        rules.append(MappingRule(field, mode, pattern, target, resource))
+    _done(doc, "$")
+    return CategoryMapping(tuple(rules), policy)
+
+
+def _us_ns(v, path):
+    if isinstance(v, bool):
+        raise TraceFormatError(f"{path}: expected number, got {v!r}")
+    if isinstance(v, float):
+        if not v.is_integer():
+            raise TraceFormatError(f"{path}: fractional timestamp {v!r} (would require rounding)")
+        v = int(v)
+    if not isinstance(v, int):
+        raise TraceFormatError(f"{path}: expected number, got {v!r}")
+    if v < 0:
+        raise TraceFormatError(f"{path}: negative value {v}")
+    return v * 1000
+
+
+def _assemble(hrecs, drecs, unmapped, mapping):
+    if unmapped and mapping.default_policy == "error":
+        shown = "; ".join(f"event {i} ({nm!r})" for i, nm in unmapped[:10])
+        more = f" (+{len(unmapped) - 10} more)" if len(unmapped) > 10 else ""
+        raise MappingError(f"{len(unmapped)} event(s) matched no rule: {shown}{more}")
+    warnings = [] if mapping.default_policy == "error" else \
+        [f"dropped unmapped event {i} ({nm!r})" for i, nm in unmapped]
+    trace = Trace(host_processes=tuple(sorted({r.rank for r in hrecs})),
+                  devices=tuple(DeviceDecl(d) for d in sorted({r.device_id for r in drecs})),
+                  host_records=tuple(hrecs), device_records=tuple(drecs))
+    return trace, warnings
+
+
+def _import_py(data, mapping):
+    doc = _load_named(data, "events document")
+    events = _expect_list(doc.get("traceEvents"), "$.traceEvents") if isinstance(doc, dict) else \
+        _expect_list(doc, "$")
+    hrecs, drecs, unmapped = [], [], []
+    for i, ev in enumerate(events):
+        path = f"$[{i}]"
+        if not isinstance(ev, dict) or ev.get("ph") != "X":
+            continue
+        name = ev.get("name")
+        if not isinstance(name, str):
+            raise TraceFormatError(f"{path}.name: expected string, got {name!r}")
+        cat = ev.get("cat", "")
+        if not isinstance(cat, str):
+            raise TraceFormatError(f"{path}.cat: expected string, got {cat!r}")
+        for key in ("ts", "dur"):
+            if key not in ev:
+                raise TraceFormatError(f"{path}: missing required field {key!r}")
+        start = _us_ns(ev["ts"], f"{path}.ts")
+        end = start + _us_ns(ev["dur"], f"{path}.dur")
+        rule = next((r for r in mapping.rules if r.matches(name, cat)), None)
+        if rule is None:
+            unmapped.append((i, name))
+            continue
+        rid = rule.resource if isinstance(rule.resource, int) else \
+            _uint(ev.get(rule.resource), f"{path}.{rule.resource}")
+        if isinstance(rule.target, HostState):
+            hrecs.append(HostRecord(rid, rule.target, Interval(start, end)))
+        else:
+            drecs.append(DeviceRecord(rid, rule.target, Interval(start, end)))
+    return _assemble(hrecs, drecs, unmapped, mapping)
+
+
+class _Rule(C.Structure):
+    _fields_ = [("field", C.c_int32), ("mode", C.c_int32), ("pattern", C.c_char_p), ("pattern_len", C.c_int64),
+                ("target", C.c_int32), ("reserved", C.c_int32), ("resource", C.c_int64)]
+
+
+class _IView(C.Structure):
+    _fields_ = [("n_records", C.c_int64), ("n_unmapped", C.c_int64), ("is_dev", C.c_void_p), ("kind", C.c_void_p),
+                ("res", C.c_void_p), ("start", C.c_void_p), ("end", C.c_void_p), ("unmapped", C.c_void_p),
+                ("name_off", C.c_void_p), ("name_len", C.c_void_p)]
+
+
+def import_mapped(data, mapping: CategoryMapping, nthreads: int | None = None):
+    """Chrome-trace events -> (Trace, warnings) (drop-in for ``trace_io.py:263-342``)."""
+    raw = data.encode("utf-8") if isinstance(data, str) else bytes(data)
+    lib = N.load()
+    pats = [r.pattern.encode("utf-8") for r in mapping.rules]
+    rules = (_Rule * max(len(pats), 1))()
+    for q, (r, pb) in enumerate(zip(mapping.rules, pats)):
+        res = r.resource if isinstance(r.resource, int) else (-1 if r.resource == "pid" else -2)
+        rules[q] = _Rule(0 if r.field == "name" else 1, 0 if r.mode == "contains" else 1, pb, len(pb),
+                         _TARGET_CODE[r.target], 0, res)
+    handle = C.c_void_p()
+    off = C.c_int64(-1)
+    rc = lib.heteff_import_events(raw, len(raw), rules, len(pats), nthreads or os.cpu_count() or 1,
+                                  C.byref(handle), C.byref(off))
+    if rc == N.PARSE_FALLBACK:
+        return _import_py(data, mapping)
+    if rc != N.OK:
+        raise N.NativeError(f"event importer failed ({rc})")
+    try:
+        v = _IView()
+        lib.heteff_imported_info(handle, C.addressof(v))
+        k, u = v.n_records, v.n_unmapped
+        is_dev = _arr(v.is_dev, k, np.uint8).tolist()
+        kind = _arr(v.kind, k, np.uint8).tolist()
+        res = _arr(v.res, k, np.uint64).tolist()
+        st = _arr(v.start, k, np.uint64).tolist()
+        en = _arr(v.end, k, np.uint64).tolist()
+        um = _arr(v.unmapped, u, np.int64).tolist()
+        no = _arr(v.name_off, u, np.int64).tolist()
+        nl = _arr(v.name_len, u, np.int64).tolist()
+    finally:
+        lib.heteff_imported_free(handle)
+    hrecs, drecs = [], []
+    for d, kd, r, a, b in zip(is_dev, kind, res, st, en):
+        if d:
+            drecs.append(DeviceRecord(r, _DEV_CODE_KIND[kd], Interval(a, b)))
+        else:
+            hrecs.append(HostRecord(r, _HOST_CODE_STATE[kd], Interval(a, b)))
+    unmapped = [(i, raw[o:o + n].decode("utf-8")) for i, o, n in zip(um, no, nl)]
+    return _assemble(hrecs, drecs, unmapped, mapping)

@@ -512,12 +512,103 @@ def trace_docs_corpus() -> list:
     return out
 
 
+# ---------------------------------------------------------------------------
+# Chrome-trace import with mapping rules (trace_io.py:196-342)
+# ---------------------------------------------------------------------------
+def import_corpus() -> list:
+    from heteff import MappingError, TraceFormatError, import_mapped, read_mapping
+
+    rng = random.Random(0x5EED09)
+    names = ["cudaLaunchKernel", "my_kernel<128>", "Memcpy HtoD", "MPI_Allreduce", "compute", "cudaMemset",
+             "MPI_Wait", "kernel_b", "idle", "cudaDeviceSynchronize", "Ω-kernel"]
+    cats = ["cuda", "mpi", "cpu", "", "gpu"]
+    maps = [
+        {"default_policy": "drop", "rules": [
+            {"name_contains": "Memcpy", "target": "memory", "resource": "pid"},
+            {"name_contains": "kernel", "target": "kernel", "resource": "pid"},
+            {"name_contains": "cudaLaunch", "target": "offload", "resource": "tid"},
+            {"name_equals": "compute", "target": "useful", "resource": 0},
+            {"category_equals": "mpi", "target": "mpi", "resource": "pid"}]},
+        {"default_policy": "error", "rules": [
+            {"category_contains": "", "target": "useful", "resource": "tid"}]},
+        {"default_policy": "error", "rules": [
+            {"name_contains": "MPI", "target": "mpi", "resource": 3}]},
+    ]
+    out = []
+    for i in range(120):
+        evs = []
+        for _ in range(rng.randint(0, 40)):
+            ev = {"name": rng.choice(names), "ph": rng.choice(["X", "X", "X", "B", "M"]),
+                  "ts": rng.choice([rng.randint(0, 10**6), float(rng.randint(0, 10**5))]),
+                  "dur": rng.randint(0, 5000), "pid": rng.randint(0, 3), "tid": rng.randint(0, 5)}
+            if rng.random() < 0.7:
+                ev["cat"] = rng.choice(cats)
+            if rng.random() < 0.3:
+                ev["args"] = {"x": [1, {"y": "}]"}], "s": "a\"b"}
+            evs.append(ev)
+        doc = json.dumps({"traceEvents": evs, "displayTimeUnit": "ms"} if i % 2 else evs)
+        mp = json.dumps(maps[i % len(maps)])
+        case = {"tag": f"imp{i}", "doc": doc, "map": mp}
+        try:
+            t, w = import_mapped(doc, read_mapping(mp))
+            case.update({"trace": enc_trace(t), "warnings": w})
+        except (TraceFormatError, MappingError) as e:
+            case.update({"error": type(e).__name__, "msg": str(e)})
+        out.append(case)
+    m0 = json.dumps(maps[0])
+    odd = {
+        "frac_ts": [{"name": "compute", "ph": "X", "ts": 1.5, "dur": 1}],
+        "neg_dur": [{"name": "compute", "ph": "X", "ts": 1, "dur": -1}],
+        "no_dur": [{"name": "compute", "ph": "X", "ts": 1}],
+        "bool_ts": [{"name": "compute", "ph": "X", "ts": True, "dur": 1}],
+        "str_ts": [{"name": "compute", "ph": "X", "ts": "1", "dur": 1}],
+        "name_int": [{"name": 5, "ph": "X", "ts": 1, "dur": 1}],
+        "cat_int": [{"name": "compute", "cat": 3, "ph": "X", "ts": 1, "dur": 1}],
+        "pid_missing": [{"name": "my_kernel", "ph": "X", "ts": 1, "dur": 1}],
+        "pid_neg": [{"name": "my_kernel", "ph": "X", "ts": 1, "dur": 1, "pid": -4}],
+        "pid_float": [{"name": "my_kernel", "ph": "X", "ts": 1, "dur": 1, "pid": 2.0}],
+        "not_x_bad": [{"name": 5, "ph": "B", "ts": "q"}, {"name": "compute", "ph": "X", "ts": 2, "dur": 3}],
+        "events_not_list": {"traceEvents": 7},
+        "escaped_name": [{"name": "my\u005fkernel", "ph": "X", "ts": 1, "dur": 1, "pid": 1}],
+        "big_ts": [{"name": "compute", "ph": "X", "ts": 2**62, "dur": 1}],
+        "exp_ts": [{"name": "compute", "ph": "X", "ts": 1.5e3, "dur": 2e0}],
+        "dup_name": '[{"name": "x", "name": "compute", "ph": "X", "ts": 1, "dur": 1}]',
+    }
+    for tag, evs in odd.items():
+        doc = evs if isinstance(evs, str) else json.dumps(evs)
+        if tag == "escaped_name":
+            doc = doc.replace("\\\\u005f", "\\u005f")
+        case = {"tag": tag, "doc": doc, "map": m0}
+        try:
+            t, w = import_mapped(doc, read_mapping(m0))
+            case.update({"trace": enc_trace(t), "warnings": w})
+        except (TraceFormatError, MappingError) as e:
+            case.update({"error": type(e).__name__, "msg": str(e)})
+        out.append(case)
+    for tag, mp in {"no_rules": {"default_policy": "drop", "rules": []},
+                    "two_keys": {"default_policy": "drop", "rules": [
+                        {"name_contains": "a", "name_equals": "b", "target": "mpi", "resource": 0}]},
+                    "bad_policy": {"default_policy": "warn", "rules": []},
+                    "bad_resource": {"default_policy": "drop", "rules": [
+                        {"name_contains": "a", "target": "mpi", "resource": "rank"}]},
+                    "neg_resource": {"default_policy": "drop", "rules": [
+                        {"name_contains": "a", "target": "mpi", "resource": -1}]},
+                    "bad_target": {"default_policy": "drop", "rules": [
+                        {"name_contains": "a", "target": "idle", "resource": 0}]}}.items():
+        try:
+            read_mapping(json.dumps(mp))
+            out.append({"tag": tag, "map": json.dumps(mp), "map_ok": True})
+        except TraceFormatError as e:
+            out.append({"tag": tag, "map": json.dumps(mp), "error": "TraceFormatError", "msg": str(e)})
+    return out
+
+
 def main() -> None:
     only = sys.argv[sys.argv.index("--only") + 1].split(",") if "--only" in sys.argv else None
     jobs = {"presets": presets, "acceptance": acceptance_corpora, "invalid": invalid_corpus,
             "summarize_device": summarize_device_corpus, "metrics": metrics_corpus,
             "config_shards": config_shards, "regions": regions_corpus, "intervals": intervals_corpus,
-            "trace_docs": trace_docs_corpus}
+            "trace_docs": trace_docs_corpus, "imports": import_corpus}
     for name, fn in jobs.items():
         if only is None or name in only:
             write(name, fn())
