@@ -460,3 +460,31 @@ def import_mapped(data, mapping: CategoryMapping, nthreads: int | None = None):
             hrecs.append(HostRecord(r, _HOST_CODE_STATE[kd], Interval(a, b)))
     unmapped = [(i, raw[o:o + n].decode("utf-8")) for i, o, n in zip(um, no, nl)]
     return _assemble(hrecs, drecs, unmapped, mapping)
+
+
+def write_trace(trace: Trace) -> bytes:
+    """Deterministic native document (``trace_io.py:161-193``): equal traces, equal bytes."""
+    by_rank = {r: [] for r in trace.host_processes}
+    for rec in trace.host_records:
+        if rec.rank not in by_rank:
+            raise ValueError(f"host record references undeclared rank {rec.rank}")
+        by_rank[rec.rank].append({"state": rec.state.value, "start": rec.interval.start, "end": rec.interval.end})
+    by_dev = {d.device_id: [] for d in trace.devices}
+    for rec in trace.device_records:
+        if rec.device_id not in by_dev:
+            raise ValueError(f"device record references undeclared device {rec.device_id}")
+        item = {"kind": rec.kind.value}
+        if rec.stream is not None:
+            item["stream"] = rec.stream
+        item["start"], item["end"] = rec.interval.start, rec.interval.end
+        by_dev[rec.device_id].append(item)
+    devices = []
+    for d in trace.devices:
+        entry = {"id": d.device_id}
+        if d.owner_rank is not None:
+            entry["owner_rank"] = d.owner_rank
+        entry["records"] = by_dev[d.device_id]
+        devices.append(entry)
+    doc = {"version": FORMAT_VERSION, "time_unit": "ns",
+           "hosts": [{"rank": r, "records": by_rank[r]} for r in trace.host_processes], "devices": devices}
+    return (json.dumps(doc, indent=2) + "\n").encode("utf-8")

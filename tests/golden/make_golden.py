@@ -603,12 +603,41 @@ def import_corpus() -> list:
     return out
 
 
+# ---------------------------------------------------------------------------
+# rendering + CLI (report.py:35-138, cli.py:80-100)
+# ---------------------------------------------------------------------------
+def render_corpus() -> list:
+    from heteff import RenderOptions, render_json, render_text, write_trace
+
+    out = []
+    traces = [(f"{n}x{k}", heteff.build(heteff.preset(n, k))) for n in ("usecase1", "usecase3", "usecase7b")
+              for k in (1, 1000)]
+    rng = random.Random(0x5EED0A)
+    traces += [(f"rand{i}", random_valid_trace(rng)) for i in range(12)]
+    traces.append(("late", Trace(host_processes=(0,), devices=(DeviceDecl(0, 0),),
+                                 host_records=(HostRecord(0, HostState.OFFLOAD, Interval(0, 100)),),
+                                 device_records=(DeviceRecord(0, DeviceActivityKind.KERNEL, Interval(90, 120)),
+                                                 DeviceRecord(0, DeviceActivityKind.MEMORY, Interval(95, 95))))))
+    for tag, t in traces:
+        r = compute_report(t)
+        renders = {}
+        for prec in (0, 2, 6):
+            for raw in (False, True):
+                for asc in (False, True):
+                    o = RenderOptions("text", prec, raw, asc)
+                    renders[f"text-{prec}-{int(raw)}-{int(asc)}"] = render_text(r, o)
+            renders[f"json-{prec}"] = render_json(r, RenderOptions("json", prec, False, False)).decode()
+        renders["json-raw"] = render_json(r, RenderOptions("json", 2, True, False)).decode()
+        out.append({"tag": tag, "doc": write_trace(t).decode(), "renders": renders})
+    return out
+
+
 def main() -> None:
     only = sys.argv[sys.argv.index("--only") + 1].split(",") if "--only" in sys.argv else None
     jobs = {"presets": presets, "acceptance": acceptance_corpora, "invalid": invalid_corpus,
             "summarize_device": summarize_device_corpus, "metrics": metrics_corpus,
             "config_shards": config_shards, "regions": regions_corpus, "intervals": intervals_corpus,
-            "trace_docs": trace_docs_corpus, "imports": import_corpus}
+            "trace_docs": trace_docs_corpus, "imports": import_corpus, "renders": render_corpus}
     for name, fn in jobs.items():
         if only is None or name in only:
             write(name, fn())
