@@ -205,7 +205,7 @@ def run_engine(args, world, rank, local):
         del perm
     region_ms = []
     # our kernels per step (regions.cu / sort.cu launch sequences)
-    launches_per_step = 1 if world == 1 else 3
+    launches_per_step = 1 if world == 1 else 3   # analysis + two metric-tree kernels (+ NCCL all-gather)
     if windows is not None:
         passes = (len(windows) + 15) // 16
         launches_per_step = 1 + 14 + passes * (4 + (1 if dt.n == 0 else 0))
@@ -225,7 +225,7 @@ def run_engine(args, world, rank, local):
             return None
         if dist:
             f = analyze_device(dt, N.MODE_REPORT, stream=stream.cuda_stream, device=local)
-            return combine_shards(f, dt, dist, local, stream.cuda_stream)
+            return combine_shards(f, dt, dist, local, stream.cuda_stream, per, per * cfg.gpus_per_rank)
         return plan.run()
 
     for _ in range(max(args.warmup, 3)):
@@ -264,7 +264,7 @@ def run_engine(args, world, rank, local):
     for _ in range(e2e_steps):
         fe = analyze_host_columns(pinned, stream=stream.cuda_stream, device=local, sort_if_needed=args.shuffle)
         if dist:
-            fe = combine_shards(fe, dt, dist, local, stream.cuda_stream)
+            fe = combine_shards(fe, dt, dist, local, stream.cuda_stream, per, per * cfg.gpus_per_rank)
     sync()
     e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
     if dist:

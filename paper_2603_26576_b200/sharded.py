@@ -4,8 +4,9 @@ Per-rank host summaries and per-device summaries are independent
 (summarize.py:74-86, :119-132); the only global coupling is the elapsed time
 E = max span_end over ALL ranks (summarize.py:88-89).  Each GPU therefore
 runs the single-launch analysis on its shard with its LOCAL E (speculative),
-then one small all-gather exchanges ``(E_local, max device end)`` plus the
-summaries:
+then ONE all-gather of a fixed-size buffer exchanges ``(E_local, max device
+end, status, sizes)`` plus the summaries (buffer sizes follow from the rank
+blocks, so no size exchange is needed):
 
 * devices whose records all end by E_local are unclamped, so their union
   lengths are final; only ``idle = E - kernel - memory`` is re-based on the
@@ -41,7 +42,8 @@ def rank_blocks(n_ranks: int, world: int) -> list[tuple[int, int]]:
     return out
 
 
-def combine(f, dist, tensor_device, recompute_device, metrics_fn):
+def combine(f, dist, tensor_device, recompute_device, metrics_fn, n_max: int | None = None,
+            m_max: int | None = None):
     """Merge this shard's findings with every other shard's.
 
     f                 -- this shard's Findings (engine or oracle; needs host_elapsed, dev_max_end,
@@ -50,46 +52,65 @@ def combine(f, dist, tensor_device, recompute_device, metrics_fn):
     tensor_device     -- "cuda:<i>" for nccl, "cpu" for gloo
     recompute_device  -- callable(E_global) -> dev_sum (uint64 [m][4]) for the explicit window
     metrics_fn        -- callable(rows uint64 [k][4], E, host_side) -> tuple of metrics
+    n_max, m_max      -- the largest shard's rank / device counts (known from the rank blocks);
+                         when given, the whole exchange is ONE all-gather of a fixed-size
+                         buffer [meta | host rows | device rows] per rank (a second one only
+                         if some shard clamped device records at its local E)
     Returns a Findings-like object with global E, global summaries and metrics (status of the job).
     """
     import torch
 
     world = dist.get_world_size()
-    meta = torch.tensor([int(f.host_elapsed), int(f.dev_max_end), int(f.status), f.host_sum.shape[0],
-                         f.dev_sum.shape[0]], dtype=torch.int64, device=tensor_device)
-    metas = [torch.zeros_like(meta) for _ in range(world)]
-    dist.all_gather(metas, meta)
-    metas = [m.cpu().numpy().astype(np.uint64) for m in metas]
-    E = int(max(int(m[0]) for m in metas))
-    status = max(int(m[2]) for m in metas)
-    dev_sum = f.dev_sum
-    if int(f.dev_max_end) > int(f.host_elapsed) and E > int(f.host_elapsed):
-        dev_sum = recompute_device(E)            # some record was clamped at the local window
-    else:
-        dev_sum = dev_sum.copy()
-        dev_sum[:, 2] = np.uint64(E) - dev_sum[:, 0] - dev_sum[:, 1]
-    n_max = int(max(int(m[3]) for m in metas))
-    m_max = int(max(int(m[4]) for m in metas))
+    rank = dist.get_rank()
+    n_loc, m_loc = f.host_sum.shape[0], f.dev_sum.shape[0]
+    if n_max is None or m_max is None:   # sizes unknown: one tiny all-gather first
+        sz = torch.tensor([n_loc, m_loc], dtype=torch.int64, device=tensor_device)
+        szs = [torch.zeros_like(sz) for _ in range(world)]
+        dist.all_gather(szs, sz)
+        n_max = int(max(int(x[0]) for x in szs))
+        m_max = int(max(int(x[1]) for x in szs))
+    H, D = 5, 5 + 4 * n_max
+    buf = np.zeros(5 + 4 * (n_max + m_max), dtype=np.uint64)
+    buf[:5] = [int(f.host_elapsed), int(f.dev_max_end), int(f.status), n_loc, m_loc]
+    buf[H:H + 4 * n_loc] = f.host_sum.reshape(-1)
+    buf[D:D + 4 * m_loc] = f.dev_sum.reshape(-1)
 
-    def gather_rows(rows, kmax):
-        pad = np.zeros((kmax, 4), dtype=np.uint64)
-        pad[: rows.shape[0]] = rows
-        t = torch.from_numpy(pad.view(np.int64)).to(tensor_device)
+    def gather(arr):
+        t = torch.from_numpy(arr.view(np.int64)).to(tensor_device)
         parts = [torch.zeros_like(t) for _ in range(world)]
         dist.all_gather(parts, t)
         return [p.cpu().numpy().view(np.uint64) for p in parts]
 
-    hs = gather_rows(f.host_sum, n_max)
-    ds = gather_rows(dev_sum, m_max)
-    host_rows = np.concatenate([h[: int(m[3])] for h, m in zip(hs, metas)])
-    dev_rows = np.concatenate([d[: int(m[4])] for d, m in zip(ds, metas)])
-    hm = metrics_fn(host_rows, E, True) if host_rows.shape[0] and status == 0 else f.host_metrics
-    dm = metrics_fn(dev_rows, E, False) if dev_rows.shape[0] and status == 0 else f.device_metrics
-    return replace(f, status=status, elapsed=E, host_elapsed=E, host_sum=host_rows, dev_sum=dev_rows,
+    parts = gather(buf)
+    E = int(max(int(p[0]) for p in parts))
+    status = max(int(p[2]) for p in parts)
+    n_of = [int(p[3]) for p in parts]
+    m_of = [int(p[4]) for p in parts]
+    host_rows = [p[H:H + 4 * n_of[r]].reshape(-1, 4) for r, p in enumerate(parts)]
+    dev_rows = [p[D:D + 4 * m_of[r]].reshape(-1, 4).copy() for r, p in enumerate(parts)]
+    # shards whose device records ran past their local E were clamped there: re-run them
+    # with the global window (rare); everyone else only re-bases idle on the global E
+    redo = [r for r, p in enumerate(parts) if int(p[1]) > int(p[0]) and E > int(p[0])]
+    if redo:
+        mine = np.zeros(4 * m_max, dtype=np.uint64)
+        if rank in redo:
+            rows = recompute_device(E)
+            mine[: rows.size] = rows.reshape(-1)
+        again = gather(mine)
+        for r in redo:
+            dev_rows[r] = again[r][: 4 * m_of[r]].reshape(-1, 4).copy()
+    for r in range(world):
+        if r not in redo and dev_rows[r].size:
+            dev_rows[r][:, 2] = np.uint64(E) - dev_rows[r][:, 0] - dev_rows[r][:, 1]
+    host_all = np.concatenate(host_rows) if host_rows else np.zeros((0, 4), np.uint64)
+    dev_all = np.concatenate(dev_rows) if dev_rows else np.zeros((0, 4), np.uint64)
+    hm = metrics_fn(host_all, E, True) if host_all.shape[0] and status == 0 else f.host_metrics
+    dm = metrics_fn(dev_all, E, False) if dev_all.shape[0] and status == 0 else f.device_metrics
+    return replace(f, status=status, elapsed=E, host_elapsed=E, host_sum=host_all, dev_sum=dev_all,
                    host_metrics=tuple(hm), device_metrics=tuple(dm))
 
 
-def combine_shards(f, dt, dist, device: int, stream):
+def combine_shards(f, dt, dist, device: int, stream, n_max: int | None = None, m_max: int | None = None):
     """Engine flavour of :func:`combine` (NCCL, GPU re-run and GPU metric kernel)."""
     from . import _native as N
     from .engine import analyze_device, metrics_from_summaries
@@ -101,4 +122,4 @@ def combine_shards(f, dt, dist, device: int, stream):
     def metrics(rows, E, host_side):
         return metrics_from_summaries(rows, E, host_side, device=device)
 
-    return combine(f, dist, f"cuda:{device}", recompute, metrics)
+    return combine(f, dist, f"cuda:{device}", recompute, metrics, n_max, m_max)

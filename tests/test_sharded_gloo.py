@@ -111,7 +111,10 @@ def _worker(rank, world, port, q):
     def recompute(E):
         return O.analyze(hh, dd, n, m, mode=O.MODE_SUMMARIZE_DEVICE, elapsed=E).dev_sum
 
-    out = combine(f, dist, "cpu", recompute, _exact_metrics)
+    sizes = [b - a for a, b in rank_blocks(2, world)]
+    out = combine(f, dist, "cpu", recompute, _exact_metrics, max(sizes), max(sizes) * g)
+    out2 = combine(f, dist, "cpu", recompute, _exact_metrics)   # sizes exchanged first
+    assert out2.elapsed == out.elapsed and np.array_equal(out2.dev_sum, out.dev_sum)
     if rank == 0:
         q.put((out.elapsed, out.host_sum.tolist(), out.dev_sum[:, :3].tolist(), out.host_metrics,
                out.device_metrics))
