@@ -222,6 +222,21 @@ def _dense_ids(declared: np.ndarray):
     return ids, pos
 
 
+def _is_sorted(keys) -> bool:
+    """Lexicographic non-decreasing order of the rows of ``keys`` (most significant first)."""
+    if keys[0].size < 2:
+        return True
+    gt = np.zeros(keys[0].size - 1, dtype=bool)    # strictly greater on an earlier key
+    eq = np.ones(keys[0].size - 1, dtype=bool)     # equal on all earlier keys
+    for k in keys:
+        a, b = k[:-1], k[1:]
+        if np.any(eq & (b < a)):
+            return False
+        gt |= eq & (b > a)
+        eq &= b == a
+    return True
+
+
 def read_trace_packed(data, nthreads: int | None = None):
     """Parse straight into a :class:`~.packing.PackedTrace` in canonical order plus the
     device owner table (dense host ids, -1 none) -- no Python record objects.
@@ -245,10 +260,19 @@ def read_trace_packed(data, nthreads: int | None = None):
     # canonical order (model.py:74-80): host (rank, start, end, state value: mpi < offload < useful),
     # device (device, start, end, kind value: kernel < memory, stream or -1)
     state_rank = np.array([2, 1, 0], dtype=np.uint8)[cols["h_kind"]]
-    ho = np.lexsort((state_rank, cols["h_end"], cols["h_start"], h_res))
-    do = np.lexsort((cols["d_stream"], cols["d_kind"], cols["d_end"], cols["d_start"], d_res))
-    host = RecordColumns(cols["h_start"][ho], cols["h_end"][ho], h_res[ho], cols["h_kind"][ho])
-    dev = RecordColumns(cols["d_start"][do], cols["d_end"][do], d_res[do], cols["d_kind"][do])
+    hkeys = (h_res, cols["h_start"], cols["h_end"], state_rank)
+    dkeys = (d_res, cols["d_start"], cols["d_end"], cols["d_kind"], cols["d_stream"])
+    # writer output is already canonical when entries come in id order: check in O(n), sort otherwise
+    ho = None if _is_sorted(hkeys) else np.lexsort(hkeys[::-1])
+    do = None if _is_sorted(dkeys) else np.lexsort(dkeys[::-1])
+
+    def take(a, o):
+        return a if o is None else a[o]
+
+    host = RecordColumns(take(cols["h_start"], ho), take(cols["h_end"], ho), take(h_res, ho),
+                         take(cols["h_kind"], ho))
+    dev = RecordColumns(take(cols["d_start"], do), take(cols["d_end"], do), take(d_res, do),
+                        take(cols["d_kind"], do))
     packed = PackedTrace(host, dev, hr_ids.tolist(), d_ids.tolist(), h_pos, d_pos, nh, nd,
                          int(hr_ids.size), int(d_ids.size))
     # owners: the first declaration of each device id; owner must be a declared rank
