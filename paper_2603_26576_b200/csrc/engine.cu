@@ -871,15 +871,14 @@ __device__ __forceinline__ bool host_fast32(const StageSmem &sm, int b, int nv, 
         rare = rare || ps64 > base;                                     // order
         pe = pe64 <= base ? 0u : (pe64 - base > 0xffffffffull ? 0xffffffffu : (uint32_t)(pe64 - base));
     }
-    const uint32_t *S32 = reinterpret_cast<const uint32_t *>(sm.s);
-    const uint32_t *E32 = reinterpret_cast<const uint32_t *>(sm.e);
     bool out = false;
     uint32_t o = 0, m = 0, l = 0;
 #pragma unroll kUnrollB
     for (int j = 0; j < kItems; ++j) {
         if (j < nv) {
             const int i = b + j;
-            const uint32_t sl = S32[2 * i], sh = S32[2 * i + 1], el = E32[2 * i], eh = E32[2 * i + 1];
+            const u64 s64 = sm.s[i], e64 = sm.e[i];   // conflict-free LDS.64 at the odd record stride
+            const uint32_t sl = (uint32_t)s64, sh = (uint32_t)(s64 >> 32), el = (uint32_t)e64, eh = (uint32_t)(e64 >> 32);
             const uint8_t k = sm.k[i];
             out = out || sh != bh || eh != bh || sl < bl || el < bl;   // outside [base, base + 2^32)
             const uint32_t s = sl - bl, e = el - bl;
@@ -1106,18 +1105,24 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
     const u64 base = sm.s[0];
     const uint32_t bl = (uint32_t)base, bh = (uint32_t)(base >> 32);
     const uint32_t *S32 = reinterpret_cast<const uint32_t *>(sm.s);
-    const uint32_t *E32 = reinterpret_cast<const uint32_t *>(sm.e);
-    // phase A: kernel-only and all-record max of relative ends
+    // phase A: kernel-only and all-record max of relative ends.  Ends are read as
+    // u64 (one conflict-free LDS.64 at the odd record stride, where two 32-bit
+    // halves would be 2-way conflicted) and, with the kinds, kept in registers
+    // for phase B.
     uint32_t vK = 0, vKM = 0;
+    uint32_t er[kItems];
+    uint32_t kmask = 0;                     // bit j: record j is a kernel
     bool out = false;
 #pragma unroll kUnrollA
     for (int j = 0; j < kItems; ++j) {
+        er[j] = 0;
         if (j < nv) {
-            const uint32_t el = E32[2 * (b + j)], eh = E32[2 * (b + j) + 1];
-            const uint32_t e = el - bl;
-            out = out || eh != bh || el < bl;      // end outside [base, base + 2^32): 64-bit path
+            const u64 e64 = sm.e[b + j];
+            const uint32_t e = (uint32_t)e64 - bl;
+            out = out || (uint32_t)(e64 >> 32) != bh || (uint32_t)e64 < bl;   // outside [base, base + 2^32)
+            er[j] = e;
             vKM = max(vKM, e);
-            if (sm.k[b + j] == 0) vK = max(vK, e);
+            if (sm.k[b + j] == 0) { vK = max(vK, e); kmask |= 1u << j; }
         }
     }
     const bool fit_w = __all_sync(0xffffffffu, !out);
@@ -1156,14 +1161,13 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
 #pragma unroll kUnrollB
     for (int j = 0; j < kItems; ++j) {
         if (j < nv) {
-            const uint32_t s0 = S32[2 * (b + j)] - bl, e0 = E32[2 * (b + j)] - bl;
-            const uint8_t kk = sm.k[b + j];
+            const uint32_t s0 = S32[2 * (b + j)] - bl, e0 = er[j];
             rare = rare || ((j > 0 || b > 0) && s0 < ps) || s0 >= e0 || e0 > Er;
             const uint32_t e = min(e0, Er), s = min(s0, e);
             const uint32_t loKM = max(runKM, s);
             runKM = max(runKM, e);
             cKM += runKM - loKM;
-            if (kk == 0) {
+            if ((kmask >> j) & 1u) {
                 const uint32_t loK = max(runK, s);
                 runK = max(runK, e);
                 cK += runK - loK;
