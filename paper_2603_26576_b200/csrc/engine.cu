@@ -69,14 +69,14 @@ __device__ unsigned long long hb_prof_buf[1024 * kProfSlots];
 struct Phases {
 #ifdef HB_PROF
     long long a = 0, bar = 0, b = 0, emit = 0, t = 0;
-    long long hb = 0, hemit = 0, hn = 0, dn = 0;
+    long long hb = 0, hemit = 0, hn = 0, dn = 0, hn2 = 0;
     __device__ __forceinline__ void mark() { t = clock64(); }
     __device__ __forceinline__ void add(long long &acc) { const long long n = clock64(); acc += n - t; t = n; }
 #else
     __device__ __forceinline__ void mark() {}
     template <typename X>
     __device__ __forceinline__ void add(X &) {}
-    int a, bar, b, emit, hb, hemit, hn, dn;
+    int a, bar, b, emit, hb, hemit, hn, dn, hn2;
 #endif
 };
 
@@ -1098,6 +1098,7 @@ __device__ __forceinline__ u64 device_E(const Params &p, int tid, int lane, u64 
 __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
                                            u64 &E_cache, bool &E_known, bool &signalled, int &kq, Phases &ph)
 {
+    ph.mark();
     const int warp = tid >> 5, lane = tid & 31;
     const int b = tid * kItems;
     const int nv = max(0, min(kItems, tc.cnt - b));
@@ -1130,6 +1131,7 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
     if (lane == 31) { c->f_k[tc.st][warp] = vK; c->f_km[tc.st][warp] = vKM; c->f_fit[tc.st][warp] = fit_w; }
     ph.add(ph.a);
     bar_compute();
+    ph.add(ph.hn2);
     const u64 E = device_E(p, tid, lane, E_cache, E_known, signalled);
     // tile-wide: all warps in the window?  cross-warp exclusive prefix
     uint32_t wK = 0, wKM = 0;
@@ -1144,12 +1146,13 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
     if (lane == 0) { xK = 0; xKM = 0; }
     if (warp > 0) { xK = max(xK, xwK); xKM = max(xKM, xwKM); }
     const bool head = c->has_prev[tc.st] && sm.r[0] == c->prev_res[tc.st];
+    ph.add(ph.bar);
     if (tid == 0) {
         // tile aggregate (a segment starts here iff the tile does not continue one)
         publish<2>(!head ? p.d_slotP + 4 * tc.lt : p.d_slotA + 4 * tc.lt, p.epoch, base + tK, base + tKM);
         if (head) post_info(c, kq, tc.lt, tc.cnt, true, false, base + tK, base + tKM);
     }
-    ph.add(ph.bar);
+    ph.add(ph.hb);
     // phase B: the union pass in 32 bits, carry 0 (the epilogue warp fixes the head)
     const uint32_t Er = E <= base ? 0u : (E - base > 0xffffffffull ? 0xffffffffu : (uint32_t)(E - base));
     const int32_t r0 = sm.r[0];
@@ -1538,7 +1541,7 @@ __global__ void __launch_bounds__(kThreads, 1) analyze_kernel(const __grid_const
             unsigned long long *o = hb_prof_buf + blockIdx.x * kProfSlots;
             o[0] = ca; o[1] = cb; o[2] = cn;
             o[3] = phs.a; o[4] = phs.bar; o[5] = phs.b; o[6] = phs.emit;
-            o[16] = phs.hb; o[17] = phs.hemit; o[18] = phs.hn; o[19] = phs.dn;
+            o[16] = phs.hb; o[17] = phs.hemit; o[18] = phs.hn; o[19] = phs.dn; o[20] = phs.hn2;
         }
 #endif
     }

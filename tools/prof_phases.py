@@ -21,8 +21,8 @@ k = N.load().heteff_prof_read(buf.ctypes.data, buf.size)
 grid = N.load()  # noqa
 P = buf[: k].reshape(-1, 32)
 P = P[P[:, 2] > 0]
-names = {0: ("c.wait_full", 2), 1: ("c.compute", 2), 16: ("host.loop", 18), 17: ("host.emit+max", 18),
-         3: ("dev.phaseA", 19), 4: ("dev.bar+view", 19), 5: ("dev.phaseB", 19), 6: ("dev.emit", 19),
+names = {0: ("c.wait_full", 2), 1: ("c.compute", 2), 16: ("host.loop+devpub", 18), 17: ("host.emit+max", 18),
+         3: ("dev.phaseA", 19), 20: ("dev.barrier", 19), 4: ("dev.E+view", 19), 5: ("dev.phaseB", 19), 6: ("dev.emit", 19),
          8: ("tma.wait_empty", 12), 9: ("tma.produce", 12), 10: ("epi.work", 19), 11: ("epi.wait_info", 19)}
 print(f"{cfg.name}: kernel {f.kernel_ms:.3f} ms, CTAs {P.shape[0]}, tiles/CTA {P[:, 2].mean():.1f}")
 print(f"  host tiles/CTA {P[:, 18].mean():.1f}, device tiles/CTA {P[:, 19].mean():.1f}")
