@@ -315,13 +315,22 @@ static int sort_side(heteff_ctx *ctx, const heteff_records &in, heteff_columns &
 static int run_analysis(heteff_ctx *ctx, const heteff_trace *t, const heteff_options *opt, heteff_result *result,
                         const heteff_outputs *out, cudaStream_t s)
 {
-    int rc = run_once(ctx, t, opt, result, out, s);
-    const int order = HETEFF_CONTRACT_HOST_ORDER | HETEFF_CONTRACT_DEV_ORDER;
-    if (rc != HETEFF_CONTRACT || !(opt->flags & HETEFF_FLAG_SORT_IF_NEEDED) || !(result->contract_flags & order))
-        return rc;
-    // K3: sort the offending side(s) into ctx-owned columns and analyze again
-    const bool sh = result->contract_flags & HETEFF_CONTRACT_HOST_ORDER;
-    const bool sd = result->contract_flags & HETEFF_CONTRACT_DEV_ORDER;
+    if (!(opt->flags & HETEFF_FLAG_SORT_IF_NEEDED)) return run_once(ctx, t, opt, result, out, s);
+    // canonical-order check of both sides (12 B/record), then sort only what needs it
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    CK(ensure(ctx->aux, 256, false), "alloc order flags");
+    unsigned int *bad = static_cast<unsigned int *>(ctx->aux.p);
+    CK(cudaMemsetAsync(bad, 0, 8, s), "memset");
+    CK(hb::launch_order_check(t->host.res, (const u64 *)t->host.start, t->host.count, bad, s), "order check");
+    CK(hb::launch_order_check(t->dev.res, (const u64 *)t->dev.start, t->dev.count, bad + 1, s), "order check");
+    unsigned int flags_h[2] = {0, 0};
+    CK(cudaMemcpyAsync(flags_h, bad, 8, cudaMemcpyDeviceToHost, s), "d2h");
+    CK(cudaStreamSynchronize(s), "order check");
+    if (!flags_h[0] && !flags_h[1]) return run_once(ctx, t, opt, result, out, s);
+    int rc;
+    // K3: sort the offending side(s) into ctx-owned columns and analyze
+    const bool sh = flags_h[0] != 0;
+    const bool sd = flags_h[1] != 0;
     auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
     const int64_t hn = sh ? t->host.count : 0, dn = sd ? t->dev.count : 0;
     const size_t bytes = up((size_t)hn * 29) + up((size_t)hn * 8) + up((size_t)dn * 29) + up((size_t)dn * 8) + 2048;

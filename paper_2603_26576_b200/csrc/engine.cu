@@ -145,6 +145,9 @@ __device__ __noinline__ void push(const Params &p, int cls, int64_t gi)
 
 __device__ __noinline__ void contract(const Params &p, unsigned flag, int64_t gi)
 {
+    // unsorted input flags (nearly) every thread: skip the atomics once an earlier index holds
+    if ((*(volatile unsigned *)&p.g->contract_flags & flag) && *(volatile long long *)&p.g->contract_index <= gi)
+        return;
     atomicOr(&p.g->contract_flags, flag);
     atomicMin(&p.g->contract_index, (long long)gi);
 }

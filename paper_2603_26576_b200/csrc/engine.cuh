@@ -185,5 +185,6 @@ cudaError_t sort_records(const u64 *S, const u64 *E, const int32_t *R, const uin
                          int32_t *orr, uint8_t *ok, int64_t *perm, void *ws, size_t ws_bytes, cudaStream_t s,
                          SortStats *stats);
 cudaError_t launch_remap(int64_t *list, int64_t k, const int64_t *perm, cudaStream_t s);
+cudaError_t launch_order_check(const int32_t *R, const u64 *S, int64_t n, unsigned int *bad, cudaStream_t s);
 
 }  // namespace hb

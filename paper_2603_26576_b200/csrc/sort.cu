@@ -32,9 +32,15 @@
 namespace hb {
 namespace rsort {
 
-constexpr int kT = 512;                 // threads per CTA (2 CTAs / SM)
+#ifndef HB_SORT_T
+#define HB_SORT_T 512
+#endif
+#ifndef HB_SORT_I
+#define HB_SORT_I 11
+#endif
+constexpr int kT = HB_SORT_T;           // threads per CTA (512: 2 CTAs / SM)
 constexpr int kW = kT / 32;
-constexpr int kI = 15;                  // keys per thread
+constexpr int kI = HB_SORT_I;           // keys per thread
 constexpr int kTileKeys = kT * kI;      // 7680 keys per tile
 constexpr int kBins = 256;              // <= 8-bit digits
 
@@ -294,7 +300,7 @@ __device__ __forceinline__ uint32_t peers_of(uint32_t d, int dbits, uint32_t val
 
 // one digit pass: stable rank of the tile's keys, reorder in shared memory,
 // coalesced digit runs to their scanned global positions
-__global__ void __launch_bounds__(kT, 2) downsweep(const u64 *__restrict__ kin, const uint32_t *__restrict__ vin,
+__global__ void __launch_bounds__(kT, (kT <= 512 ? 2 : 1)) downsweep(const u64 *__restrict__ kin, const uint32_t *__restrict__ vin,
                                                    u64 *__restrict__ kout, uint32_t *__restrict__ vout, int64_t n,
                                                    int shift, int dbits, const uint32_t *__restrict__ offs,
                                                    int64_t tiles)
@@ -421,7 +427,28 @@ __global__ void remap_kernel(int64_t *list, int64_t k, const int64_t *__restrict
         list[i] = perm[list[i]];
 }
 
+// canonical-order check of one record set: (res, start) non-decreasing
+__global__ void __launch_bounds__(512) order_check(const int32_t *__restrict__ R, const u64 *__restrict__ S, int64_t n,
+                                                   unsigned int *bad)
+{
+    bool b = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x + 1; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t r = __ldcs(R + i), rp = __ldg(R + i - 1);
+        b = b || r < rp || (r == rp && __ldcs(S + i) < __ldg(S + i - 1));
+    }
+    if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+}
+
 }  // namespace rsort
+
+cudaError_t launch_order_check(const int32_t *R, const u64 *S, int64_t n, unsigned int *bad, cudaStream_t s)
+{
+    if (n < 2) return cudaSuccess;
+    int64_t g = (n + 511) / 512;
+    if (g > 148 * 8) g = 148 * 8;
+    rsort::order_check<<<(unsigned)g, 512, 0, s>>>(R, S, n, bad);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_remap(int64_t *list, int64_t k, const int64_t *perm, cudaStream_t s)
 {

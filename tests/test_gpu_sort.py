@@ -24,7 +24,7 @@ from paper_2603_26576_b200.engine import (DeviceTrace, analyze_device, analyze_h
                                           analyze_packed, sort_records)
 from paper_2603_26576_b200.packing import PackedTrace, RecordColumns  # noqa: E402
 
-TILE = 512 * 15
+TILE = 512 * 11
 
 
 def _cuda(a: np.ndarray) -> torch.Tensor:
