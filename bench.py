@@ -172,7 +172,9 @@ def run_engine(args, world, rank, local):
 
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    # HETEFF_FORCE_DIST=1 runs the multi-GPU protocol even at world size 1 (exercises the
+    # NCCL all-reduce / all-gather and the merge kernel on a single GPU)
+    if world > 1 or os.environ.get("HETEFF_FORCE_DIST") == "1":
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = _global_config(args.config, world)
@@ -205,7 +207,7 @@ def run_engine(args, world, rank, local):
         del perm
     region_ms = []
     # our kernels per step (regions.cu / sort.cu launch sequences)
-    launches_per_step = 1 if world == 1 else 3   # analysis + two metric-tree kernels (+ NCCL all-gather)
+    launches_per_step = 1 if world == 1 else 3   # host pass + device pass + merge (+ NCCL all-reduce / all-gather)
     if windows is not None:
         passes = (len(windows) + 15) // 16
         launches_per_step = 1 + 14 + passes * (4 + (1 if dt.n == 0 else 0))
@@ -216,6 +218,10 @@ def run_engine(args, world, rank, local):
         del probe
 
     plan = AnalysisPlan(dt, N.MODE_REPORT, stream=stream.cuda_stream, device=local, sort_if_needed=args.shuffle)
+    merge = None
+    if dist:   # device-resident protocol: host pass, all-reduce E, device pass, all-gather, merge kernel
+        from paper_2603_26576_b200.sharded import DeviceMerge
+        merge = DeviceMerge(dt, dist, local, stream.cuda_stream, [per] * world, [per * cfg.gpus_per_rank] * world)
 
     def step():
         if windows is not None:   # compute_report of the trace + every region tree + overlap, one call
@@ -223,9 +229,8 @@ def run_engine(args, world, rank, local):
             assert run.status == N.OK, run.status
             region_ms.append(run.kernel_ms)
             return None
-        if dist:
-            f = analyze_device(dt, N.MODE_REPORT, stream=stream.cuda_stream, device=local)
-            return combine_shards(f, dt, dist, local, stream.cuda_stream, per, per * cfg.gpus_per_rank)
+        if merge is not None:
+            return merge.step()
         return plan.run()
 
     for _ in range(max(args.warmup, 3)):
@@ -240,7 +245,7 @@ def run_engine(args, world, rank, local):
         ev0.record(stream)
         for _ in range(args.steps):
             f = step()
-            if f is not None:
+            if f is not None and merge is None:
                 kernel_ms.append(f.kernel_ms)
         ev1.record(stream)
         sync()
@@ -257,8 +262,8 @@ def run_engine(args, world, rank, local):
                          dt.n, dt.m)
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     f = analyze_host_columns(pinned, stream=stream.cuda_stream, device=local, sort_if_needed=args.shuffle)
-    if not kernel_ms:   # region steps: the analysis kernel's own time from the host-column run
-        kernel_ms.append(f.kernel_ms)
+    if not kernel_ms:   # region / multi-GPU steps: the one-launch analysis kernel's time on this shard
+        kernel_ms.append(analyze_device(dt, N.MODE_REPORT, stream=stream.cuda_stream, device=local).kernel_ms)
     sync()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):

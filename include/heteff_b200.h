@@ -114,7 +114,10 @@ enum {
     /* records not in canonical order are sorted on the GPU (K3, heteff_sort_records)
        and the analysis re-run, instead of returning HETEFF_CONTRACT; list indices
        still refer to the caller's input positions */
-    HETEFF_FLAG_SORT_IF_NEEDED = 1
+    HETEFF_FLAG_SORT_IF_NEEDED = 1,
+    /* SUMMARIZE_DEVICE: heteff_options.elapsed holds the DEVICE address of the u64
+       window (read by the kernel; e.g. an all-reduced E that never visits the host) */
+    HETEFF_FLAG_ELAPSED_DEVICE_PTR = 2
 };
 
 typedef struct {
@@ -316,6 +319,27 @@ typedef struct {
 /* trace columns in device memory */
 int heteff_analyze_regions(heteff_ctx *ctx, const heteff_trace *trace, const heteff_regions *regions,
                            heteff_region_outputs *out, void *stream);
+
+/* ---- multi-GPU (one process per GPU, rank-sharded trace) ----
+ * Per step every rank runs, all stream-ordered and without host syncs:
+ *   1. heteff_analyze_into(SUMMARIZE_HOST) on its host records -> block host header
+ *      (local E = host_elapsed at byte 16) + host rows;
+ *   2. all-reduce MAX of the local E over NVLink (8 bytes);
+ *   3. heteff_analyze_into(SUMMARIZE_DEVICE, HETEFF_FLAG_ELAPSED_DEVICE_PTR -> the
+ *      all-reduced E) on its device records -> block device header + device rows,
+ *      clamped at the GLOBAL E (summarize.py:88-89, :113);
+ *   4. all-gather of the fixed-size blocks; 5. heteff_merge_shards: one kernel,
+ *      concatenated summaries + both metric trees, one small D2H.
+ * Block: [host header 256 B | device header 256 B | host rows [n_max][4] |
+ * device rows [m_max][4]], block_bytes >= 512 + 32 (n_max + m_max).  Every record
+ * is read once, as in the single-GPU launch.  heteff_merge_shards returns
+ * HETEFF_PARSE_FALLBACK ("defer") when a shard's status is not OK (the caller then
+ * takes the synchronous path for the exact error). */
+int heteff_analyze_into(heteff_ctx *ctx, const heteff_trace *trace, const heteff_options *opt, void *dev_block,
+                        size_t block_bytes, int32_t n_max, int32_t m_max, void *stream);
+int heteff_merge_shards(heteff_ctx *ctx, const void *gathered, int32_t world, size_t block_bytes, int32_t n_max,
+                        int32_t m_max, const int32_t *n_of, const int32_t *m_of, const uint64_t *elapsed_dev,
+                        heteff_result *result, const heteff_outputs *out, void *stream);
 
 /* overlap errors: cover index of each listed record (model.py:208-215), host memory */
 int heteff_overlap_covers(heteff_ctx *ctx, const heteff_trace *trace, int host_columns_on_host,

@@ -88,6 +88,7 @@ class RegionOutputs(C.Structure):
 
 
 FLAG_SORT_IF_NEEDED = 1
+FLAG_ELAPSED_DEVICE_PTR = 2
 CONTRACT_HOST_ORDER, CONTRACT_DEV_ORDER, CONTRACT_HOST_KIND, CONTRACT_DEV_KIND = 1, 2, 4, 8
 
 
@@ -110,6 +111,7 @@ EXPORTED = (
     "heteff_flatten", "heteff_subtract", "heteff_intersect", "heteff_total_duration",
     "heteff_parse_trace", "heteff_parsed_info", "heteff_parsed_free",
     "heteff_import_events", "heteff_imported_info", "heteff_imported_free",
+    "heteff_analyze_into", "heteff_merge_shards",
 )
 
 _lib = None
@@ -169,6 +171,12 @@ def load() -> C.CDLL:
     lib.heteff_imported_info.argtypes = [C.c_void_p, C.c_void_p]
     lib.heteff_imported_free.restype = None
     lib.heteff_imported_free.argtypes = [C.c_void_p]
+    lib.heteff_analyze_into.restype = C.c_int
+    lib.heteff_analyze_into.argtypes = [_p, C.POINTER(TraceABI), C.POINTER(Options), _p, C.c_size_t, C.c_int32,
+                                        C.c_int32, _p]
+    lib.heteff_merge_shards.restype = C.c_int
+    lib.heteff_merge_shards.argtypes = [_p, _p, C.c_int32, C.c_size_t, C.c_int32, C.c_int32, _p, _p, _p,
+                                        C.POINTER(Result), C.POINTER(Outputs), _p]
     lib.heteff_generate.restype = C.c_int
     lib.heteff_generate.argtypes = [_p, C.POINTER(GenSide), _p, _p, _p, _p, _p]
     _lib = lib

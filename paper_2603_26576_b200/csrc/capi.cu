@@ -136,8 +136,14 @@ const char *heteff_last_error(const heteff_ctx *ctx) { return ctx ? ctx->err.c_s
 
 static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+struct IntoBlock {   // heteff_analyze_into: results go to a caller-owned device block, no sync
+    void *p;
+    int32_t n_max, m_max;
+};
+
 static int run_once(heteff_ctx *ctx, const heteff_trace *t, const heteff_options *opt, heteff_result *result,
-                    const heteff_outputs *out, cudaStream_t s, const int64_t *const perms[2] = nullptr)
+                    const heteff_outputs *out, cudaStream_t s, const int64_t *const perms[2] = nullptr,
+                    const IntoBlock *into = nullptr)
 {
     if (!ctx || !t || !opt || !result) return fail(ctx, HETEFF_BAD_ARG, "null argument");
     if (t->host.count < 0 || t->dev.count < 0 || t->host_ids < 0 || t->dev_ids < 0 || t->n < 0 || t->m < 0 ||
@@ -227,6 +233,15 @@ static int run_once(heteff_ctx *ctx, const heteff_trace *t, const heteff_options
     p.res = reinterpret_cast<hb::ResultDev *>(blk);
     p.host_out = reinterpret_cast<u64 *>(blk + ob_res);
     p.dev_out = reinterpret_cast<u64 *>(blk + ob_res + ob_h);
+    if (opt->flags & HETEFF_FLAG_ELAPSED_DEVICE_PTR) p.elapsed_ptr = reinterpret_cast<const u64 *>(opt->elapsed);
+    if (into) {   // [host header | device header | host rows [n_max] | device rows [m_max]]
+        uint8_t *b = static_cast<uint8_t *>(into->p);
+        p.res = reinterpret_cast<hb::ResultDev *>(b + (opt->mode == HETEFF_MODE_SUMMARIZE_DEVICE ? 256 : 0));
+        p.host_out = reinterpret_cast<u64 *>(b + 512);
+        p.dev_out = reinterpret_cast<u64 *>(b + 512 + (size_t)into->n_max * 32);
+        CK(hb::launch_analyze(p, ctx->grid, s), "launch analyze");
+        return HETEFF_OK;
+    }
     const bool want_sums = out && (out->host_summaries || out->device_summaries);
     const size_t ob_copy = want_sums ? ob_total : sizeof(hb::ResultDev);
 
@@ -571,6 +586,71 @@ int heteff_total_duration(heteff_ctx *ctx, const uint64_t *start, const uint64_t
     CK(cudaStreamSynchronize(s), "total");
     ctx->err.clear();
     return HETEFF_OK;
+}
+
+int heteff_analyze_into(heteff_ctx *ctx, const heteff_trace *trace, const heteff_options *opt, void *dev_block,
+                        size_t block_bytes, int32_t n_max, int32_t m_max, void *stream)
+{
+    if (!ctx || !trace || !opt || !dev_block || n_max < 0 || m_max < 0) return fail(ctx, HETEFF_BAD_ARG, "bad argument");
+    if (trace->n > n_max || trace->m > m_max || block_bytes < 512 + 32 * ((size_t)n_max + (size_t)m_max))
+        return fail(ctx, HETEFF_BAD_ARG, "result block too small");
+    if (opt->flags & HETEFF_FLAG_SORT_IF_NEEDED) return fail(ctx, HETEFF_BAD_ARG, "sort_if_needed needs the sync path");
+    heteff_result r{};
+    IntoBlock into{dev_block, n_max, m_max};
+    return run_once(ctx, trace, opt, &r, nullptr, static_cast<cudaStream_t>(stream), nullptr, &into);
+}
+
+int heteff_merge_shards(heteff_ctx *ctx, const void *gathered, int32_t world, size_t block_bytes, int32_t n_max,
+                        int32_t m_max, const int32_t *n_of, const int32_t *m_of, const uint64_t *elapsed_dev,
+                        heteff_result *result, const heteff_outputs *out, void *stream)
+{
+    if (!ctx || !gathered || world < 1 || !n_of || !m_of || !elapsed_dev || !result)
+        return fail(ctx, HETEFF_BAD_ARG, "bad argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    int64_t ntot = 0, mtot = 0;
+    for (int r = 0; r < world; ++r) { ntot += n_of[r]; mtot += m_of[r]; }
+    const size_t need = 256 + 32 * (size_t)(ntot + mtot) + 8 * (size_t)world;
+    CK(ensure(ctx->aux, need + 256, false), "alloc merge output");
+    uint8_t *dout = static_cast<uint8_t *>(ctx->aux.p);
+    int32_t *sizes_d = reinterpret_cast<int32_t *>(dout + ((256 + 32 * (size_t)(ntot + mtot) + 255) & ~(size_t)255));
+    if (ctx->out_pin_bytes < need) {
+        if (ctx->out_pin) cudaFreeHost(ctx->out_pin);
+        ctx->out_pin = nullptr;
+        ctx->out_pin_bytes = 0;
+        CK(cudaMallocHost(&ctx->out_pin, need + need / 4), "alloc pinned results");
+        ctx->out_pin_bytes = need + need / 4;
+    }
+    int32_t *sizes_h = static_cast<int32_t *>(ctx->out_pin);   // staged through pinned memory
+    for (int r = 0; r < world; ++r) { sizes_h[r] = n_of[r]; sizes_h[world + r] = m_of[r]; }
+    CK(cudaMemcpyAsync(sizes_d, sizes_h, 8 * (size_t)world, cudaMemcpyHostToDevice, s), "h2d sizes");
+    CK(cudaEventRecord(ctx->ev0, s), "event");
+    CK(hb::launch_merge(gathered, world, block_bytes, n_max, m_max, sizes_d, sizes_d + world, dout,
+                        (const u64 *)elapsed_dev, s),
+       "launch merge");
+    CK(cudaEventRecord(ctx->ev1, s), "event");
+    const bool sums = out && (out->host_summaries || out->device_summaries);
+    const size_t copy = sums ? 256 + 32 * (size_t)(ntot + mtot) : sizeof(hb::ResultDev);
+    CK(cudaMemcpyAsync(ctx->out_pin, dout, copy, cudaMemcpyDeviceToHost, s), "d2h merged");
+    CK(cudaStreamSynchronize(s), "merge");
+    const hb::ResultDev &r = *static_cast<const hb::ResultDev *>(ctx->out_pin);
+    memset(result, 0, sizeof(*result));
+    result->status = r.status;
+    result->elapsed = r.elapsed;
+    result->host_elapsed = r.host_elapsed;
+    for (int i = 0; i < 5; ++i) result->host_metrics[i] = r.host_metrics[i];
+    for (int i = 0; i < 4; ++i) result->device_metrics[i] = r.device_metrics[i];
+    result->host_mask = r.host_mask;
+    result->device_mask = r.device_mask;
+    result->host_present = ntot >= 1;
+    result->device_present = mtot >= 1;
+    if (r.status == 0 && sums) {
+        const uint8_t *b = static_cast<const uint8_t *>(ctx->out_pin) + 256;
+        if (out->host_summaries) memcpy(out->host_summaries, b, 32 * (size_t)ntot);
+        if (out->device_summaries) memcpy(out->device_summaries, b + 32 * (size_t)ntot, 32 * (size_t)mtot);
+    }
+    ctx->err.clear();
+    return r.status == -2 ? HETEFF_PARSE_FALLBACK : HETEFF_OK;
 }
 
 int heteff_sort_records(heteff_ctx *ctx, const heteff_records *in, const heteff_columns *out, int64_t *perm,

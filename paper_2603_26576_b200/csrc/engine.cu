@@ -215,7 +215,7 @@ __device__ __forceinline__ void host_phase_done(const Params &p)
 
 __device__ u64 device_window(const Params &p)
 {
-    if (p.mode == kSummarizeDevice) return p.elapsed_arg;
+    if (p.mode == kSummarizeDevice) return p.elapsed_ptr ? ld_relaxed(p.elapsed_ptr) : p.elapsed_arg;
     if ((p.mode == kReport || p.mode == kValidate) && p.n >= 1) {
         while (ld_acquire64(&p.g->host_done) < (u64)gridDim.x) __nanosleep(64);
         return umax(ld_relaxed(&p.g->host_max_end), p.host_elapsed_floor);
@@ -1337,7 +1337,7 @@ __device__ void finalize(const Params &p, u128 *scratch, int tid)
     const u64 host_elapsed = umax(ld_relaxed(&g->host_max_end), p.host_elapsed_floor);
     if (tid == 0) {
         u64 E;
-        if (p.mode == kSummarizeDevice) E = p.elapsed_arg;
+        if (p.mode == kSummarizeDevice) E = p.elapsed_ptr ? ld_relaxed(p.elapsed_ptr) : p.elapsed_arg;
         else E = p.n >= 1 ? host_elapsed : dev_max_end;
         s_E = E;
         u64 cnt[8];
@@ -1758,6 +1758,88 @@ int analyze_grid(int device)
 cudaError_t launch_analyze(const Params &p, int grid, cudaStream_t s)
 {
     analyze_kernel<<<grid, kThreads, analyze_smem_bytes(), s>>>(p);
+    return cudaGetLastError();
+}
+
+// =========================================================================
+// multi-GPU merge of gathered per-rank result blocks (one CTA).  Every rank
+// ran two launches into its block [host header 256 B | device header 256 B |
+// host rows [n_max][4] | device rows [m_max][4]]: its host records
+// (SUMMARIZE_HOST) and, after the all-reduce of E, its device records
+// clamped at the GLOBAL E (SUMMARIZE_DEVICE, window read from device memory).
+// The merge concatenates the rows in rank order and evaluates both metric
+// trees; a non-OK shard makes it defer (status -2) to the host path.
+// =========================================================================
+__global__ void __launch_bounds__(1024) merge_kernel(const uint8_t *blocks, int32_t world, size_t block_bytes,
+                                                     int32_t n_max, int32_t m_max, const int32_t *n_of,
+                                                     const int32_t *m_of, uint8_t *out, const u64 *E_global)
+{
+    __shared__ u128 scratch[33];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    ResultDev *res = reinterpret_cast<ResultDev *>(out);
+    const u64 E = ld_relaxed(E_global);
+    __shared__ int s_defer;
+    if (tid == 0) {
+        int defer = 0;
+        for (int r = 0; r < world; ++r) {
+            const uint8_t *blk = blocks + (size_t)r * block_bytes;
+            const ResultDev *h = reinterpret_cast<const ResultDev *>(blk);
+            const ResultDev *d = reinterpret_cast<const ResultDev *>(blk + 256);
+            if (h->status != 0 || d->status != 0) defer = 1;
+        }
+        s_defer = defer;
+        res->status = defer ? -2 : (E == 0 ? 2 : 0);
+        res->elapsed = E;
+        res->host_elapsed = E;
+        res->host_mask = res->device_mask = 0;
+    }
+    __syncthreads();
+    if (s_defer) return;
+    int32_t ntot = 0, mtot = 0;
+    for (int r = 0; r < world; ++r) { ntot += n_of[r]; mtot += m_of[r]; }
+    u64 *hout = reinterpret_cast<u64 *>(out + 256);
+    u64 *dout = hout + 4 * (size_t)ntot;
+    u128 su = 0, suw = 0, muw = 0, sk = 0, mk = 0, mkm = 0;
+    int32_t hb = 0, db = 0;
+    for (int r = 0; r < world; ++r) {
+        const u64 *hr = reinterpret_cast<const u64 *>(blocks + (size_t)r * block_bytes + 512);
+        const u64 *dr = hr + 4 * (size_t)n_max;
+        for (int32_t i = tid; i < n_of[r]; i += nt) {
+            const u64 *x = hr + 4 * (size_t)i;
+            u64 *o = hout + 4 * (size_t)(hb + i);
+            o[0] = x[0]; o[1] = x[1]; o[2] = x[2]; o[3] = x[3];
+            const u128 uw = (u128)x[0] + x[1];
+            su += x[0];
+            suw += uw;
+            if (uw > muw) muw = uw;
+        }
+        for (int32_t i = tid; i < m_of[r]; i += nt) {
+            const u64 *x = dr + 4 * (size_t)i;
+            u64 *o = dout + 4 * (size_t)(db + i);
+            o[0] = x[0]; o[1] = x[1]; o[2] = x[2]; o[3] = x[3];
+            sk += x[0];
+            if ((u128)x[0] > mk) mk = x[0];
+            const u128 km = (u128)x[0] + x[1];
+            if (km > mkm) mkm = km;
+        }
+        hb += n_of[r];
+        db += m_of[r];
+    }
+    su = block_reduce128<false>(su, scratch, tid, nt);
+    suw = block_reduce128<false>(suw, scratch, tid, nt);
+    muw = block_reduce128<true>(muw, scratch, tid, nt);
+    sk = block_reduce128<false>(sk, scratch, tid, nt);
+    mk = block_reduce128<true>(mk, scratch, tid, nt);
+    mkm = block_reduce128<true>(mkm, scratch, tid, nt);
+    if (E == 0) return;
+    metric_trees(res, ntot >= 1, mtot >= 1, E, ntot, mtot, su, suw, muw, sk, mk, mkm, tid);
+}
+
+cudaError_t launch_merge(const void *blocks, int32_t world, size_t block_bytes, int32_t n_max, int32_t m_max,
+                         const int32_t *n_of, const int32_t *m_of, void *out, const u64 *E_global, cudaStream_t s)
+{
+    merge_kernel<<<1, 1024, 0, s>>>(static_cast<const uint8_t *>(blocks), world, block_bytes, n_max, m_max, n_of,
+                                    m_of, static_cast<uint8_t *>(out), E_global);
     return cudaGetLastError();
 }
 

@@ -79,6 +79,7 @@ struct Params {
     int32_t mode;
     int32_t use_tma;
     u64 elapsed_arg;
+    const u64 *elapsed_ptr;   // SUMMARIZE_DEVICE: the window read from device memory (multi-GPU: all-reduced E)
     int64_t cap;
     int64_t host_tiles, dev_tiles;
     uint32_t epoch;
@@ -103,6 +104,8 @@ int analyze_grid(int device);
 cudaError_t launch_analyze(const Params &p, int grid, cudaStream_t s);
 cudaError_t launch_metrics(const u64 *summaries, int32_t k, u64 elapsed, int host_side, ResultDev *res,
                            cudaStream_t s);
+cudaError_t launch_merge(const void *blocks, int32_t world, size_t block_bytes, int32_t n_max, int32_t m_max,
+                         const int32_t *n_of, const int32_t *m_of, void *out, const u64 *E_global, cudaStream_t s);
 // error path: exact host-overlap findings (only when ovl_suspect), then finalize
 cudaError_t launch_overlap_pass(const Params &p, u64 *scratch, cudaStream_t s);
 cudaError_t launch_covers(const Params &p, const int64_t *err_idx, int64_t count, int64_t *cover, cudaStream_t s);

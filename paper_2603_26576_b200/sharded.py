@@ -46,8 +46,8 @@ def combine(f, dist, tensor_device, recompute_device, metrics_fn, n_max: int | N
             m_max: int | None = None):
     """Merge this shard's findings with every other shard's.
 
-    f                 -- this shard's Findings (engine or oracle; needs host_elapsed, dev_max_end,
-                         status, host_sum, dev_sum)
+    f                 -- this shard's Findings (engine or oracle; needs host_elapsed, status,
+                         host_sum, dev_sum with the clamp counts in column 3)
     dist              -- torch.distributed (initialised; nccl or gloo)
     tensor_device     -- "cuda:<i>" for nccl, "cpu" for gloo
     recompute_device  -- callable(E_global) -> dev_sum (uint64 [m][4]) for the explicit window
@@ -71,7 +71,10 @@ def combine(f, dist, tensor_device, recompute_device, metrics_fn, n_max: int | N
         m_max = int(max(int(x[1]) for x in szs))
     H, D = 5, 5 + 4 * n_max
     buf = np.zeros(5 + 4 * (n_max + m_max), dtype=np.uint64)
-    buf[:5] = [int(f.host_elapsed), int(f.dev_max_end), int(f.status), n_loc, m_loc]
+    # did any device record end past the local E (clamp counts, column 3)?  Only then a
+    # larger global E changes this shard's device summaries
+    clamped = int(f.dev_sum[:, 3].astype(object).sum()) if f.dev_sum.shape[1] > 3 and m_loc else 0
+    buf[:5] = [int(f.host_elapsed), 1 if clamped else 0, int(f.status), n_loc, m_loc]
     buf[H:H + 4 * n_loc] = f.host_sum.reshape(-1)
     buf[D:D + 4 * m_loc] = f.dev_sum.reshape(-1)
 
@@ -90,7 +93,7 @@ def combine(f, dist, tensor_device, recompute_device, metrics_fn, n_max: int | N
     dev_rows = [p[D:D + 4 * m_of[r]].reshape(-1, 4).copy() for r, p in enumerate(parts)]
     # shards whose device records ran past their local E were clamped there: re-run them
     # with the global window (rare); everyone else only re-bases idle on the global E
-    redo = [r for r, p in enumerate(parts) if int(p[1]) > int(p[0]) and E > int(p[0])]
+    redo = [r for r, p in enumerate(parts) if int(p[1]) and E > int(p[0])]
     if redo:
         mine = np.zeros(4 * m_max, dtype=np.uint64)
         if rank in redo:
@@ -123,3 +126,72 @@ def combine_shards(f, dt, dist, device: int, stream, n_max: int | None = None, m
         return metrics_from_summaries(rows, E, host_side, device=device)
 
     return combine(f, dist, f"cuda:{device}", recompute, metrics, n_max, m_max)
+
+
+class DeviceMerge:
+    """The device-resident multi-GPU step (include/heteff_b200.h, "multi-GPU"): this
+    rank's host records are summarized into a device result block, the local E is
+    all-reduced (MAX, 8 bytes over NVLink), the device records are summarized with the
+    GLOBAL E read from device memory (so no shard ever clamps at a local E and nothing
+    is re-run), ONE all-gather of the fixed-size blocks follows, and one merge kernel
+    evaluates the summaries and both metric trees; a single small D2H brings the report
+    to the host.  Every record is read once per step, as on one GPU.  A non-OK shard
+    (invalid trace, ...) defers to the synchronous host path for the exact error."""
+
+    def __init__(self, dt, dist, device: int, stream, n_of: list[int], m_of: list[int]):
+        import ctypes as C
+
+        import torch
+
+        from . import _native as N
+        from .engine import _dptr
+
+        self.N, self.C, self.dist, self.dt, self.device, self.stream = N, C, dist, dt, device, stream
+        self.lib, self.ctx = N.load(), N.context(device)
+        self.world = len(n_of)
+        self.n_max, self.m_max = max(n_of), max(m_of)
+        self.n_of = (C.c_int32 * self.world)(*n_of)
+        self.m_of = (C.c_int32 * self.world)(*m_of)
+        self.bytes = 512 + 32 * (self.n_max + self.m_max)
+        dev = torch.device("cuda", device)
+        self.block = torch.zeros(self.bytes // 8, dtype=torch.int64, device=dev)
+        self.gathered = torch.zeros(self.world * self.bytes // 8, dtype=torch.int64, device=dev)
+        self.e = torch.zeros(1, dtype=torch.int64, device=dev)
+        hrec = N.Records(_dptr(dt.h_start), _dptr(dt.h_end), _dptr(dt.h_res), _dptr(dt.h_kind), dt.host_count)
+        drec = N.Records(_dptr(dt.d_start), _dptr(dt.d_end), _dptr(dt.d_res), _dptr(dt.d_kind), dt.dev_count)
+        none = N.Records(None, None, None, None, 0)
+        self.t_host = N.TraceABI(hrec, none, dt.n, 0, None, None, dt.n, 0, dt.host_elapsed_floor)
+        self.t_dev = N.TraceABI(none, drec, 0, dt.m, None, None, 0, dt.m, 0)
+        self.o_host = N.Options(N.MODE_SUMMARIZE_HOST, 0, 0, 0)
+        self.o_dev = N.Options(N.MODE_SUMMARIZE_DEVICE, N.FLAG_ELAPSED_DEVICE_PTR, self.e.data_ptr(), 0)
+        self.res = N.Result()
+        ntot, mtot = sum(n_of), sum(m_of)
+        self.host_sum = np.zeros((max(ntot, 1), 4), dtype=np.uint64)
+        self.dev_sum = np.zeros((max(mtot, 1), 4), dtype=np.uint64)
+        self.out = N.Outputs(self.host_sum.ctypes.data, self.dev_sum.ctypes.data, (C.c_void_p * N.NUM_LISTS)())
+        self.ntot, self.mtot = ntot, mtot
+
+    def _into(self, t, opt):
+        rc = self.lib.heteff_analyze_into(self.ctx, self.C.byref(t), self.C.byref(opt), self.block.data_ptr(),
+                                          self.bytes, self.n_max, self.m_max, self.stream)
+        if rc != self.N.OK:
+            raise self.N.NativeError(f"heteff_analyze_into failed ({rc}): {self.N.last_error(self.ctx)}")
+
+    def step(self):
+        from .engine import _findings, analyze_device
+
+        N, C = self.N, self.C
+        self._into(self.t_host, self.o_host)                       # host records -> local E (header byte 16)
+        self.e.copy_(self.block[2:3])
+        self.dist.all_reduce(self.e, op=self.dist.ReduceOp.MAX)    # global E, never on the host
+        self._into(self.t_dev, self.o_dev)                         # device records clamped at the global E
+        self.dist.all_gather_into_tensor(self.gathered, self.block)
+        rc = self.lib.heteff_merge_shards(self.ctx, self.gathered.data_ptr(), self.world, self.bytes, self.n_max,
+                                          self.m_max, self.n_of, self.m_of, self.e.data_ptr(), C.byref(self.res),
+                                          C.byref(self.out), self.stream)
+        if rc == N.PARSE_FALLBACK:   # some shard is not OK: the synchronous path reports it exactly
+            f = analyze_device(self.dt, N.MODE_REPORT, stream=self.stream, device=self.device)
+            return combine_shards(f, self.dt, self.dist, self.device, self.stream, self.n_max, self.m_max)
+        if rc != N.OK:
+            raise N.NativeError(f"heteff_merge_shards failed ({rc}): {N.last_error(self.ctx)}")
+        return _findings(self.res, self.host_sum[: self.ntot], self.dev_sum[: self.mtot], [])
