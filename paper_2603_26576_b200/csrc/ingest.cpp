@@ -181,6 +181,7 @@ struct Entry {
 struct Slice {
     uint64_t id = 0;
     int64_t owner = -1;
+    const char *stop = nullptr;   // one past the entry's closing brace
     std::vector<uint8_t> kind;
     std::vector<int64_t> stream;
     std::vector<uint64_t> start, end;
@@ -291,7 +292,47 @@ bool parse_entry(const Entry &en, Slice &out)
         } while (c.eat(','));
     }
     if (!c.eat('}') || !h_id || !h_recs) { out.fail = c.p; return false; }
+    out.stop = c.p;
     return true;
+}
+
+// entry-start candidate at '{': the first key is "rank" (host) or "id" (device)
+// -- what every writer emits; records start with other keys
+int entry_kind_at(const char *q, const char *e)
+{
+    ++q;
+    while (q < e && (*q == ' ' || *q == '\n' || *q == '\r' || *q == '\t')) ++q;
+    if (e - q >= 6 && memcmp(q, "\"rank\"", 6) == 0) return 0;
+    if (e - q >= 4 && memcmp(q, "\"id\"", 4) == 0) return 1;
+    return -1;
+}
+
+// phase 0 of one chunk [a, b): speculative discovery + parse of the entries starting there
+struct Spec {
+    size_t off;          // entry start offset
+    int dev;
+    Slice slice;
+};
+
+void discover(const char *data, size_t len, size_t a, size_t b, std::vector<Spec> &found)
+{
+    const char *e = data + len;
+    const char *q = data + a;
+    while (q < data + b) {
+        q = static_cast<const char *>(memchr(q, '{', (size_t)(data + b - q)));
+        if (!q) break;
+        const int kind = entry_kind_at(q, e);
+        if (kind < 0) { ++q; continue; }
+        Spec sp;
+        sp.off = (size_t)(q - data);
+        sp.dev = kind;
+        if (parse_entry(Entry{q, e, kind == 1}, sp.slice) && sp.slice.stop) {
+            q = sp.slice.stop;
+            found.push_back(std::move(sp));
+        } else {
+            ++q;   // not an entry after all (or an error the skeleton pass will meet)
+        }
+    }
 }
 
 }  // namespace
@@ -615,12 +656,47 @@ int heteff_parse_trace(const char *data, size_t len, int nthreads, heteff_parsed
         *fail_offset = (int64_t)(at - data);
         return HETEFF_PARSE_FALLBACK;
     };
-    // ---- phase 1: top level + entry byte ranges
+    int nt = nthreads > 0 ? nthreads : (int)std::thread::hardware_concurrency();
+    if (nt < 1) nt = 1;
     if (c.e - c.p >= 3 && (unsigned char)c.p[0] == 0xEF && (unsigned char)c.p[1] == 0xBB) return fail(c.p);   // BOM
+    // ---- phase 0 (parallel): every chunk finds and parses the entries that start in it
+    std::vector<std::vector<Spec>> spec((size_t)nt);
+    {
+        std::vector<std::thread> pool;
+        const size_t chunk = (len + (size_t)nt - 1) / (size_t)nt;
+        for (int t = 0; t < nt; ++t) {
+            const size_t a = (size_t)t * chunk, b = a + chunk < len ? a + chunk : len;
+            if (a >= b) continue;
+            if (t == 0) continue;   // run chunk 0 on this thread below
+            pool.emplace_back(discover, data, len, a, b, std::ref(spec[(size_t)t]));
+        }
+        if (len > 0) discover(data, len, 0, chunk < len ? chunk : len, spec[0]);
+        for (auto &th : pool) th.join();
+    }
+    // chunks are disjoint and in order, so the candidates are sorted by offset
+    std::vector<Spec *> cand;
+    for (auto &v : spec)
+        for (auto &x : v) cand.push_back(&x);
+    auto lookup = [&](size_t off) -> Spec * {
+        size_t lo = 0, hi = cand.size();
+        while (lo < hi) {
+            const size_t mid = (lo + hi) >> 1;
+            if (cand[mid]->off < off) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo < cand.size() && cand[lo]->off == off ? cand[lo] : nullptr;
+    };
+    // ---- phase 1 (sequential skeleton): the top level; each entry is taken from phase 0 by
+    // its offset, or skipped and queued for phase 2 when phase 0 did not decide it
     if (!c.eat('{')) return fail(c.p);
     bool h_ver = false, h_tu = false, h_hosts = false, h_devs = false;
     std::vector<Entry> entries;
+    std::vector<Slice> slices;
+    std::vector<size_t> todo;   // entries phase 0 did not parse
     size_t n_hosts = 0;
+    std::vector<Entry> dev_entries;
+    std::vector<Slice> dev_slices;
+    std::vector<size_t> dev_todo;
     if (!c.peek('}')) {
         do {
             const char *k;
@@ -638,24 +714,30 @@ int heteff_parse_trace(const char *data, size_t len, int nthreads, heteff_parsed
             } else if (key_is(k, kn, "hosts") || key_is(k, kn, "devices")) {
                 const bool dev = key_is(k, kn, "devices");
                 if ((dev ? h_devs : h_hosts) || !c.eat('[')) return fail(c.p);
-                std::vector<Entry> mine;
+                std::vector<Entry> &E = dev ? dev_entries : entries;
+                std::vector<Slice> &S = dev ? dev_slices : slices;
+                std::vector<size_t> &T = dev ? dev_todo : todo;
                 if (!c.peek(']')) {
                     do {
                         c.ws();
                         const char *b = c.p;
-                        if (!c.peek('{') || !skip_value(c)) return fail(b);
-                        mine.push_back(Entry{b, c.p, dev});
+                        if (!c.peek('{')) return fail(b);
+                        Spec *sp = lookup((size_t)(b - data));
+                        if (sp && sp->dev == (dev ? 1 : 0)) {
+                            c.p = sp->slice.stop;
+                            E.push_back(Entry{b, c.p, dev});
+                            S.push_back(std::move(sp->slice));
+                        } else {
+                            if (!skip_value(c)) return fail(b);
+                            T.push_back(E.size());
+                            E.push_back(Entry{b, c.p, dev});
+                            S.emplace_back();
+                        }
                     } while (c.eat(','));
                 }
                 if (!c.eat(']')) return fail(c.p);
-                if (dev) {
-                    h_devs = true;
-                    entries.insert(entries.end(), mine.begin(), mine.end());
-                } else {
-                    h_hosts = true;
-                    entries.insert(entries.begin(), mine.begin(), mine.end());   // hosts first
-                    n_hosts = mine.size();
-                }
+                if (dev) h_devs = true;
+                else { h_hosts = true; n_hosts = entries.size(); }
             } else {
                 return fail(c.p);
             }
@@ -664,26 +746,27 @@ int heteff_parse_trace(const char *data, size_t len, int nthreads, heteff_parsed
     if (!c.eat('}') || !h_ver || !h_tu || !h_hosts || !h_devs) return fail(c.p);
     c.ws();
     if (c.p != c.e) return fail(c.p);
+    for (size_t i : dev_todo) todo.push_back(n_hosts + i);   // hosts first, then devices
+    entries.insert(entries.end(), dev_entries.begin(), dev_entries.end());
+    for (auto &x : dev_slices) slices.push_back(std::move(x));
 
-    // ---- phase 2: entries in parallel
-    std::vector<Slice> slices(entries.size());
+    // ---- phase 2 (parallel): entries phase 0 left (unusual key order, errors)
     std::atomic<size_t> next{0};
-    int nt = nthreads > 0 ? nthreads : (int)std::thread::hardware_concurrency();
-    if (nt < 1) nt = 1;
-    if ((size_t)nt > entries.size()) nt = entries.size() > 0 ? (int)entries.size() : 1;
     auto work = [&]() {
         for (;;) {
-            const size_t i = next.fetch_add(1);
-            if (i >= entries.size()) break;
+            const size_t q = next.fetch_add(1);
+            if (q >= todo.size()) break;
+            const size_t i = todo[q];
             if (!parse_entry(entries[i], slices[i]) && !slices[i].fail) slices[i].fail = entries[i].b;
         }
     };
     std::vector<std::thread> pool;
-    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+    const int nt2 = (size_t)nt > todo.size() ? (todo.empty() ? 1 : (int)todo.size()) : nt;
+    for (int t = 1; t < nt2; ++t) pool.emplace_back(work);
     work();
     for (auto &th : pool) th.join();
-    for (const Slice &s : slices)
-        if (s.fail) return fail(s.fail);
+    for (const Slice &sl : slices)
+        if (sl.fail) return fail(sl.fail);
 
     // ---- merge in file order
     heteff_parsed *P = new heteff_parsed();
