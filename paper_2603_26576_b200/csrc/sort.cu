@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(512) build_res_keys(const int32_t *__restrict_
 struct PassSmem {
     u64 k[kTileKeys];
     uint32_t v[kTileKeys];
+    uint16_t src[kTileKeys];     // payload passes: in-tile source position of each sorted key
     uint32_t whist[kW][kBins];   // per-warp digit counts -> warp-exclusive offsets
     uint32_t bexcl[kBins];       // tile-local exclusive digit offsets
     uint32_t gbase[kBins];       // destination of the tile's first key of each digit
@@ -300,10 +301,20 @@ __device__ __forceinline__ uint32_t peers_of(uint32_t d, int dbits, uint32_t val
 
 // one digit pass: stable rank of the tile's keys, reorder in shared memory,
 // coalesced digit runs to their scanned global positions
+// payload columns moved with the keys (start-ordered input: start, end, kind ride
+// along, so the sorted columns need no random gather at the end)
+struct Payload {
+    const u64 *s_in, *e_in;
+    const uint8_t *k_in;
+    u64 *s_out, *e_out;
+    uint8_t *k_out;
+};
+
+template <bool PL>
 __global__ void __launch_bounds__(kT, (kT <= 512 ? 2 : 1)) downsweep(const u64 *__restrict__ kin, const uint32_t *__restrict__ vin,
                                                    u64 *__restrict__ kout, uint32_t *__restrict__ vout, int64_t n,
                                                    int shift, int dbits, const uint32_t *__restrict__ offs,
-                                                   int64_t tiles)
+                                                   int64_t tiles, Payload pl)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PassSmem &sm = *reinterpret_cast<PassSmem *>(smem_raw);
@@ -370,6 +381,7 @@ __global__ void __launch_bounds__(kT, (kT <= 512 ? 2 : 1)) downsweep(const u64 *
             const uint32_t pos = sm.bexcl[dj] + sm.whist[warp][dj] + ((rk[j >> 1] >> (16 * (j & 1))) & 0xffffu);
             sm.k[pos] = k[j];
             sm.v[pos] = __ldcs(vin + wbase + o);
+            if (PL) sm.src[pos] = (uint16_t)(warp * 32 * kI + o);
         }
     }
     __syncthreads();
@@ -380,6 +392,12 @@ __global__ void __launch_bounds__(kT, (kT <= 512 ? 2 : 1)) downsweep(const u64 *
         const u64 dst = (u64)sm.gbase[dd] + (u64)(i - (int)sm.bexcl[dd]);
         kout[dst] = key;
         vout[dst] = sm.v[i];
+        if (PL) {   // tile-local gather (L2-resident), coalesced digit-run writes
+            const int64_t src = base + sm.src[i];
+            pl.s_out[dst] = __ldg(pl.s_in + src);
+            pl.e_out[dst] = __ldg(pl.e_in + src);
+            pl.k_out[dst] = __ldg(pl.k_in + src);
+        }
     }
 }
 
@@ -401,6 +419,16 @@ __global__ void __launch_bounds__(512) finish_narrow(const u64 *__restrict__ K, 
         oe[i] = __ldg(E + v);
         ok[i] = __ldg(KD + v);
         if (perm) perm[i] = v;
+    }
+}
+
+__global__ void __launch_bounds__(512) finish_payload(const u64 *__restrict__ K, const uint32_t *__restrict__ V,
+                                                      int64_t n, KeyPlan kp, int32_t *__restrict__ orr,
+                                                      int64_t *__restrict__ perm)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        orr[i] = unflip((unsigned int)__ldcs(K + i) + kp.rmin);
+        if (perm) perm[i] = __ldcs(V + i);
     }
 }
 
@@ -468,7 +496,8 @@ size_t sort_workspace_bytes(int64_t n)
 {
     const int64_t m = tiles_of(n) * rsort::kBins;
     return 2 * up256((size_t)n * 8) + 2 * up256((size_t)n * 4) + up256((size_t)m * 4) +
-           up256((size_t)(m / rsort::kScanBlock + 1) * 4) + up256(sizeof(rsort::Range));
+           up256((size_t)(m / rsort::kScanBlock + 1) * 4) + up256(sizeof(rsort::Range)) +
+           2 * up256((size_t)n * 8) + up256((size_t)n);   // payload ping-pong (start-ordered input)
 }
 
 static int bits_of(u64 x) { return x ? 64 - __builtin_clzll(x) : 0; }
@@ -494,8 +523,11 @@ cudaError_t sort_records(const u64 *S, const u64 *E, const int32_t *R, const uin
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     static bool attr_done = false;
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(downsweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(downsweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)sizeof(PassSmem));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(downsweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(PassSmem));
         if (e != cudaSuccess) return e;
         attr_done = true;
     }
@@ -512,6 +544,9 @@ cudaError_t sort_records(const u64 *S, const u64 *E, const int32_t *R, const uin
     uint32_t *counts = static_cast<uint32_t *>(take((size_t)m * 4));
     uint32_t *bsum = static_cast<uint32_t *>(take((size_t)(m / kScanBlock + 1) * 4));
     Range *range = static_cast<Range *>(take(sizeof(Range)));
+    u64 *PS = static_cast<u64 *>(take((size_t)n * 8));
+    u64 *PE = static_cast<u64 *>(take((size_t)n * 8));
+    uint8_t *PK = static_cast<uint8_t *>(take((size_t)n));
     cudaError_t e;
 
     // 1. key range (one D2H of 32 bytes decides the key layout)
@@ -535,6 +570,10 @@ cudaError_t sort_records(const u64 *S, const u64 *E, const int32_t *R, const uin
     u64 *kin = K0, *kout = K1;
     uint32_t *vin = V0, *vout = V1;
     int total_passes = 0;
+    // start-ordered input: start / end / kind ride along with the keys (no final gather);
+    // the last pass writes them straight into the output columns
+    const bool carry = kp.res_only && stage_bits[0] > 0;
+    Payload pl{S, E, KD, nullptr, nullptr, nullptr};
     for (int stage = 0; stage < 2; ++stage) {
         const int bits = stage_bits[stage];
         if (stage == 1 && !kp.wide) break;
@@ -551,8 +590,20 @@ cudaError_t sort_records(const u64 *S, const u64 *E, const int32_t *R, const uin
             scan_sums<<<(unsigned)nbb, kScanT, 0, s>>>(counts, mm, bsum);
             scan_top<<<1, kScanT, 0, s>>>(bsum, nbb);
             scan_blocks<<<(unsigned)nbb, kScanT, 0, s>>>(counts, mm, bsum);
-            downsweep<<<(unsigned)tiles, kT, sizeof(PassSmem), s>>>(kin, vin, kout, vout, n, shift, kp.dbits, counts,
-                                                                    tiles);
+            if (carry) {
+                const bool to_out = ((passes - 1 - p) & 1) == 0;
+                pl.s_out = to_out ? os : PS;
+                pl.e_out = to_out ? oe : PE;
+                pl.k_out = to_out ? ok : PK;
+                downsweep<true><<<(unsigned)tiles, kT, sizeof(PassSmem), s>>>(kin, vin, kout, vout, n, shift,
+                                                                              kp.dbits, counts, tiles, pl);
+                pl.s_in = pl.s_out;
+                pl.e_in = pl.e_out;
+                pl.k_in = pl.k_out;
+            } else {
+                downsweep<false><<<(unsigned)tiles, kT, sizeof(PassSmem), s>>>(kin, vin, kout, vout, n, shift,
+                                                                               kp.dbits, counts, tiles, pl);
+            }
             u64 *tk = kin; kin = kout; kout = tk;
             uint32_t *tv = vin; vin = vout; vout = tv;
             ++total_passes;
@@ -562,6 +613,8 @@ cudaError_t sort_records(const u64 *S, const u64 *E, const int32_t *R, const uin
     (void)nb;
     if (!kp.wide && !kp.res_only) {
         finish_narrow<<<grid_for(n, sms), 512, 0, s>>>(kin, vin, n, kp, E, KD, os, oe, orr, ok, perm);
+    } else if (carry) {
+        finish_payload<<<grid_for(n, sms), 512, 0, s>>>(kin, vin, n, kp, orr, perm);
     } else {
         finish_gather<<<grid_for(n, sms), 512, 0, s>>>(vin, n, S, E, R, KD, os, oe, orr, ok, perm);
     }

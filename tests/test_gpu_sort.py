@@ -91,6 +91,17 @@ def test_sort_time_ordered_log_sorts_by_resource_only():
     assert got.start_sorted and got.key_bits == 12 and got.passes == 2
 
 
+@pytest.mark.parametrize("ids,passes", [(200, 1), (70_000, 3), (1, 0)])
+def test_sort_time_ordered_payload_pass_counts(ids, passes):
+    """Start-ordered input carries start/end/kind through 0, 1 (odd) or 3 passes."""
+    rng = np.random.default_rng(ids)
+    n = 150_000
+    s = np.sort(rng.integers(0, 1 << 50, n, dtype=np.uint64))
+    r = rng.integers(0, ids, n, dtype=np.int32)
+    got = _check_sort(s, s + rng.integers(0, 9, n, dtype=np.uint64), r, rng.integers(0, 2, n, dtype=np.uint8))
+    assert got.start_sorted and got.passes == passes
+
+
 @pytest.mark.parametrize("bits", [8, 17, 33, 47, 64])
 def test_sort_key_widths(bits):
     rng = np.random.default_rng(bits)
