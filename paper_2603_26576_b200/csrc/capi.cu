@@ -416,7 +416,7 @@ int heteff_analyze_regions(heteff_ctx *ctx, const heteff_trace *t, const heteff_
     const size_t b_dagg = up((size_t)(tiles + 1) * 24), b_drun = up((size_t)(tiles + 1) * 16);
     const size_t b_dsum = up((size_t)(tiles + 1) * 32), b_dck = up((size_t)(tiles + 1) * 24);
     const size_t b_scan = up((size_t)scan_blocks * 64), b_tst = up((size_t)(tiles + 1) * 16);
-    const size_t b_dsub = up((size_t)(tiles + 1) * 8 * 64);
+    const size_t b_dsub = up((size_t)(tiles + 1) * hb::region_subs() * 64);
     const size_t b_hacc = up((size_t)W * hid * 24), b_dacc = up((size_t)W * did * 32);
     const size_t b_E = up(W * 8), b_dmax = up(W * 8), b_own = up((size_t)did * 4);
     CK(ensure(ctx->reg_ws, b_hseg + b_dseg + b_hagg + b_hck + b_dagg + b_drun + b_dsum + b_dck + b_scan + b_tst + b_dsub + b_hacc +

@@ -162,6 +162,7 @@ struct RegParams {
 };
 
 size_t region_hchunks(int64_t hn);
+size_t region_subs();
 size_t region_tiles(int64_t dn);
 cudaError_t launch_regions_prepare(const RegParams &p, cudaStream_t s);
 cudaError_t launch_regions_phase1(const RegParams &p, cudaStream_t s);

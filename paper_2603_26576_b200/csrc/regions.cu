@@ -50,7 +50,13 @@ namespace hb {
 namespace reg {
 
 constexpr int kHC = 256;             // host records per checkpoint chunk
-constexpr int kDT = 128;             // device tile threads
+#ifndef HB_REG_DT
+#define HB_REG_DT 128
+#endif
+#ifndef HB_REG_STAGE
+#define HB_REG_STAGE 1024
+#endif
+constexpr int kDT = HB_REG_DT;       // device tile threads
 constexpr int kDI = 9;               // device records per thread (odd: conflict-free smem)
 constexpr int kDTile = kDT * kDI;    // 1152 device records per tile (= checkpoint chunk)
 constexpr int kST = 1024;            // scan block
@@ -494,7 +500,7 @@ struct DevTile {
 // the owner's OFFLOAD intervals overlapping a tile's time range, staged in
 // shared memory (sorted, disjoint: ends increase too) so the per-thread merges
 // run out of smem instead of chains of dependent global loads
-constexpr int kStage = 1024;
+constexpr int kStage = HB_REG_STAGE;
 
 struct OffStage {
     u64 s[kStage];
@@ -850,6 +856,7 @@ __global__ void __launch_bounds__(kFT) reg_final(const __grid_constant__ RegPara
 }  // namespace reg
 
 size_t region_tiles(int64_t dn) { return (size_t)((dn + reg::kDTile - 1) / reg::kDTile); }
+size_t region_subs() { return (size_t)reg::kSubs; }
 size_t region_hchunks(int64_t hn) { return (size_t)((hn + reg::kHC - 1) / reg::kHC); }
 
 static int grid_cap(int64_t g, int sms, int per_sm)
@@ -880,7 +887,7 @@ cudaError_t launch_regions_prepare(const RegParams &p, cudaStream_t s)
     if (p.tiles > 0) {
         rd_runagg<<<grid_cap((p.tiles + 7) / 8, sms, 8), 256, 0, s>>>(p);
         seg_scan<0, 2>(p.dagg, p.tiles, p.scan_tmp, p.drun, s);
-        rd_sums<<<grid_cap(p.tiles, sms, 5), kDT, 0, s>>>(p);
+        rd_sums<<<grid_cap(p.tiles, sms, kDT <= 128 ? 5 : 3), kDT, 0, s>>>(p);
         seg_scan<3, 0>(p.dsum, p.tiles, p.scan_tmp, p.dck, s);
     }
     return cudaGetLastError();
