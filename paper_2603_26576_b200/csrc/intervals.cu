@@ -277,6 +277,39 @@ __global__ void __launch_bounds__(1024) prefix_u32(const uint32_t *__restrict__ 
     if (n == 0 && tid == 0) out[0] = 0;
 }
 
+// multi-block exclusive prefix of u32 flags into int64 positions (out[n] = total):
+// per-block sums, a scan of the block sums (scan_counts), per-block apply
+__global__ void __launch_bounds__(kT) flag_sums(const uint32_t *__restrict__ f, int64_t n, uint32_t *__restrict__ bsum)
+{
+    __shared__ uint32_t ws[kT / 32 + 1];
+    const int64_t b0 = (int64_t)blockIdx.x * kB + (int64_t)threadIdx.x * kI;
+    uint32_t c = 0;
+#pragma unroll
+    for (int q = 0; q < kI; ++q) c += b0 + q < n ? f[b0 + q] : 0u;
+    uint32_t tot;
+    block_excl_sum(c, ws, tot);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kT) flag_apply(const uint32_t *__restrict__ f, int64_t n,
+                                                 const int64_t *__restrict__ boff, const int64_t *total,
+                                                 int64_t *__restrict__ out)
+{
+    __shared__ uint32_t ws[kT / 32 + 1];
+    const int64_t b0 = (int64_t)blockIdx.x * kB + (int64_t)threadIdx.x * kI;
+    uint32_t v[kI], c = 0;
+#pragma unroll
+    for (int q = 0; q < kI; ++q) { v[q] = b0 + q < n ? f[b0 + q] : 0u; c += v[q]; }
+    uint32_t tot;
+    int64_t run = boff[blockIdx.x] + block_excl_sum(c, ws, tot);
+#pragma unroll
+    for (int q = 0; q < kI; ++q) {
+        if (b0 + q < n) out[b0 + q] = run;
+        run += v[q];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[n] = *total;
+}
+
 __global__ void sub_write(const u64 *__restrict__ as, const u64 *__restrict__ ae, int64_t na,
                           const u64 *__restrict__ bs, const u64 *__restrict__ be, int64_t nb,
                           const uint32_t *__restrict__ fa, const uint32_t *__restrict__ fb,
@@ -440,8 +473,19 @@ cudaError_t iv_flatten(const u64 *s, const u64 *e, int64_t n, u64 *os, u64 *oe, 
 
 size_t iv_subtract_ws(int64_t na, int64_t nb)
 {
+    const int64_t ba = iv::nblocks(na) + 1, bb = iv::nblocks(nb) + 1;
     return up256((size_t)(na + 1) * 4) + up256((size_t)(nb + 1) * 4) + up256((size_t)(na + 1) * 8) +
-           up256((size_t)(nb + 1) * 8);
+           up256((size_t)(nb + 1) * 8) + 2 * up256((size_t)(ba + bb) * 12) + 256;
+}
+
+// exclusive positions of n flags (out[n] = total) with the multi-block scan
+static void flag_prefix(const uint32_t *f, int64_t n, int64_t *out, uint32_t *bsum, int64_t *boff, int64_t *total,
+                        cudaStream_t st)
+{
+    const int64_t nb = iv::nblocks(n > 0 ? n : 1);
+    iv::flag_sums<<<(unsigned)nb, iv::kT, 0, st>>>(f, n, bsum);
+    iv::scan_counts<<<1, 1024, 0, st>>>(bsum, nb, boff, total);
+    iv::flag_apply<<<(unsigned)nb, iv::kT, 0, st>>>(f, n, boff, total, out);
 }
 
 cudaError_t iv_subtract(const u64 *as, const u64 *ae, int64_t na, const u64 *bs, const u64 *be, int64_t nb, u64 *os,
@@ -458,8 +502,14 @@ cudaError_t iv_subtract(const u64 *as, const u64 *ae, int64_t na, const u64 *bs,
     int64_t *pa = static_cast<int64_t *>(take((size_t)(na + 1) * 8));
     int64_t *pb = static_cast<int64_t *>(take((size_t)(nb + 1) * 8));
     iv::sub_flags<<<grid_of(na + nb, 256), 256, 0, st>>>(as, ae, na, bs, be, nb, fa, fb);
-    iv::prefix_u32<<<1, 1024, 0, st>>>(fa, na, pa);
-    iv::prefix_u32<<<1, 1024, 0, st>>>(fb, nb, pb);
+    const int64_t ba = iv::nblocks(na) + 1, bb = iv::nblocks(nb) + 1;
+    uint32_t *bsa = static_cast<uint32_t *>(take((size_t)ba * 4));
+    int64_t *boa = static_cast<int64_t *>(take((size_t)ba * 8));
+    uint32_t *bsb = static_cast<uint32_t *>(take((size_t)bb * 4));
+    int64_t *bob = static_cast<int64_t *>(take((size_t)bb * 8));
+    int64_t *tots = static_cast<int64_t *>(take(16));
+    flag_prefix(fa, na, pa, bsa, boa, tots, st);
+    flag_prefix(fb, nb, pb, bsb, bob, tots + 1, st);
     iv::sub_write<<<grid_of(na + nb, 256), 256, 0, st>>>(as, ae, na, bs, be, nb, fa, fb, pa, pb, os, oe);
     int64_t ca = 0, cb = 0;
     cudaError_t err;

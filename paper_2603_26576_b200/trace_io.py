@@ -444,7 +444,7 @@ class _IView(C.Structure):
                 ("name_off", C.c_void_p), ("name_len", C.c_void_p)]
 
 
-def import_mapped(data, mapping: CategoryMapping, nthreads: int | None = None):
+def import_mapped(data, mapping: CategoryMapping, nthreads: int | None = None, columns: bool = False):
     """Chrome-trace events -> (Trace, warnings) (drop-in for ``trace_io.py:263-342``)."""
     raw = data.encode("utf-8") if isinstance(data, str) else bytes(data)
     lib = N.load()
@@ -466,16 +466,20 @@ def import_mapped(data, mapping: CategoryMapping, nthreads: int | None = None):
         v = _IView()
         lib.heteff_imported_info(handle, C.addressof(v))
         k, u = v.n_records, v.n_unmapped
-        is_dev = _arr(v.is_dev, k, np.uint8).tolist()
-        kind = _arr(v.kind, k, np.uint8).tolist()
-        res = _arr(v.res, k, np.uint64).tolist()
-        st = _arr(v.start, k, np.uint64).tolist()
-        en = _arr(v.end, k, np.uint64).tolist()
+        is_dev = _arr(v.is_dev, k, np.uint8)
+        kind = _arr(v.kind, k, np.uint8)
+        res = _arr(v.res, k, np.uint64)
+        st = _arr(v.start, k, np.uint64)
+        en = _arr(v.end, k, np.uint64)
+        if not columns:
+            is_dev, kind, res, st, en = (x.tolist() for x in (is_dev, kind, res, st, en))
         um = _arr(v.unmapped, u, np.int64).tolist()
         no = _arr(v.name_off, u, np.int64).tolist()
         nl = _arr(v.name_len, u, np.int64).tolist()
     finally:
         lib.heteff_imported_free(handle)
+    if columns:
+        return (is_dev, kind, res, st, en), [(i, raw[o:o + n].decode("utf-8")) for i, o, n in zip(um, no, nl)]
     hrecs, drecs = [], []
     for d, kd, r, a, b in zip(is_dev, kind, res, st, en):
         if d:
@@ -512,3 +516,29 @@ def write_trace(trace: Trace) -> bytes:
     doc = {"version": FORMAT_VERSION, "time_unit": "ns",
            "hosts": [{"rank": r, "records": by_rank[r]} for r in trace.host_processes], "devices": devices}
     return (json.dumps(doc, indent=2) + "\n").encode("utf-8")
+
+
+def import_mapped_packed(data, mapping: CategoryMapping, nthreads: int | None = None):
+    """Chrome-trace events straight into a :class:`~.packing.PackedTrace` (no Python record
+    objects): the imported trace declares exactly the ranks and devices that received
+    records (``trace_io.py:333-341``), in id order.  Returns ``(packed, warnings)``."""
+    raw = data.encode("utf-8") if isinstance(data, str) else bytes(data)
+    out = import_mapped(raw, mapping, nthreads, columns=True)
+    if isinstance(out[0], Trace):   # the strict fallback decided it
+        t, w = out
+        return pack_trace(t), w
+    (is_dev, kind, res, st, en), unmapped = out
+    _, warnings = _assemble([], [], unmapped, mapping)   # MappingError / warnings exactly as the reference
+    h, d = is_dev == 0, is_dev == 1
+    h_ids, h_dense = np.unique(res[h], return_inverse=True)
+    d_ids, d_dense = np.unique(res[d], return_inverse=True)
+    h_res, d_res = h_dense.astype(np.int32), d_dense.astype(np.int32)
+    state_rank = np.array([2, 1, 0], dtype=np.uint8)[kind[h]] if h.any() else np.zeros(0, np.uint8)
+    ho = np.lexsort((state_rank, en[h], st[h], h_res))
+    do = np.lexsort((kind[d], en[d], st[d], d_res))
+    host = RecordColumns(st[h][ho], en[h][ho], h_res[ho], kind[h][ho])
+    dev = RecordColumns(st[d][do], en[d][do], d_res[do], kind[d][do])
+    nh, nd = int(h_ids.size), int(d_ids.size)
+    packed = PackedTrace(host, dev, h_ids.tolist(), d_ids.tolist(), np.arange(nh, dtype=np.int32),
+                         np.arange(nd, dtype=np.int32), nh, nd, nh, nd)
+    return packed, warnings

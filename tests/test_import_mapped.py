@@ -57,3 +57,21 @@ def test_import_native_fast_path_decides_plain_documents():
     assert min(r.interval.start for r in t.device_records) == 0
     assert max(r.interval.end for r in t.device_records) == 19999 * 1000 + 2000
     assert t.devices == tuple(trace_io.DeviceDecl(d) for d in (0, 1, 2))
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if "trace" in c], ids=[c["tag"] for c in CASES if "trace" in c])
+def test_import_mapped_packed_equals_pack_of_reference_trace(case):
+    from golden_io import to_trace
+    from paper_2603_26576_b200.packing import pack_trace
+
+    import numpy as np
+
+    ref = pack_trace(to_trace(case["trace"]))
+    got, w = trace_io.import_mapped_packed(case["doc"], trace_io.read_mapping(case["map"]))
+    assert w == case["warnings"]
+    for side in ("host", "dev"):
+        a, b = getattr(got, side), getattr(ref, side)
+        for col in ("start", "end", "res", "kind"):
+            assert np.array_equal(getattr(a, col), getattr(b, col)), (side, col)
+    assert list(got.host_ids) == list(ref.host_ids) and list(got.dev_ids) == list(ref.dev_ids)
+    assert (got.n, got.m) == (ref.n, ref.m)
