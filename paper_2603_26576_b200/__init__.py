@@ -38,6 +38,19 @@ from .model import (
     Trace,
     ValidationReport,
 )
+from .report import RenderOptions, render_json, render_text
+from .trace_io import (
+    CategoryMapping,
+    MappingError,
+    MappingRule,
+    TraceFormatError,
+    import_mapped,
+    import_mapped_packed,
+    read_mapping,
+    read_trace,
+    read_trace_packed,
+    write_trace,
+)
 
 __version__ = "0.1.0"
 
@@ -47,4 +60,7 @@ __all__ = [
     "RegionReport", "region_reports", "compute_report", "device_metrics", "host_metrics", "summarize_device", "summarize_host", "validate",
     "U64_MAX", "DeviceActivityKind", "DeviceDecl", "DeviceRecord", "HostRecord", "HostState", "Interval",
     "InvalidTraceError", "Trace", "ValidationReport",
+    "RenderOptions", "render_json", "render_text",
+    "CategoryMapping", "MappingError", "MappingRule", "TraceFormatError", "import_mapped", "import_mapped_packed",
+    "read_mapping", "read_trace", "read_trace_packed", "write_trace",
 ]
