@@ -44,6 +44,12 @@
 #include "ptx.cuh"
 #include "exact.cuh"
 
+#ifndef HB_DEV_SCHED
+#define HB_DEV_SCHED 2   // single-segment device tiles: 0 two passes, 1 one pass + correction, 2 per-warp adaptive
+#endif
+#ifndef HB_UNROLL_G
+#define HB_UNROLL_G HB_ITEMS
+#endif
 #ifndef HB_UNROLL_A
 #define HB_UNROLL_A HB_ITEMS
 #endif
@@ -69,19 +75,20 @@ __device__ unsigned long long hb_prof_buf[1024 * kProfSlots];
 struct Phases {
 #ifdef HB_PROF
     long long a = 0, bar = 0, b = 0, emit = 0, t = 0;
-    long long hb = 0, hemit = 0, hn = 0, dn = 0, hn2 = 0;
+    long long hb = 0, hemit = 0, hn = 0, dn = 0, hn2 = 0, mg = 0, nd = 0;
     __device__ __forceinline__ void mark() { t = clock64(); }
     __device__ __forceinline__ void add(long long &acc) { const long long n = clock64(); acc += n - t; t = n; }
 #else
     __device__ __forceinline__ void mark() {}
     template <typename X>
     __device__ __forceinline__ void add(X &) {}
-    int a, bar, b, emit, hb, hemit, hn, dn, hn2;
+    int a, bar, b, emit, hb, hemit, hn, dn, hn2, mg, nd;
 #endif
 };
 
 constexpr int kUnrollA = HB_UNROLL_A;
 constexpr int kUnrollB = HB_UNROLL_B;
+constexpr int kUnrollG = HB_UNROLL_G;   // general (multi-segment / multi-rank) paths: off the hot loop
 
 struct StageSmem {
     u64 s[kTile];
@@ -643,7 +650,7 @@ __device__ __forceinline__ void phase_a(const StageSmem &sm, const Ctrl *c, int 
         pr = sm.r[b - 1];
     }
     mn = sm.s[b];
-#pragma unroll kUnrollA
+#pragma unroll kUnrollG
     for (int j = 0; j < kItems; ++j) {
         if (j < nv) {
             const int32_t r = sm.r[b + j];
@@ -959,7 +966,7 @@ __device__ __forceinline__ void host_compute(const Params &p, const StageSmem &s
             done = true;
         }
     }
-#pragma unroll kUnrollB
+#pragma unroll kUnrollG
     for (int j = 0; j < kItems; ++j) {
         if (!done && j < nv) {
             const int32_t r = sm.r[b + j];
@@ -1039,7 +1046,7 @@ __device__ __forceinline__ bool dev_phase_b(const Params &p, const StageSmem &sm
         pr = sm.r[b - 1];
         ps = D.ld(sm.s, b - 1);
     }
-#pragma unroll kUnrollB
+#pragma unroll kUnrollG
     for (int j = 0; j < kItems; ++j) {
         if (j < nv) {
             const T s0 = D.ld(sm.s, b + j), e0 = D.ld(sm.e, b + j);
@@ -1096,10 +1103,27 @@ __device__ __forceinline__ u64 device_E(const Params &p, int tid, int lane, u64 
 // Single-segment device tile (every record of one device -- the common case):
 // no segment flags, the tile base is its first start (records are
 // start-sorted), every running max is a plain 32-bit max relative to it.
-// Returns false (nothing done) if some end leaves the base's 2^32 window.
+// Each thread needs its tile-exclusive carry X (the running max of the ends
+// before its records), known only after the CTA barrier.  Two schedules, chosen
+// per warp from its previous device tile:
+//  * ONE pass (serialized streams): before the barrier, the union pieces
+//    c = max(run, e) - max(run, min(s, e)) with carry 0 and unclamped ends,
+//    plus the thread's max ends (the scan aggregate).  X only changes the
+//    records j with max(run_j, s_j) < X -- none when the thread's first start
+//    is >= X; otherwise an early-exit correction over that prefix.  A thread
+//    with an end beyond E redoes its pass clamped (records after the last
+//    host end: rare).  A warp that needed a correction switches to
+//  * TWO passes (overlapping streams): max ends (kept in registers) before the
+//    barrier, the union pass with the carry after it -- and back to one pass
+//    once no lane starts below its carry.
+// Starts / ends outside the base's 2^32 window: ends -> the general path
+// (tile-wide, decided after the barrier), starts -> findings (rescan).
+// Returns false (nothing done) if some end leaves the window.
 // -------------------------------------------------------------------------
+template <bool MERGED>
 __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
-                                           u64 &E_cache, bool &E_known, bool &signalled, int &kq, Phases &ph)
+                                           u64 &E_cache, bool &E_known, bool &signalled, int &kq, bool &one_pass,
+                                           Phases &ph)
 {
     ph.mark();
     const int warp = tid >> 5, lane = tid & 31;
@@ -1108,28 +1132,50 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
     const int64_t gi0 = tc.gbase + (int64_t)b;
     const u64 base = sm.s[0];
     const uint32_t bl = (uint32_t)base, bh = (uint32_t)(base >> 32);
-    const uint32_t *S32 = reinterpret_cast<const uint32_t *>(sm.s);
-    // phase A: kernel-only and all-record max of relative ends.  Ends are read as
-    // u64 (one conflict-free LDS.64 at the odd record stride, where two 32-bit
-    // halves would be 2-way conflicted) and, with the kinds, kept in registers
-    // for phase B.
-    uint32_t vK = 0, vKM = 0;
-    uint32_t er[kItems];
-    uint32_t kmask = 0;                     // bit j: record j is a kernel
-    bool out = false;
+    constexpr bool merged = MERGED;
+    uint32_t runK = 0, runKM = 0, cK = 0, cKM = 0, ps = 0;
+    uint32_t er[MERGED ? 1 : kItems];
+    uint32_t kmask = 0;             // bit j: record j is a kernel
+    bool out = false, bad = false;  // bad: start outside the window / order / zero-length / malformed
+    if (b > 0) ps = (uint32_t)sm.s[b - 1] - bl;
+    if constexpr (merged) {
+        er[0] = 0;
+#pragma unroll kUnrollB
+        for (int j = 0; j < kItems; ++j) {
+            if (j < nv) {
+                const u64 s64 = sm.s[b + j], e64 = sm.e[b + j];   // conflict-free LDS.64 at the odd record stride
+                const uint32_t sl = (uint32_t)s64, el = (uint32_t)e64;
+                out = out || (uint32_t)(e64 >> 32) != bh || el < bl;
+                const uint32_t s0 = sl - bl, e = el - bl;
+                bad = bad || (uint32_t)(s64 >> 32) != bh || sl < bl || ((j > 0 || b > 0) && s0 < ps) || s0 >= e;
+                const uint32_t s = min(s0, e);
+                const uint32_t loKM = max(runKM, s);
+                runKM = max(runKM, e);
+                cKM += runKM - loKM;
+                if (sm.k[b + j] == 0) {
+                    const uint32_t loK = max(runK, s);
+                    runK = max(runK, e);
+                    cK += runK - loK;
+                }
+                ps = s0;
+            }
+        }
+    } else {
 #pragma unroll kUnrollA
-    for (int j = 0; j < kItems; ++j) {
-        er[j] = 0;
-        if (j < nv) {
-            const u64 e64 = sm.e[b + j];
-            const uint32_t e = (uint32_t)e64 - bl;
-            out = out || (uint32_t)(e64 >> 32) != bh || (uint32_t)e64 < bl;   // outside [base, base + 2^32)
-            er[j] = e;
-            vKM = max(vKM, e);
-            if (sm.k[b + j] == 0) { vK = max(vK, e); kmask |= 1u << j; }
+        for (int j = 0; j < kItems; ++j) {
+            er[j] = 0;
+            if (j < nv) {
+                const u64 e64 = sm.e[b + j];
+                const uint32_t e = (uint32_t)e64 - bl;
+                out = out || (uint32_t)(e64 >> 32) != bh || (uint32_t)e64 < bl;
+                er[MERGED ? 0 : j] = e;
+                runKM = max(runKM, e);
+                if (sm.k[b + j] == 0) { runK = max(runK, e); kmask |= 1u << j; }
+            }
         }
     }
     const bool fit_w = __all_sync(0xffffffffu, !out);
+    uint32_t vK = runK, vKM = runKM;   // the thread's max (unclamped) ends: scan aggregate
     warp_max_scan2(vK, vKM, lane);
     if (lane == 31) { c->f_k[tc.st][warp] = vK; c->f_km[tc.st][warp] = vKM; c->f_fit[tc.st][warp] = fit_w; }
     ph.add(ph.a);
@@ -1156,36 +1202,85 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
         if (head) post_info(c, kq, tc.lt, tc.cnt, true, false, base + tK, base + tKM);
     }
     ph.add(ph.hb);
-    // phase B: the union pass in 32 bits, carry 0 (the epilogue warp fixes the head)
     const uint32_t Er = E <= base ? 0u : (E - base > 0xffffffffull ? 0xffffffffu : (uint32_t)(E - base));
     const int32_t r0 = sm.r[0];
     const bool decl = declared(p.dev_decl, p.dev_ids, p.m, r0);
-    bool rare = E < base || !decl;
-    uint32_t runK = min(xK, Er), runKM = min(xKM, Er), cK = 0, cKM = 0, ps = 0;
+    const bool clamp = nv > 0 && (E < base || runKM > Er);   // some end beyond E
+    bool rare = clamp || !decl;
     if (b == 0) rare = rare || (head && nv > 0 && sm.s[0] < c->prev_start[tc.st]);
-    else ps = S32[2 * (b - 1)] - bl;
+    const uint32_t XK = min(xK, Er), XKM = min(xKM, Er);
+    const uint32_t s_first = nv > 0 ? (uint32_t)sm.s[b] - bl : 0xffffffffu;
+    const bool need = !clamp && s_first < XKM;   // the carry reaches into this thread's records
+    one_pass = !__any_sync(0xffffffffu, need);
+#ifdef HB_PROF
+    ph.mg += merged;
+    ph.nd += !one_pass;
+#endif
+    if constexpr (!merged) {
+        // the union pass with the tile-exclusive carry and clamped ends
+        runK = XK; runKM = XKM;
 #pragma unroll kUnrollB
-    for (int j = 0; j < kItems; ++j) {
-        if (j < nv) {
-            const uint32_t s0 = S32[2 * (b + j)] - bl, e0 = er[j];
-            rare = rare || ((j > 0 || b > 0) && s0 < ps) || s0 >= e0 || e0 > Er;
-            const uint32_t e = min(e0, Er), s = min(s0, e);
+        for (int j = 0; j < kItems; ++j) {
+            if (j < nv) {
+                const u64 s64 = sm.s[b + j];
+                const uint32_t sl = (uint32_t)s64, s0 = sl - bl, e0 = er[MERGED ? 0 : j];
+#ifdef HB_NO_SCHECK
+                bad = bad || ((j > 0 || b > 0) && s0 < ps) || s0 >= e0;
+#else
+                bad = bad || (uint32_t)(s64 >> 32) != bh || sl < bl || ((j > 0 || b > 0) && s0 < ps) || s0 >= e0;
+#endif
+                const uint32_t e = min(e0, Er), s = min(s0, e);
+                const uint32_t loKM = max(runKM, s);
+                runKM = max(runKM, e);
+                cKM += runKM - loKM;
+                if ((kmask >> j) & 1u) {
+                    const uint32_t loK = max(runK, s);
+                    runK = max(runK, e);
+                    cK += runK - loK;
+                }
+                ps = s0;
+            }
+        }
+    } else if (clamp) {
+        // the exact pass with the carry and clamped ends
+        runK = XK; runKM = XKM; cK = cKM = 0;
+        for (int j = 0; j < nv; ++j) {
+            const uint32_t s0 = (uint32_t)sm.s[b + j] - bl;
+            const uint32_t e = min((uint32_t)sm.e[b + j] - bl, Er), s = min(s0, e);
             const uint32_t loKM = max(runKM, s);
             runKM = max(runKM, e);
             cKM += runKM - loKM;
-            if ((kmask >> j) & 1u) {
+            if (sm.k[b + j] == 0) {
                 const uint32_t loK = max(runK, s);
                 runK = max(runK, e);
                 cK += runK - loK;
             }
-            ps = s0;
+        }
+    } else if (need) {
+        // carry correction over the prefix the carry reaches (no end exceeds E here)
+        uint32_t rK = 0, rKM = 0;
+        for (int j = 0; j < nv && (rKM < XKM || rK < XK); ++j) {
+            const uint32_t s0 = (uint32_t)sm.s[b + j] - bl, e = (uint32_t)sm.e[b + j] - bl, s = min(s0, e);
+            if (rKM < XKM) {
+                const uint32_t lo = max(rKM, s);
+                cKM -= (max(rKM, e) - lo) - (max(XKM, e) - max(XKM, s));
+            }
+            rKM = max(rKM, e);
+            if (sm.k[b + j] == 0) {
+                if (rK < XK) {
+                    const uint32_t lo = max(rK, s);
+                    cK -= (max(rK, e) - lo) - (max(XK, e) - max(XK, s));
+                }
+                rK = max(rK, e);
+            }
         }
     }
+    rare = rare || bad;
     if (rare) rescan<true>(p, sm, c, tc.st, b, nv, 0, E, (p.mode == kReport || p.mode == kValidate) && p.n >= 1, gi0);
     ph.add(ph.b);
     // one piece for the whole tile: warp reductions, one RED per field per warp
     const u64 sK = warp_sum32(cK), sKM = warp_sum32(cKM);
-    const uint32_t mx = __reduce_max_sync(0xffffffffu, nv > 0 ? runKM : 0u);
+    const uint32_t mx = __reduce_max_sync(0xffffffffu, nv > 0 ? min(runKM, Er) : 0u);
     if (lane == 0 && r0 >= 0 && r0 < p.dev_ids) {
         if (sK) red_add(p.d_k + r0, sK);
         if (sKM) red_add(p.d_km + r0, sKM);
@@ -1195,12 +1290,36 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
     return true;
 }
 
+#ifdef HB_GENERAL_NOINLINE
+#define DEV_GENERAL_ATTR __device__ __noinline__
+#else
+#define DEV_GENERAL_ATTR __device__ __forceinline__
+#endif
+DEV_GENERAL_ATTR void dev_general(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
+                                  u64 &E_cache, bool &E_known, bool &signalled, int &k, Phases &ph);
+
 __device__ __forceinline__ void dev_compute(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
-                                            u64 &E_cache, bool &E_known, bool &signalled, int &k, Phases &ph)
+                                            u64 &E_cache, bool &E_known, bool &signalled, int &k, bool &one_pass,
+                                            Phases &ph)
 {
-    if (tc.cnt > 0 && sm.r[0] == sm.r[tc.cnt - 1] &&
-        dev_single(p, sm, c, tc, tid, E_cache, E_known, signalled, k, ph))
-        return;
+    if (tc.cnt > 0 && sm.r[0] == sm.r[tc.cnt - 1]) {
+#if HB_DEV_SCHED == 0
+        const bool done = dev_single<false>(p, sm, c, tc, tid, E_cache, E_known, signalled, k, one_pass, ph);
+#elif HB_DEV_SCHED == 1
+        const bool done = dev_single<true>(p, sm, c, tc, tid, E_cache, E_known, signalled, k, one_pass, ph);
+#else
+        const bool done = one_pass ? dev_single<true>(p, sm, c, tc, tid, E_cache, E_known, signalled, k, one_pass, ph)
+                                   : dev_single<false>(p, sm, c, tc, tid, E_cache, E_known, signalled, k, one_pass, ph);
+#endif
+        if (done) return;
+    }
+    dev_general(p, sm, c, tc, tid, E_cache, E_known, signalled, k, ph);
+}
+
+// tiles holding several devices (or leaving the 2^32 window): segmented scans, 64-bit fallback
+DEV_GENERAL_ATTR void dev_general(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
+                                  u64 &E_cache, bool &E_known, bool &signalled, int &k, Phases &ph)
+{
     ph.mark();
     const int warp = tid >> 5, lane = tid & 31;
     const int b = tid * kItems;
@@ -1505,7 +1624,7 @@ __global__ void __launch_bounds__(kThreads, 1) analyze_kernel(const __grid_const
         // ---------------- compute warps ----------------
         PROF_DECL(ca); PROF_DECL(cb); PROF_DECL(cn);
         Phases phs;
-        bool signalled = false;
+        bool signalled = false, one_pass = true;
         int k = 0;
         for (int it = 0;; ++it) {
             const int st = it % kStages;
@@ -1522,7 +1641,7 @@ __global__ void __launch_bounds__(kThreads, 1) analyze_kernel(const __grid_const
             tc.gbase = tc.lt * kTile;
             t0 = PROF_NOW();
             if (!dev) host_compute(p, stages[st], c, tc, tid, phs);
-            else dev_compute(p, stages[st], c, tc, tid, E_cache, E_known, signalled, k, phs);
+            else dev_compute(p, stages[st], c, tc, tid, E_cache, E_known, signalled, k, one_pass, phs);
 #ifdef HB_PROF
             if (dev) ++phs.dn; else ++phs.hn;
 #endif
@@ -1544,7 +1663,7 @@ __global__ void __launch_bounds__(kThreads, 1) analyze_kernel(const __grid_const
             unsigned long long *o = hb_prof_buf + blockIdx.x * kProfSlots;
             o[0] = ca; o[1] = cb; o[2] = cn;
             o[3] = phs.a; o[4] = phs.bar; o[5] = phs.b; o[6] = phs.emit;
-            o[16] = phs.hb; o[17] = phs.hemit; o[18] = phs.hn; o[19] = phs.dn; o[20] = phs.hn2;
+            o[16] = phs.hb; o[17] = phs.hemit; o[18] = phs.hn; o[19] = phs.dn; o[20] = phs.hn2; o[21] = phs.mg; o[22] = phs.nd;
         }
 #endif
     }

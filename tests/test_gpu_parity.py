@@ -241,3 +241,42 @@ def test_repeated_calls_are_deterministic_and_self_cleaning():
     for _ in range(5):
         again, _ = _engine_vs_oracle(h, d, 8, 8)
         assert np.array_equal(first.dev_sum, again.dev_sum)
+
+
+@pytest.mark.parametrize("k", [20_000, 5_281, 3])
+def test_device_start_outside_the_tile_window(k):
+    """A malformed last record (start > end) whose START lies 2^32 ns past its
+    predecessor's while its end stays inside the tile's 2^32 window: tile-relative
+    32-bit values would show a well-ordered, positive-length record."""
+    rng = np.random.default_rng(21)
+    n, m = 1, 1
+    h = _host_chain(rng, n, np.array([3000]))
+    base = np.uint64(10 ** 12)
+    s = base + np.sort(rng.integers(0, 2 ** 31, size=k, dtype=np.uint64))
+    e = s + rng.integers(1, 5000, size=k, dtype=np.uint64)
+    s[-1] = s[-2] + np.uint64(2 ** 32 + 1)
+    e[-1] = s[-2] + np.uint64(1000)
+    d = (s, e, np.zeros(k, np.int32), rng.integers(0, 2, size=k, dtype=np.uint8))
+    he = h[1] + base
+    he[-1] += np.uint64(2 ** 34)                 # E after every device end
+    got, ref = _engine_vs_oracle((h[0] + base, he, h[2], h[3]), d, n, m, N.MODE_VALIDATE)
+    assert ref.counts[4] == 1 and got.counts[4] == 1 and ref.counts[3] == 0
+
+
+@pytest.mark.parametrize("depth", [2, 8, 64])
+def test_device_carry_correction_on_overlapping_streams(depth):
+    """Overlapping device streams (arrival process): most threads' first records start
+    before the running max carried in from earlier threads of the tile."""
+    rng = np.random.default_rng(depth)
+    n, m = 4, 4
+    h = _host_chain(rng, n, np.array([20_000] * n))
+    counts = np.array([60_000] * m)
+    res = np.repeat(np.arange(m, dtype=np.int32), counts)
+    gaps = rng.integers(0, 40, size=res.size).astype(np.uint64)
+    start = np.concatenate([np.cumsum(gaps[o:o + c]) for o, c in zip(np.r_[0, np.cumsum(counts)[:-1]], counts)])
+    dur = rng.integers(1, 40 * depth, size=res.size).astype(np.uint64)
+    d = _canonical(start.astype(np.uint64), start.astype(np.uint64) + dur, res,
+                   rng.integers(0, 2, size=res.size, dtype=np.uint8), False)
+    _engine_vs_oracle(h, d, n, m)
+    for el in (int(h[1].max() // 3) + 1, int(d[1].max()) + 10):
+        _engine_vs_oracle(h, d, n, m, N.MODE_SUMMARIZE_DEVICE, el)

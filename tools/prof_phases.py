@@ -26,6 +26,7 @@ names = {0: ("c.wait_full", 2), 1: ("c.compute", 2), 16: ("host.loop+devpub", 18
          8: ("tma.wait_empty", 12), 9: ("tma.produce", 12), 10: ("epi.work", 19), 11: ("epi.wait_info", 19)}
 print(f"{cfg.name}: kernel {f.kernel_ms:.3f} ms, CTAs {P.shape[0]}, tiles/CTA {P[:, 2].mean():.1f}")
 print(f"  host tiles/CTA {P[:, 18].mean():.1f}, device tiles/CTA {P[:, 19].mean():.1f}")
+print(f"  single-segment device tiles run in one pass (warp 0): {P[:, 21].mean():.1f}/CTA, needing a carry fix: {P[:, 22].mean():.1f}/CTA")
 for i, (nm, den) in names.items():
     per = P[:, i].astype(float) / np.maximum(P[:, den], 1)
     print(f"  {nm:14s} mean {per.mean():9.0f} cyc/tile   p10 {np.percentile(per, 10):9.0f}  p90 {np.percentile(per, 90):9.0f}")
