@@ -378,25 +378,38 @@ __global__ void __launch_bounds__(256) rd_runagg(const __grid_constant__ RegPara
     const int64_t warps = (int64_t)gridDim.x * 8;
     for (int64_t t = (blockIdx.x * 256ll + threadIdx.x) >> 5; t < p.tiles; t += warps) {
         const int64_t b = t * kDTile, e = umin((u64)(b + kDTile), (u64)p.dn);
+        // one pass, fixed trip (loads in flight): per lane the max ends over the tile, over
+        // the tile's first device, and the tile's last segment start
+        const int32_t r0 = __ldg(p.dr + b);
         int64_t last = -1;
-        for (int64_t i = b + lane; i < e; i += 32)
-            if (i == 0 || __ldg(p.dr + i) != __ldg(p.dr + i - 1)) last = i;
+        u64 mk = 0, mkm = 0, e0 = 0;
+#pragma unroll 9
+        for (int q = 0; q < kDTile / 32; ++q) {
+            const int64_t i = b + q * 32 + lane;
+            if (i < e) {
+                const int32_t r = __ldg(p.dr + i);
+                const u64 en = __ldg(p.de + i);
+                const bool kern = __ldg(p.dk + i) == 0;
+                if (i == 0 || r != __ldg(p.dr + i - 1)) last = i;
+                mkm = umax(mkm, en);
+                if (kern) mk = umax(mk, en);
+                if (r == r0) e0 = umax(e0, en);
+            }
+        }
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) {
             const int64_t o = __shfl_xor_sync(0xffffffffu, last, d);
             last = o > last ? o : last;
         }
-        u64 mk = 0, mkm = 0;
-        for (int64_t i = (last < 0 ? b : last) + lane; i < e; i += 32) {
-            const u64 en = __ldg(p.de + i);
-            mkm = umax(mkm, en);
-            if (__ldg(p.dk + i) == 0) mk = umax(mk, en);
+        if (last >= 0) {
+            // a device starts in the tile (rare): the aggregate covers its last segment only
+            mk = 0; mkm = 0;
+            for (int64_t i = last + lane; i < e; i += 32) {
+                const u64 en = __ldg(p.de + i);
+                mkm = umax(mkm, en);
+                if (__ldg(p.dk + i) == 0) mk = umax(mk, en);
+            }
         }
-        // max end of the tile's FIRST device (its owner's offload records get staged by rd_sums)
-        const int32_t r0 = __ldg(p.dr + b);
-        u64 e0 = 0;
-        for (int64_t i = b + lane; i < e; i += 32)
-            if (__ldg(p.dr + i) == r0) e0 = umax(e0, __ldg(p.de + i));
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) {
             mk = umax(mk, __shfl_xor_sync(0xffffffffu, mk, d));
@@ -549,11 +562,15 @@ __global__ void __launch_bounds__(kDT) rd_sums(const __grid_constant__ RegParams
         const int64_t base = t * kDTile;
         const int cnt = (int)umin((u64)kDTile, (u64)(p.dn - base));
         __syncthreads();
-        for (int i = tid; i < cnt; i += kDT) {
-            T.s[i] = __ldcs(p.ds + base + i);
-            T.e[i] = __ldcs(p.de + base + i);
-            T.r[i] = __ldcs(p.dr + base + i);
-            T.k[i] = __ldcs(p.dk + base + i);
+#pragma unroll
+        for (int k = 0; k < kDI; ++k) {   // every load of the tile in flight at once
+            const int i = tid + k * kDT;
+            if (i < cnt) {
+                T.s[i] = __ldcs(p.ds + base + i);
+                T.e[i] = __ldcs(p.de + base + i);
+                T.r[i] = __ldcs(p.dr + base + i);
+                T.k[i] = __ldcs(p.dk + base + i);
+            }
         }
         const int32_t prev_r = base > 0 ? __ldg(p.dr + base - 1) : INT_MIN;
         __syncthreads();
