@@ -261,13 +261,20 @@ def run_engine(args, world, rank, local):
                                                           dt.d_start, dt.d_end, dt.d_res, dt.d_kind)),
                          dt.n, dt.m)
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    f = analyze_host_columns(pinned, stream=stream.cuda_stream, device=local, sort_if_needed=args.shuffle)
+    # canonical (grouped) records travel as CSR: start, end, kind + per-resource offsets
+    # (heteff_analyze_host_csr, 17 B/interval); a shuffled device side needs its res column
+    csr = None
+    if not args.shuffle:
+        csr = tuple(np.concatenate([[0], np.cumsum(np.bincount(r.numpy(), minlength=k))]).astype(np.int64)
+                    for r, k in ((pinned.h_res, dt.n), (pinned.d_res, dt.m)))
+    f = analyze_host_columns(pinned, stream=stream.cuda_stream, device=local, sort_if_needed=args.shuffle, csr=csr)
     if not kernel_ms:   # region / multi-GPU steps: the one-launch analysis kernel's time on this shard
         kernel_ms.append(analyze_device(dt, N.MODE_REPORT, stream=stream.cuda_stream, device=local).kernel_ms)
     sync()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        fe = analyze_host_columns(pinned, stream=stream.cuda_stream, device=local, sort_if_needed=args.shuffle)
+        fe = analyze_host_columns(pinned, stream=stream.cuda_stream, device=local, sort_if_needed=args.shuffle,
+                                  csr=csr)
         if dist:
             fe = combine_shards(fe, dt, dist, local, stream.cuda_stream, per, per * cfg.gpus_per_rank)
     sync()
@@ -281,7 +288,8 @@ def run_engine(args, world, rank, local):
         # e2e of a region step is not separately staged from host buffers; it is
         # the compute_report path (the regions' inputs are the same columns)
         pass
-    h2d = intervals_local * BYTES_PER_INTERVAL
+    h2d = intervals_local * BYTES_PER_INTERVAL if csr is None else \
+        intervals_local * (BYTES_PER_INTERVAL - 4) + 8 * (dt.n + dt.m + 2)
     d2h = 160 + (dt.n + dt.m) * 32
 
     if rank != 0:
@@ -300,7 +308,9 @@ def run_engine(args, world, rank, local):
                    "ranks": cfg.n_ranks, "devices": cfg.n_devices, "parallelism": f"dp{world} (rank-sharded)",
                    "l2": "inputs larger than L2 (21 B x intervals >> 126 MB)"},
         "e2e": {"value": intervals_total / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                "input": "pinned host SoA, res as CSR offsets (heteff_analyze_host_csr)" if csr is not None
+                else "pinned host SoA (heteff_analyze_host)"},
         "gpu_launches": args.steps * launches_per_step,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_source": peak_kind,

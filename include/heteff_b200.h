@@ -165,6 +165,17 @@ int heteff_analyze(heteff_ctx *ctx, const heteff_trace *trace, const heteff_opti
 int heteff_analyze_host(heteff_ctx *ctx, const heteff_trace *trace, const heteff_options *opt,
                         heteff_result *result, const heteff_outputs *out, void *stream);
 
+/* heteff_analyze_host with the res columns given as CSR offsets instead: records
+   [seg[r], seg[r+1]) have dense id r (seg[0] = 0, non-decreasing, seg[ids] = count;
+   host_seg has host_ids + 1 entries, dev_seg dev_ids + 1).  trace->host.res /
+   trace->dev.res are ignored; the ids are expanded on the device, so 4 bytes per
+   record less cross PCIe ("SoA arrays plus CSR offsets").
+   Replaces the same reference entry points as heteff_analyze (compute_report,
+   metrics.py:125-154, and the stage functions). */
+int heteff_analyze_host_csr(heteff_ctx *ctx, const heteff_trace *trace, const int64_t *host_seg,
+                            const int64_t *dev_seg, const heteff_options *opt, heteff_result *result,
+                            const heteff_outputs *out, void *stream);
+
 /* K3: stable GPU radix sort of one record set (device memory) into the canonical
  * order the analysis expects -- grouped by res ascending, start ascending within
  * a resource, ties kept in input order.  Replaces the canonical sort of

@@ -105,7 +105,7 @@ class GenSide(C.Structure):
 #: every symbol include/heteff_b200.h declares
 EXPORTED = (
     "heteff_abi_version", "heteff_create", "heteff_destroy", "heteff_last_error",
-    "heteff_analyze", "heteff_analyze_host", "heteff_overlap_covers",
+    "heteff_analyze", "heteff_analyze_host", "heteff_analyze_host_csr", "heteff_overlap_covers",
     "heteff_host_metrics", "heteff_device_metrics", "heteff_generate", "heteff_prof_read",
     "heteff_sort_records", "heteff_analyze_regions",
     "heteff_flatten", "heteff_subtract", "heteff_intersect", "heteff_total_duration",
@@ -136,6 +136,9 @@ def load() -> C.CDLL:
         f = getattr(lib, name)
         f.restype = C.c_int
         f.argtypes = [_p, C.POINTER(TraceABI), C.POINTER(Options), C.POINTER(Result), C.POINTER(Outputs), _p]
+    lib.heteff_analyze_host_csr.restype = C.c_int
+    lib.heteff_analyze_host_csr.argtypes = [_p, C.POINTER(TraceABI), _p, _p, C.POINTER(Options), C.POINTER(Result),
+                                            C.POINTER(Outputs), _p]
     lib.heteff_overlap_covers.restype = C.c_int
     lib.heteff_overlap_covers.argtypes = [_p, C.POINTER(TraceABI), C.c_int, _p, C.c_int64, _p, _p]
     for name in ("heteff_host_metrics", "heteff_device_metrics"):

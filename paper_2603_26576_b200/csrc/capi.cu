@@ -679,8 +679,19 @@ int heteff_analyze(heteff_ctx *ctx, const heteff_trace *trace, const heteff_opti
 }
 
 // stage host columns into the context's device buffer, then analyze
-int heteff_analyze_host(heteff_ctx *ctx, const heteff_trace *trace, const heteff_options *opt, heteff_result *result,
-                        const heteff_outputs *out, void *stream)
+// CSR offsets of one record set: seg[0] = 0, non-decreasing, seg[ids] = count
+static bool seg_ok(const int64_t *seg, int32_t ids, int64_t count)
+{
+    if (!seg || ids < 0 || seg[0] != 0 || seg[ids] != count) return false;
+    for (int32_t r = 0; r < ids; ++r)
+        if (seg[r + 1] < seg[r]) return false;
+    return true;
+}
+
+// host buffers -> staging (H2D on the stream) -> run_analysis.  With CSR offsets
+// (hseg / dseg non-null) the res columns are not copied but expanded on the device.
+static int analyze_host_impl(heteff_ctx *ctx, const heteff_trace *trace, const int64_t *hseg, const int64_t *dseg,
+                             const heteff_options *opt, heteff_result *result, const heteff_outputs *out, void *stream)
 {
     if (!ctx || !trace) return fail(ctx, HETEFF_BAD_ARG, "null argument");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -691,7 +702,9 @@ int heteff_analyze_host(heteff_ctx *ctx, const heteff_trace *trace, const heteff
     const size_t db8 = up((size_t)dn * 8), db4 = up((size_t)dn * 4), db1 = up((size_t)dn);
     const size_t hd = up((size_t)(trace->host_decl ? trace->host_ids : 0) * 4);
     const size_t dd = up((size_t)(trace->dev_decl ? trace->dev_ids : 0) * 4);
-    const size_t total = 2 * hb8 + hb4 + hb1 + 2 * db8 + db4 + db1 + hd + dd;
+    const size_t hs8 = hseg ? up(((size_t)trace->host_ids + 1) * 8) : 0;
+    const size_t ds8 = dseg ? up(((size_t)trace->dev_ids + 1) * 8) : 0;
+    const size_t total = 2 * hb8 + hb4 + hb1 + 2 * db8 + db4 + db1 + hd + dd + hs8 + ds8;
     CK(ensure(ctx->stage, total, false), "alloc staging");
     uint8_t *b = static_cast<uint8_t *>(ctx->stage.p);
     heteff_trace d = *trace;
@@ -704,11 +717,11 @@ int heteff_analyze_host(heteff_ctx *ctx, const heteff_trace *trace, const heteff
     };
     d.host.start = static_cast<const uint64_t *>(put(trace->host.start, (size_t)hn * 8, hb8));
     d.host.end = static_cast<const uint64_t *>(put(trace->host.end, (size_t)hn * 8, hb8));
-    d.host.res = static_cast<const int32_t *>(put(trace->host.res, (size_t)hn * 4, hb4));
+    d.host.res = static_cast<const int32_t *>(put(hseg ? nullptr : trace->host.res, (size_t)hn * 4, hb4));
     d.host.kind = static_cast<const uint8_t *>(put(trace->host.kind, (size_t)hn, hb1));
     d.dev.start = static_cast<const uint64_t *>(put(trace->dev.start, (size_t)dn * 8, db8));
     d.dev.end = static_cast<const uint64_t *>(put(trace->dev.end, (size_t)dn * 8, db8));
-    d.dev.res = static_cast<const int32_t *>(put(trace->dev.res, (size_t)dn * 4, db4));
+    d.dev.res = static_cast<const int32_t *>(put(dseg ? nullptr : trace->dev.res, (size_t)dn * 4, db4));
     d.dev.kind = static_cast<const uint8_t *>(put(trace->dev.kind, (size_t)dn, db1));
     d.host_decl = trace->host_decl
                       ? static_cast<const int32_t *>(put(trace->host_decl, (size_t)trace->host_ids * 4, hd))
@@ -716,8 +729,32 @@ int heteff_analyze_host(heteff_ctx *ctx, const heteff_trace *trace, const heteff
     d.dev_decl = trace->dev_decl
                      ? static_cast<const int32_t *>(put(trace->dev_decl, (size_t)trace->dev_ids * 4, dd))
                      : nullptr;
+    if (hseg) {
+        const int64_t *g = static_cast<const int64_t *>(put(hseg, ((size_t)trace->host_ids + 1) * 8, hs8));
+        CK(hb::launch_expand_res(g, trace->host_ids, hn, const_cast<int32_t *>(d.host.res), s), "expand host res");
+    }
+    if (dseg) {
+        const int64_t *g = static_cast<const int64_t *>(put(dseg, ((size_t)trace->dev_ids + 1) * 8, ds8));
+        CK(hb::launch_expand_res(g, trace->dev_ids, dn, const_cast<int32_t *>(d.dev.res), s), "expand dev res");
+    }
     CK(cudaGetLastError(), "h2d");
     return run_analysis(ctx, &d, opt, result, out, s);
+}
+
+int heteff_analyze_host(heteff_ctx *ctx, const heteff_trace *trace, const heteff_options *opt, heteff_result *result,
+                        const heteff_outputs *out, void *stream)
+{
+    return analyze_host_impl(ctx, trace, nullptr, nullptr, opt, result, out, stream);
+}
+
+int heteff_analyze_host_csr(heteff_ctx *ctx, const heteff_trace *trace, const int64_t *host_seg,
+                            const int64_t *dev_seg, const heteff_options *opt, heteff_result *result,
+                            const heteff_outputs *out, void *stream)
+{
+    if (!trace) return fail(ctx, HETEFF_BAD_ARG, "null argument");
+    if (!seg_ok(host_seg, trace->host_ids, trace->host.count) || !seg_ok(dev_seg, trace->dev_ids, trace->dev.count))
+        return fail(ctx, HETEFF_BAD_ARG, "CSR offsets must start at 0, never decrease and end at the record count");
+    return analyze_host_impl(ctx, trace, host_seg, dev_seg, opt, result, out, stream);
 }
 
 int heteff_overlap_covers(heteff_ctx *ctx, const heteff_trace *trace, int host_columns_on_host,

@@ -1776,6 +1776,43 @@ __global__ void __launch_bounds__(kOvlThreads) ovl_detect_kernel(const __grid_co
     }
 }
 
+// CSR offsets -> per-record dense ids (the res column of a CSR input): each block
+// takes a chunk of records, finds the groups it touches once, then every record
+// binary-searches only those (usually one) -- coalesced writes, no per-record
+// search over the whole offset table.  Record i belongs to the last group r with
+// seg[r] <= i (empty groups share an offset with the next one).
+constexpr int kExpandChunk = 8192;
+__device__ __forceinline__ int32_t last_le(const int64_t *seg, int32_t lo, int32_t hi, int64_t i)
+{
+    while (lo < hi) {   // last r in [lo, hi] with seg[r] <= i (seg[lo] <= i holds)
+        const int32_t mid = lo + ((hi - lo + 1) >> 1);
+        if (__ldg(seg + mid) <= i) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(256) expand_res_kernel(const int64_t *seg, int32_t ids, int64_t n, int32_t *res)
+{
+    __shared__ int32_t s_lo, s_hi;
+    const int64_t c0 = (int64_t)blockIdx.x * kExpandChunk;
+    const int64_t c1 = c0 + kExpandChunk < n ? c0 + kExpandChunk : n;
+    if (threadIdx.x == 0) {
+        s_lo = last_le(seg, 0, ids - 1, c0);
+        s_hi = last_le(seg, s_lo, ids - 1, c1 - 1);
+    }
+    __syncthreads();
+    const int32_t lo = s_lo, hi = s_hi;
+    for (int64_t i = c0 + threadIdx.x; i < c1; i += 256) res[i] = lo == hi ? lo : last_le(seg, lo, hi, i);
+}
+
+cudaError_t launch_expand_res(const int64_t *seg, int32_t ids, int64_t n, int32_t *res, cudaStream_t s)
+{
+    if (n <= 0 || ids <= 0) return cudaSuccess;
+    expand_res_kernel<<<(unsigned)((n + kExpandChunk - 1) / kExpandChunk), 256, 0, s>>>(seg, ids, n, res);
+    return cudaGetLastError();
+}
+
 __global__ void __launch_bounds__(kThreads) finalize_kernel(const __grid_constant__ Params p)
 {
     __shared__ u128 scratch[40];

@@ -104,6 +104,8 @@ int analyze_grid(int device);
 cudaError_t launch_analyze(const Params &p, int grid, cudaStream_t s);
 cudaError_t launch_metrics(const u64 *summaries, int32_t k, u64 elapsed, int host_side, ResultDev *res,
                            cudaStream_t s);
+// CSR offsets [ids + 1] -> res[n] (dense id of every record)
+cudaError_t launch_expand_res(const int64_t *seg, int32_t ids, int64_t n, int32_t *res, cudaStream_t s);
 cudaError_t launch_merge(const void *blocks, int32_t world, size_t block_bytes, int32_t n_max, int32_t m_max,
                          const int32_t *n_of, const int32_t *m_of, void *out, const u64 *E_global, cudaStream_t s);
 // error path: exact host-overlap findings (only when ovl_suspect), then finalize

@@ -220,8 +220,12 @@ class AnalysisPlan:
 
 
 def analyze_host_columns(dt: DeviceTrace, mode: int = N.MODE_REPORT, stream: int | None = None,
-                         device: int | None = None, sort_if_needed: bool = False) -> Findings:
-    """Same as :func:`analyze_device` but the columns are HOST tensors (pinned); H2D inside."""
+                         device: int | None = None, sort_if_needed: bool = False, csr=None) -> Findings:
+    """Same as :func:`analyze_device` but the columns are HOST tensors (pinned); H2D inside.
+
+    ``csr=(host_seg, dev_seg)`` (int64 host arrays / tensors of ``ids + 1`` offsets) sends
+    the resource ids as CSR offsets instead of the res columns (``heteff_analyze_host_csr``:
+    17 instead of 21 bytes per interval over PCIe; ``dt``'s res columns are not read)."""
     ctx = N.context(device)
     lib = N.load()
     t = device_trace_abi(dt)
@@ -230,7 +234,12 @@ def analyze_host_columns(dt: DeviceTrace, mode: int = N.MODE_REPORT, stream: int
     out = N.Outputs(_ptr(host_sum), _ptr(dev_sum), (C.c_void_p * N.NUM_LISTS)())
     opt = N.Options(mode, N.FLAG_SORT_IF_NEEDED if sort_if_needed else 0, 0, 0)
     res = N.Result()
-    rc = lib.heteff_analyze_host(ctx, C.byref(t), C.byref(opt), C.byref(res), C.byref(out), stream)
+    if csr is not None:
+        hseg, dseg = (np.ascontiguousarray(x.numpy() if hasattr(x, "numpy") else x, dtype=np.int64) for x in csr)
+        rc = lib.heteff_analyze_host_csr(ctx, C.byref(t), _ptr(hseg), _ptr(dseg), C.byref(opt), C.byref(res),
+                                         C.byref(out), stream)
+    else:
+        rc = lib.heteff_analyze_host(ctx, C.byref(t), C.byref(opt), C.byref(res), C.byref(out), stream)
     _check(ctx, rc)
     return _findings(res, host_sum[: dt.n], dev_sum[: dt.m], [])
 

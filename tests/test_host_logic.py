@@ -116,3 +116,18 @@ def test_engine_raises_without_gpu():
     t = hb.Trace(host_processes=(0,), host_records=(hb.HostRecord(0, hb.HostState.USEFUL, hb.Interval(0, 5)),))
     with pytest.raises(Exception):
         hb.compute_report(t)
+
+
+@pytest.mark.parametrize("seg", [[1, 5, 10], [0, 5, 9], [0, 6, 5, 10]])
+def test_csr_offsets_are_checked_before_any_device_work(seg):
+    """heteff_analyze_host_csr rejects malformed CSR offsets with BAD_ARG (no GPU needed)."""
+    from paper_2603_26576_b200 import _native as N
+
+    lib = N.load()
+    ids = len(seg) - 1
+    t = N.TraceABI(N.Records(None, None, None, None, 10), N.Records(None, None, None, None, 0),
+                   ids, 0, None, None, ids, 0, 0)
+    hseg = np.array(seg, dtype=np.int64)
+    dseg = np.zeros(1, dtype=np.int64)
+    rc = lib.heteff_analyze_host_csr(None, C.byref(t), hseg.ctypes.data, dseg.ctypes.data, None, None, None, None)
+    assert rc == N.BAD_ARG
