@@ -42,13 +42,14 @@ constexpr int kT = HB_SORT_T;           // threads per CTA (512: 2 CTAs / SM)
 constexpr int kW = kT / 32;
 constexpr int kI = HB_SORT_I;           // keys per thread
 constexpr int kTileKeys = kT * kI;      // 7680 keys per tile
-constexpr int kBins = 256;              // <= 8-bit digits
+constexpr int kDMax = 8;                 // max bits per digit (9-bit digits / 4 passes measured slower:
+constexpr int kBins = 1 << kDMax;        // shorter digit runs scatter the writes)
 
 struct Range {
     u64 smin, smax;
     unsigned int rmin, rmax;            // flipped domain
     unsigned int start_desc;            // some start is below its predecessor's
-    unsigned int pad;
+    unsigned int kind_wide;             // some kind code > 3: not packable into the index
 };
 
 __device__ __forceinline__ unsigned int flip(int32_t r) { return (unsigned int)r ^ 0x80000000u; }
@@ -64,6 +65,7 @@ __global__ void range_init(Range *g)
     g->rmin = 0xffffffffu;
     g->rmax = 0;
     g->start_desc = 0;
+    g->kind_wide = 0;
 }
 
 __global__ void __launch_bounds__(512) range_kernel(const u64 *__restrict__ S, const int32_t *__restrict__ R,
@@ -110,6 +112,7 @@ struct KeyPlan {
     int res_only;      // 1: input already start-sorted: one stable sort by r' suffices
     int passes;        // digit passes of this stage
     int dbits;         // bits per digit
+    int packk;         // narrow keys, n <= 2^30: the kind rides in the index's top two bits
 };
 
 __device__ __forceinline__ u64 make_key(const KeyPlan &kp, u64 s, int32_t r)
@@ -120,12 +123,25 @@ __device__ __forceinline__ u64 make_key(const KeyPlan &kp, u64 s, int32_t r)
     return ((u64)(flip(r) - kp.rmin) << kp.bt) | so;
 }
 
-__global__ void __launch_bounds__(512) build_keys(const u64 *__restrict__ S, const int32_t *__restrict__ R, int64_t n,
-                                                  KeyPlan kp, u64 *__restrict__ K, uint32_t *__restrict__ V)
+// packk: V = index | kind << 30, so the final gather fetches the end column alone
+// (one random 32-byte sector per record instead of two); kinds > 3 raise kind_wide
+// and the finish gathers them instead
+constexpr uint32_t kIdxMask = 0x3fffffffu;
+
+__global__ void __launch_bounds__(512) build_keys(const u64 *__restrict__ S, const int32_t *__restrict__ R,
+                                                  const uint8_t *__restrict__ KD, int64_t n, KeyPlan kp,
+                                                  u64 *__restrict__ K, uint32_t *__restrict__ V,
+                                                  unsigned int *__restrict__ kind_wide)
 {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         K[i] = make_key(kp, __ldcs(S + i), __ldcs(R + i));
-        V[i] = (uint32_t)i;
+        uint32_t v = (uint32_t)i;
+        if (kp.packk) {
+            const uint32_t k = __ldcs(KD + i);
+            if (k > 3u) atomicOr(kind_wide, 1u);
+            v |= (k & 3u) << 30;
+        }
+        V[i] = v;
     }
 }
 
@@ -289,8 +305,8 @@ __global__ void __launch_bounds__(kScanT) scan_blocks(uint32_t *c, int64_t m, co
 __device__ __forceinline__ uint32_t peers_of(uint32_t d, int dbits, uint32_t valid_mask)
 {
     uint32_t m = valid_mask;
-#pragma unroll 8
-    for (int b = 0; b < 8; ++b) {
+#pragma unroll
+    for (int b = 0; b < kDMax; ++b) {
         if (b < dbits) {
             const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
             m &= ((d >> b) & 1u) ? bb : ~bb;
@@ -405,19 +421,22 @@ __global__ void __launch_bounds__(kT, (kT <= 512 ? 2 : 1)) downsweep(const u64 *
 // output columns
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(512) finish_narrow(const u64 *__restrict__ K, const uint32_t *__restrict__ V,
-                                                     int64_t n, KeyPlan kp, const u64 *__restrict__ E,
+                                                     int64_t n, KeyPlan kp, const unsigned int *__restrict__ kind_wide,
+                                                     const u64 *__restrict__ E,
                                                      const uint8_t *__restrict__ KD, u64 *__restrict__ os,
                                                      u64 *__restrict__ oe, int32_t *__restrict__ orr,
                                                      uint8_t *__restrict__ ok, int64_t *__restrict__ perm)
 {
     const u64 tmask = kp.bt >= 64 ? ~0ull : ((1ull << kp.bt) - 1);
+    const bool gather_k = !kp.packk || *kind_wide;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const u64 key = __ldcs(K + i);
-        const uint32_t v = __ldcs(V + i);
+        const uint32_t pv = __ldcs(V + i);
+        const uint32_t v = kp.packk ? pv & kIdxMask : pv;
         os[i] = (key & tmask) + kp.smin;
         orr[i] = unflip((kp.bt >= 64 ? 0u : (unsigned int)(key >> kp.bt)) + kp.rmin);
         oe[i] = __ldg(E + v);
-        ok[i] = __ldg(KD + v);
+        ok[i] = gather_k ? __ldg(KD + v) : (uint8_t)(pv >> 30);
         if (perm) perm[i] = v;
     }
 }
@@ -565,6 +584,7 @@ cudaError_t sort_records(const u64 *S, const u64 *E, const int32_t *R, const uin
     // a stable sort by resource alone yields the canonical order
     kp.res_only = rg.start_desc ? 0 : 1;
     kp.wide = (!kp.res_only && bt + br > 64) ? 1 : 0;
+    kp.packk = (!kp.wide && !kp.res_only && n <= (int64_t)kIdxMask + 1) ? 1 : 0;
     const int stage_bits[2] = {kp.res_only ? br : (kp.wide ? bt : bt + br), kp.wide ? br : 0};
 
     u64 *kin = K0, *kout = K1;
@@ -577,10 +597,10 @@ cudaError_t sort_records(const u64 *S, const u64 *E, const int32_t *R, const uin
     for (int stage = 0; stage < 2; ++stage) {
         const int bits = stage_bits[stage];
         if (stage == 1 && !kp.wide) break;
-        const int passes = bits == 0 ? 0 : (bits + 7) / 8;
+        const int passes = bits == 0 ? 0 : (bits + kDMax - 1) / kDMax;
         kp.passes = passes;
         kp.dbits = passes ? (bits + passes - 1) / passes : 1;
-        if (stage == 0) build_keys<<<grid_for(n, sms), 512, 0, s>>>(S, R, n, kp, kin, vin);
+        if (stage == 0) build_keys<<<grid_for(n, sms), 512, 0, s>>>(S, R, KD, n, kp, kin, vin, &range->kind_wide);
         else build_res_keys<<<grid_for(n, sms), 512, 0, s>>>(R, vin, n, kp, kin);
         for (int p = 0; p < passes; ++p) {
             const int shift = p * kp.dbits;
@@ -612,7 +632,8 @@ cudaError_t sort_records(const u64 *S, const u64 *E, const int32_t *R, const uin
     }
     (void)nb;
     if (!kp.wide && !kp.res_only) {
-        finish_narrow<<<grid_for(n, sms), 512, 0, s>>>(kin, vin, n, kp, E, KD, os, oe, orr, ok, perm);
+        finish_narrow<<<grid_for(n, sms), 512, 0, s>>>(kin, vin, n, kp, &range->kind_wide, E, KD, os, oe, orr, ok,
+                                                       perm);
     } else if (carry) {
         finish_payload<<<grid_for(n, sms), 512, 0, s>>>(kin, vin, n, kp, orr, perm);
     } else {

@@ -224,3 +224,13 @@ def test_analysis_plan_repeated_runs_match():
         assert got.status == N.OK and got.elapsed == ref.elapsed
         assert np.array_equal(got.host_sum, ref.host_sum) and np.array_equal(got.dev_sum, ref.dev_sum)
         assert got.host_metrics == ref.host_metrics and got.device_metrics == ref.device_metrics
+
+
+@pytest.mark.parametrize("kmax", [4, 256])
+def test_sort_keeps_kind_codes_that_do_not_fit_the_index(kmax):
+    """Kinds ride in the index's top two bits; codes > 3 (contract violations the
+    analysis reports) must still come out unchanged -- the finish gathers them."""
+    rng = np.random.default_rng(kmax)
+    s, e, r, _ = _random(rng, 3 * TILE + 5, 7, 10 ** 6)
+    k = rng.integers(0, kmax, s.size, dtype=np.uint16).astype(np.uint8)
+    _check_sort(s, e, r, k)
