@@ -50,6 +50,9 @@ struct Range {
     unsigned int rmin, rmax;            // flipped domain
     unsigned int start_desc;            // some start is below its predecessor's
     unsigned int kind_wide;             // some kind code > 3: not packable into the index
+    u64 dmax;                           // max end - start
+    unsigned int neg;                   // some end < start (malformed)
+    unsigned int pad;
 };
 
 __device__ __forceinline__ unsigned int flip(int32_t r) { return (unsigned int)r ^ 0x80000000u; }
@@ -66,34 +69,42 @@ __global__ void range_init(Range *g)
     g->rmax = 0;
     g->start_desc = 0;
     g->kind_wide = 0;
+    g->dmax = 0;
+    g->neg = 0;
 }
 
-__global__ void __launch_bounds__(512) range_kernel(const u64 *__restrict__ S, const int32_t *__restrict__ R,
-                                                    int64_t n, Range *g)
+__global__ void __launch_bounds__(512) range_kernel(const u64 *__restrict__ S, const u64 *__restrict__ E,
+                                                    const int32_t *__restrict__ R, int64_t n, Range *g)
 {
-    u64 smin = ~0ull, smax = 0;
+    u64 smin = ~0ull, smax = 0, dmax = 0;
     unsigned int rmin = 0xffffffffu, rmax = 0;
-    bool desc = false;
+    bool desc = false, neg = false;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const u64 s = __ldg(S + i);
+        const u64 s = __ldg(S + i), e = __ldcs(E + i);
         if (i > 0) desc = desc || __ldg(S + i - 1) > s;
         const unsigned int r = flip(__ldcs(R + i));
         smin = umin(smin, s);
         smax = umax(smax, s);
         rmin = min(rmin, r);
         rmax = max(rmax, r);
+        neg = neg || e < s;
+        dmax = umax(dmax, e - s);
     }
     // 64-bit warp reductions by shuffles (the kernel is bandwidth-bound)
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
         smin = umin(smin, __shfl_xor_sync(0xffffffffu, smin, d));
         smax = umax(smax, __shfl_xor_sync(0xffffffffu, smax, d));
+        dmax = umax(dmax, __shfl_xor_sync(0xffffffffu, dmax, d));
     }
+    neg = __any_sync(0xffffffffu, neg);
     rmin = __reduce_min_sync(0xffffffffu, rmin);
     rmax = __reduce_max_sync(0xffffffffu, rmax);
     desc = __any_sync(0xffffffffu, desc);
     if ((threadIdx.x & 31) == 0) {
         if (desc) atomicOr(&g->start_desc, 1u);
+        if (neg) atomicOr(&g->neg, 1u);
+        atomicMax(&g->dmax, dmax);
         atomicMin(&g->smin, smin);
         atomicMax(&g->smax, smax);
         atomicMin(&g->rmin, rmin);
@@ -113,6 +124,8 @@ struct KeyPlan {
     int passes;        // digit passes of this stage
     int dbits;         // bits per digit
     int packk;         // narrow keys, n <= 2^30: the kind rides in the index's top two bits
+    int dshift;        // > 0: end - start stashed in key bits [dshift, 64), above every digit pass
+    int br;            // bits of the resource offset
 };
 
 __device__ __forceinline__ u64 make_key(const KeyPlan &kp, u64 s, int32_t r)
@@ -123,18 +136,25 @@ __device__ __forceinline__ u64 make_key(const KeyPlan &kp, u64 s, int32_t r)
     return ((u64)(flip(r) - kp.rmin) << kp.bt) | so;
 }
 
+// durations stashed above the digit passes ride through every pass for free: the
+// finish rebuilds end = start + duration and no random gather is left
+
 // packk: V = index | kind << 30, so the final gather fetches the end column alone
 // (one random 32-byte sector per record instead of two); kinds > 3 raise kind_wide
 // and the finish gathers them instead
 constexpr uint32_t kIdxMask = 0x3fffffffu;
 
-__global__ void __launch_bounds__(512) build_keys(const u64 *__restrict__ S, const int32_t *__restrict__ R,
+__global__ void __launch_bounds__(512) build_keys(const u64 *__restrict__ S, const u64 *__restrict__ E,
+                                                  const int32_t *__restrict__ R,
                                                   const uint8_t *__restrict__ KD, int64_t n, KeyPlan kp,
                                                   u64 *__restrict__ K, uint32_t *__restrict__ V,
                                                   unsigned int *__restrict__ kind_wide)
 {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        K[i] = make_key(kp, __ldcs(S + i), __ldcs(R + i));
+        const u64 si = __ldcs(S + i);
+        u64 key = make_key(kp, si, __ldcs(R + i));
+        if (kp.dshift) key |= (__ldcs(E + i) - si) << kp.dshift;
+        K[i] = key;
         uint32_t v = (uint32_t)i;
         if (kp.packk) {
             const uint32_t k = __ldcs(KD + i);
@@ -433,9 +453,11 @@ __global__ void __launch_bounds__(512) finish_narrow(const u64 *__restrict__ K, 
         const u64 key = __ldcs(K + i);
         const uint32_t pv = __ldcs(V + i);
         const uint32_t v = kp.packk ? pv & kIdxMask : pv;
-        os[i] = (key & tmask) + kp.smin;
-        orr[i] = unflip((kp.bt >= 64 ? 0u : (unsigned int)(key >> kp.bt)) + kp.rmin);
-        oe[i] = __ldg(E + v);
+        const u64 st = (key & tmask) + kp.smin;
+        os[i] = st;
+        const u64 rbits = kp.bt >= 64 ? 0ull : (key >> kp.bt) & ((1ull << kp.br) - 1);
+        orr[i] = unflip((unsigned int)rbits + kp.rmin);
+        oe[i] = kp.dshift ? st + (key >> kp.dshift) : __ldg(E + v);
         ok[i] = gather_k ? __ldg(KD + v) : (uint8_t)(pv >> 30);
         if (perm) perm[i] = v;
     }
@@ -570,7 +592,7 @@ cudaError_t sort_records(const u64 *S, const u64 *E, const int32_t *R, const uin
 
     // 1. key range (one D2H of 32 bytes decides the key layout)
     range_init<<<1, 1, 0, s>>>(range);
-    range_kernel<<<grid_for(n, sms), 512, 0, s>>>(S, R, n, range);
+    range_kernel<<<grid_for(n, sms), 512, 0, s>>>(S, E, R, n, range);
     Range rg;
     if ((e = cudaMemcpyAsync(&rg, range, sizeof(Range), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
@@ -580,6 +602,8 @@ cudaError_t sort_records(const u64 *S, const u64 *E, const int32_t *R, const uin
     kp.smin = rg.smin;
     kp.rmin = rg.rmin;
     kp.bt = bt;
+    kp.br = br;
+    kp.dshift = 0;
     // input already ordered by start (e.g. a globally time-ordered event log):
     // a stable sort by resource alone yields the canonical order
     kp.res_only = rg.start_desc ? 0 : 1;
@@ -600,7 +624,13 @@ cudaError_t sort_records(const u64 *S, const u64 *E, const int32_t *R, const uin
         const int passes = bits == 0 ? 0 : (bits + kDMax - 1) / kDMax;
         kp.passes = passes;
         kp.dbits = passes ? (bits + passes - 1) / passes : 1;
-        if (stage == 0) build_keys<<<grid_for(n, sms), 512, 0, s>>>(S, R, KD, n, kp, kin, vin, &range->kind_wide);
+        if (stage == 0) {
+            // narrow keys: stash end - start above the bits the passes examine when it fits
+            kp.dshift = 0;
+            const int cover = passes * kp.dbits;
+            if (!kp.wide && !kp.res_only && !rg.neg && cover < 64 && bits_of(rg.dmax) <= 64 - cover) kp.dshift = cover;
+            build_keys<<<grid_for(n, sms), 512, 0, s>>>(S, E, R, KD, n, kp, kin, vin, &range->kind_wide);
+        }
         else build_res_keys<<<grid_for(n, sms), 512, 0, s>>>(R, vin, n, kp, kin);
         for (int p = 0; p < passes; ++p) {
             const int shift = p * kp.dbits;

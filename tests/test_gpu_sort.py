@@ -234,3 +234,18 @@ def test_sort_keeps_kind_codes_that_do_not_fit_the_index(kmax):
     s, e, r, _ = _random(rng, 3 * TILE + 5, 7, 10 ** 6)
     k = rng.integers(0, kmax, s.size, dtype=np.uint16).astype(np.uint8)
     _check_sort(s, e, r, k)
+
+
+@pytest.mark.parametrize("case", ["malformed", "huge_duration", "max_duration_that_fits"])
+def test_sort_end_column_with_and_without_the_duration_stash(case):
+    """Durations ride in the key bits above the digit passes when every one fits; a
+    malformed record (end < start) or a too-long duration falls back to the gather."""
+    rng = np.random.default_rng(len(case))
+    s, e, r, k = _random(rng, 2 * TILE + 3, 300, 10 ** 9)
+    if case == "malformed":
+        e[17] = s[17] - np.uint64(1)
+    elif case == "huge_duration":
+        e[5] = s[5] + np.uint64(2 ** 40)
+    else:
+        e[5] = s[5] + np.uint64(2 ** 20)    # 30 + 9 key bits -> 5 passes x 8 = 40 covered, 24 left
+    _check_sort(s, e, r, k)
