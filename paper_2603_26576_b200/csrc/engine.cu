@@ -1187,19 +1187,23 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
     bool fit = true;
     if (lane < kComputeWarps) { wK = c->f_k[tc.st][lane]; wKM = c->f_km[tc.st][lane]; fit = c->f_fit[tc.st][lane] != 0; }
     if (!__all_sync(0xffffffffu, fit)) return false;
-    warp_max_scan2(wK, wKM, lane);
-    const uint32_t tK = __shfl_sync(0xffffffffu, wK, kComputeWarps - 1), tKM = __shfl_sync(0xffffffffu, wKM, kComputeWarps - 1);
-    const uint32_t xwK = __shfl_sync(0xffffffffu, wK, warp > 0 ? warp - 1 : 0);
-    const uint32_t xwKM = __shfl_sync(0xffffffffu, wKM, warp > 0 ? warp - 1 : 0);
+    // the max over earlier warps: one predicated REDUX each, no shuffle scan
+    const uint32_t xwK = __reduce_max_sync(0xffffffffu, lane < warp ? wK : 0u);
+    const uint32_t xwKM = __reduce_max_sync(0xffffffffu, lane < warp ? wKM : 0u);
     uint32_t xK = __shfl_up_sync(0xffffffffu, vK, 1), xKM = __shfl_up_sync(0xffffffffu, vKM, 1);
     if (lane == 0) { xK = 0; xKM = 0; }
-    if (warp > 0) { xK = max(xK, xwK); xKM = max(xKM, xwKM); }
+    xK = max(xK, xwK);
+    xKM = max(xKM, xwKM);
     const bool head = c->has_prev[tc.st] && sm.r[0] == c->prev_res[tc.st];
     ph.add(ph.bar);
-    if (tid == 0) {
-        // tile aggregate (a segment starts here iff the tile does not continue one)
-        publish<2>(!head ? p.d_slotP + 4 * tc.lt : p.d_slotA + 4 * tc.lt, p.epoch, base + tK, base + tKM);
-        if (head) post_info(c, kq, tc.lt, tc.cnt, true, false, base + tK, base + tKM);
+    if (warp == 0) {
+        // tile aggregate (warp 0 only): the max over every warp
+        const uint32_t tK = __reduce_max_sync(0xffffffffu, wK), tKM = __reduce_max_sync(0xffffffffu, wKM);
+        if (lane == 0) {
+            // a segment starts here iff the tile does not continue one
+            publish<2>(!head ? p.d_slotP + 4 * tc.lt : p.d_slotA + 4 * tc.lt, p.epoch, base + tK, base + tKM);
+            if (head) post_info(c, kq, tc.lt, tc.cnt, true, false, base + tK, base + tKM);
+        }
     }
     ph.add(ph.hb);
     const uint32_t Er = E <= base ? 0u : (E - base > 0xffffffffull ? 0xffffffffu : (uint32_t)(E - base));
@@ -1540,7 +1544,10 @@ __device__ void finalize(const Params &p, u128 *scratch, int tid)
 // =========================================================================
 // the kernel
 // =========================================================================
-__global__ void __launch_bounds__(kThreads, 1) analyze_kernel(const __grid_constant__ Params p)
+#ifndef HB_MINB
+#define HB_MINB 1   // resident CTAs per SM the register budget is sized for
+#endif
+__global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid_constant__ Params p)
 {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     StageSmem *stages = reinterpret_cast<StageSmem *>(smem_raw);
