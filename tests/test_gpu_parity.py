@@ -280,3 +280,21 @@ def test_device_carry_correction_on_overlapping_streams(depth):
     _engine_vs_oracle(h, d, n, m)
     for el in (int(h[1].max() // 3) + 1, int(d[1].max()) + 10):
         _engine_vs_oracle(h, d, n, m, N.MODE_SUMMARIZE_DEVICE, el)
+
+
+@pytest.mark.parametrize("offset", [2 ** 64 - 10 ** 9, 2 ** 64 - 2 ** 33 - 12345, 2 ** 32 - 5000])
+def test_timestamps_at_the_top_of_u64_and_across_a_32_bit_boundary(offset):
+    """Records near U64_MAX (the tile-relative 32-bit windows and E sit at the top of
+    the range) and records straddling a 2^32 boundary, through the engine vs the oracle."""
+    rng = np.random.default_rng(offset % 997)
+    n, m = 3, 4
+    h = _host_chain(rng, n, np.array([6000, 9000, 7000]))
+    d = _random_side(rng, m, np.array([8000, 12000, 0, 9000]), host=False, long_frac=0.001,
+                     span=int(h[1].max()))
+    top = np.uint64(offset)
+    hs = (h[0] + top, h[1] + top, h[2], h[3])
+    ds = (d[0] + top, d[1] + top, d[2], d[3])
+    assert int(max(hs[1].max(), ds[1].max())) <= 2 ** 64 - 1
+    got, _ = _engine_vs_oracle(hs, ds, n, m)        # report mode compares the finding lists too
+    assert got.elapsed == int(hs[1].max())
+    _engine_vs_oracle(hs, ds, n, m, N.MODE_SUMMARIZE_DEVICE, int(hs[1].max()) - 1000)
