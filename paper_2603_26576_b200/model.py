@@ -80,6 +80,20 @@ class DeviceDecl:
     owner_rank: int | None = None
 
 
+_HOST_BY_VALUE = tuple(sorted(HostState, key=lambda m: m.value))
+_DEV_BY_VALUE = tuple(sorted(DeviceActivityKind, key=lambda m: m.value))
+
+
+def _already_canonical(records, res_attr, kind_attr, members, stream_attr) -> bool:
+    if len(records) < 2:
+        return True
+    try:
+        from . import _pack
+    except ImportError:
+        return False
+    return _pack.is_canonical(records, res_attr, kind_attr, members, stream_attr)
+
+
 def _canonical_host(rec: HostRecord):
     iv = rec.interval
     return (rec.rank, iv.start, iv.end, rec.state.value)
@@ -110,8 +124,15 @@ class Trace:
         set_ = object.__setattr__
         set_(self, "host_processes", tuple(self.host_processes))
         set_(self, "devices", tuple(self.devices))
-        set_(self, "host_records", tuple(sorted(self.host_records, key=_canonical_host)))
-        set_(self, "device_records", tuple(sorted(self.device_records, key=_canonical_device)))
+        hr, dr = tuple(self.host_records), tuple(self.device_records)
+        # records that already arrive in canonical order (files, time-ordered generators)
+        # skip the key-function sort: one native pass decides it (csrc/pack.c)
+        if not _already_canonical(hr, "rank", "state", _HOST_BY_VALUE, None):
+            hr = tuple(sorted(hr, key=_canonical_host))
+        if not _already_canonical(dr, "device_id", "kind", _DEV_BY_VALUE, "stream"):
+            dr = tuple(sorted(dr, key=_canonical_device))
+        set_(self, "host_records", hr)
+        set_(self, "device_records", dr)
 
     @property
     def n(self) -> int:

@@ -20,6 +20,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+from operator import attrgetter
+
 import numpy as np
 
 from .model import DEVICE_KIND_CODE, HOST_STATE_CODE, U64_MAX, Trace
@@ -99,8 +101,29 @@ def _decl_table(ids, declared) -> tuple[np.ndarray, int]:
     return table, len(first)
 
 
-def _pack_side(records, res_of, code_of, dense, label, res_label):
+try:   # one-pass native packer (csrc/pack.c), built in-tree by __graft_entry__.build()
+    from . import _pack
+except ImportError:   # host-side ingest only: the Python packer below is the same mapping
+    _pack = None
+
+
+def _members(codes: dict) -> tuple:
+    out = [None] * (max(codes.values()) + 1)
+    for member, code in codes.items():
+        out[code] = member
+    return tuple(out)
+
+
+_HOST_MEMBERS = _members(HOST_STATE_CODE)
+_DEV_MEMBERS = _members(DEVICE_KIND_CODE)
+
+
+def _pack_side(records, res_of, code_of, dense, label, res_label, native=None):
     k = len(records)
+    if _pack is not None and native is not None and k:
+        cols = (np.empty(k, np.uint64), np.empty(k, np.uint64), np.empty(k, np.int32), np.empty(k, np.uint8))
+        if _pack.pack_side(records, native[0], native[1], dense, native[2], *cols):
+            return RecordColumns(*cols, None), [], 0
     try:  # fast path: every timestamp is a plain in-range int
         if all(type(r.interval.start) is int and type(r.interval.end) is int for r in records):
             start = np.fromiter((r.interval.start for r in records), dtype=np.uint64, count=k)
@@ -153,16 +176,16 @@ def pack_trace(trace: Trace) -> PackedTrace:
     """Pack a :class:`Trace` into SoA columns in canonical order."""
     hp = trace.host_processes
     dev_decl_ids = [d.device_id for d in trace.devices]
-    host_ids, hdense = _dense(hp, (r.rank for r in trace.host_records))
-    dev_ids, ddense = _dense(dev_decl_ids, (r.device_id for r in trace.device_records))
+    host_ids, hdense = _dense(hp, map(attrgetter("rank"), trace.host_records))
+    dev_ids, ddense = _dense(dev_decl_ids, map(attrgetter("device_id"), trace.device_records))
     host_decl, n_unique = _decl_table(host_ids, hp)
     dev_decl, m_unique = _decl_table(dev_ids, dev_decl_ids)
     host, host_q, floor = _pack_side(
         trace.host_records, lambda r: r.rank, lambda r: HOST_STATE_CODE[r.state],
-        hdense, "host", "rank")
+        hdense, "host", "rank", ("rank", "state", _HOST_MEMBERS))
     dev, dev_q, _ = _pack_side(
         trace.device_records, lambda r: r.device_id, lambda r: DEVICE_KIND_CODE[r.kind],
-        ddense, "device", "device")
+        ddense, "device", "device", ("device_id", "kind", _DEV_MEMBERS))
     return PackedTrace(host, dev, host_ids, dev_ids, host_decl, dev_decl,
                        trace.n, trace.m, n_unique, m_unique, host_q, dev_q, floor)
 
