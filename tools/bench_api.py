@@ -86,9 +86,27 @@ t4 = time.perf_counter()
 pk, w2 = trace_io.import_mapped_packed(doc, mapping)
 t5 = time.perf_counter()
 from paper_2603_26576_b200 import engine as EN  # noqa: E402
-EN.analyze_packed(pk)
+EN.analyze_packed(pk, N.MODE_REPORT)
 t6 = time.perf_counter()
-EN.analyze_packed(pk)
+EN.analyze_packed(pk, N.MODE_REPORT)
 t7 = time.perf_counter()
 print(f"import_mapped_packed: {len(evs)} events in {t5 - t4:.2f} s = {len(evs) / (t5 - t4) / 1e6:.2f} M events/s "
       f"(columns, no record objects); analyze_packed of it {(t7 - t6) * 1e3:.1f} ms (warm)")
+
+# the drop-in API: compute_report(Trace) on a pre-built 2e6-record Trace (packing + H2D + kernel + result objects)
+import paper_2603_26576_b200 as hb  # noqa: E402
+
+host = [hb.HostRecord(j // 125000, hb.HostState.OFFLOAD if j % 3 == 1 else hb.HostState.USEFUL,
+                      hb.Interval(j * 10, j * 10 + 5)) for j in range(1_000_000)]
+dev = [hb.DeviceRecord(h.rank, hb.DeviceActivityKind.KERNEL if j % 5 else hb.DeviceActivityKind.MEMORY,
+                       hb.Interval(h.interval.start + 2, h.interval.end + 4), None) for j, h in enumerate(host)]
+t0 = time.perf_counter()
+tr = hb.Trace(host_processes=tuple(range(8)), devices=tuple(hb.DeviceDecl(d, d) for d in range(8)),
+              host_records=tuple(host), device_records=tuple(dev))
+t1 = time.perf_counter()
+hb.compute_report(tr)
+t2 = time.perf_counter()
+rep = hb.compute_report(tr)
+t3 = time.perf_counter()
+print(f"compute_report(Trace) of 2e6 records: {(t3 - t2) * 1e3:.0f} ms = {2e6 / (t3 - t2) / 1e6:.2f} M intervals/s "
+      f"(Trace construction {t1 - t0:.2f} s, by the caller); E={rep.elapsed_ns}")
