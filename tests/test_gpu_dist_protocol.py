@@ -1,0 +1,29 @@
+"""The multi-GPU merge protocol with real processes (torch.distributed.run, W ranks)
+on the one GPU available: every rank's shard goes through the real kernels and the
+merged report must equal the single-process analysis bit for bit (tools/dist_check.py)."""
+
+from __future__ import annotations
+
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+from conftest import gpu_available
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+@pytest.mark.parametrize("world,cfg,ranks,port", [(2, "c2", 64, 29611), (3, "c3", 16, 29612), (4, "c5", 10, 29613)])
+def test_merge_protocol_across_processes(world, cfg, ranks, port):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "tools" / "dist_check.py"), cfg, str(ranks)]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=str(ROOT))
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["world"] == world and line["status"] == 0
+    assert line["identical_to_single_process"], line
