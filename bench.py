@@ -171,13 +171,24 @@ def run_engine(args, world, rank, local):
     from paper_2603_26576_b200.engine import AnalysisPlan, DeviceTrace, analyze_device, analyze_host_columns
     from paper_2603_26576_b200.synth import generate
 
+    # test plumbing: HETEFF_DIST_BACKEND=gloo puts every rank on cuda:0 and runs the
+    # collectives through gloo on host copies (several ranks on the one GPU of a test box)
+    gloo = os.environ.get("HETEFF_DIST_BACKEND") == "gloo"
+    if gloo:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     # HETEFF_FORCE_DIST=1 runs the multi-GPU protocol even at world size 1 (exercises the
     # NCCL all-reduce / all-gather and the merge kernel on a single GPU)
     if world > 1 or os.environ.get("HETEFF_FORCE_DIST") == "1":
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        import torch.distributed as tdist
+        if gloo:
+            from paper_2603_26576_b200.sharded import HostCollectives
+            tdist.init_process_group("gloo")
+            dist = HostCollectives(tdist)
+        else:
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist = tdist
     cfg = _global_config(args.config, world)
     per = cfg.n_ranks // world
     r0, r1 = rank * per, (rank + 1) * per
@@ -303,7 +314,8 @@ def run_engine(args, world, rank, local):
         t = torch.tensor([e2e_ms], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    assert fe.status == N.OK and fe.elapsed == f.elapsed
+    # the merged (global) E of the device-resident protocol and of the host-buffer path agree
+    assert fe.status == N.OK and fe.elapsed == (merge.step().elapsed if merge is not None else f.elapsed)
     if windows is not None:
         # e2e of a region step is not separately staged from host buffers; it is
         # the compute_report path (the regions' inputs are the same columns)

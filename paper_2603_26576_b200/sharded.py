@@ -195,3 +195,35 @@ class DeviceMerge:
         if rc != N.OK:
             raise N.NativeError(f"heteff_merge_shards failed ({rc}): {N.last_error(self.ctx)}")
         return _findings(self.res, self.host_sum[: self.ntot], self.dev_sum[: self.mtot], [])
+
+
+class HostCollectives:
+    """TEST PLUMBING: the collectives this module issues, run by a gloo process group on
+    host copies of the (CUDA) tensors -- lets several ranks share the one GPU of a test
+    box, where NCCL refuses two ranks on one device (``tools/dist_check.py``,
+    ``HETEFF_DIST_BACKEND=gloo`` in ``bench.py``).  Production runs use NCCL directly."""
+
+    def __init__(self, dist):
+        self._d = dist
+        self.ReduceOp = dist.ReduceOp
+
+    def all_reduce(self, t, op):
+        h = t.cpu()
+        self._d.all_reduce(h, op=op)
+        t.copy_(h)
+
+    def all_gather_into_tensor(self, out, inp):
+        import torch
+
+        h = torch.empty(out.numel(), dtype=out.dtype)
+        self._d.all_gather_into_tensor(h, inp.cpu())
+        out.copy_(h)
+
+    def all_gather(self, outs, inp):
+        hs = [o.cpu() for o in outs]
+        self._d.all_gather(hs, inp.cpu())
+        for o, h in zip(outs, hs):
+            o.copy_(h)
+
+    def __getattr__(self, name):
+        return getattr(self._d, name)

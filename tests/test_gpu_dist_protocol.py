@@ -27,3 +27,23 @@ def test_merge_protocol_across_processes(world, cfg, ranks, port):
     line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["world"] == world and line["status"] == 0
     assert line["identical_to_single_process"], line
+
+
+@pytest.mark.parametrize("cfg,world,port", [("c2", 2, 29621), ("c1", 2, 29622), ("c2", 8, 29623)])
+def test_bench_under_torchrun(cfg, world, port):
+    """bench.py exactly as the driver's scaling run launches it (torchrun, W ranks), with
+    the collectives on gloo so the ranks can share the one GPU: it must finish and print
+    one JSON line for the whole job."""
+    import os
+
+    env = dict(os.environ, HETEFF_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py"), "--gpus", str(world),
+           "--config", cfg, "--steps", "5", "--warmup", "3", "--e2e-steps", "2", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=str(ROOT), env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == world and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["config"]["intervals"] == world * d["config"]["intervals_per_gpu"]

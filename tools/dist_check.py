@@ -20,26 +20,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2603_26576_b200 import _native as N  # noqa: E402
 from paper_2603_26576_b200.configs import CONFIGS, scaled  # noqa: E402
 from paper_2603_26576_b200.engine import analyze_device  # noqa: E402
-from paper_2603_26576_b200.sharded import DeviceMerge  # noqa: E402
+from paper_2603_26576_b200.sharded import DeviceMerge, HostCollectives  # noqa: E402
 from paper_2603_26576_b200.synth import generate  # noqa: E402
-
-
-class GlooOnHost:
-    """The two collectives DeviceMerge issues, through gloo on host copies."""
-    ReduceOp = dist.ReduceOp
-
-    def all_reduce(self, t, op):
-        h = t.cpu()
-        dist.all_reduce(h, op=op)
-        t.copy_(h)
-
-    def all_gather_into_tensor(self, out, inp):
-        h = torch.empty(out.numel(), dtype=out.dtype)
-        dist.all_gather_into_tensor(h, inp.cpu())
-        out.copy_(h)
-
-    def __getattr__(self, name):
-        return getattr(dist, name)
 
 
 def main():
@@ -53,7 +35,7 @@ def main():
     r0 = sum(n_of[:rank])
     dt = generate(cfg, r0, r0 + n_of[rank], device=0)
     stream = torch.cuda.current_stream(0).cuda_stream
-    merge = DeviceMerge(dt, GlooOnHost(), 0, stream, n_of, [k * cfg.gpus_per_rank for k in n_of])
+    merge = DeviceMerge(dt, HostCollectives(dist), 0, stream, n_of, [k * cfg.gpus_per_rank for k in n_of])
     f = merge.step()
     f = merge.step()                       # a second step: the workspace resets correctly
     if rank == 0:
