@@ -1134,7 +1134,7 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
     const uint32_t bl = (uint32_t)base, bh = (uint32_t)(base >> 32);
     constexpr bool merged = MERGED;
     uint32_t runK = 0, runKM = 0, cK = 0, cKM = 0, ps = 0;
-    uint32_t er[MERGED ? 1 : kItems];
+    uint32_t er[MERGED ? 1 : kItems], sr[MERGED ? 1 : kItems];
     uint32_t kmask = 0;             // bit j: record j is a kernel
     bool out = false, bad = false;  // bad: start outside the window / order / zero-length / malformed
     if (b > 0) ps = (uint32_t)sm.s[b - 1] - bl;
@@ -1161,14 +1161,19 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
             }
         }
     } else {
+        // starts are loaded (and window-checked) here too, so the pass after the
+        // barrier -- where every warp resumes at once -- runs on registers alone
 #pragma unroll kUnrollA
         for (int j = 0; j < kItems; ++j) {
             er[j] = 0;
+            sr[j] = 0;
             if (j < nv) {
-                const u64 e64 = sm.e[b + j];
-                const uint32_t e = (uint32_t)e64 - bl;
+                const u64 e64 = sm.e[b + j], s64 = sm.s[b + j];
+                const uint32_t e = (uint32_t)e64 - bl, sl = (uint32_t)s64;
                 out = out || (uint32_t)(e64 >> 32) != bh || (uint32_t)e64 < bl;
+                bad = bad || (uint32_t)(s64 >> 32) != bh || sl < bl;
                 er[MERGED ? 0 : j] = e;
+                sr[MERGED ? 0 : j] = sl - bl;
                 runKM = max(runKM, e);
                 if (sm.k[b + j] == 0) { runK = max(runK, e); kmask |= 1u << j; }
             }
@@ -1226,13 +1231,8 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
 #pragma unroll kUnrollB
         for (int j = 0; j < kItems; ++j) {
             if (j < nv) {
-                const u64 s64 = sm.s[b + j];
-                const uint32_t sl = (uint32_t)s64, s0 = sl - bl, e0 = er[MERGED ? 0 : j];
-#ifdef HB_NO_SCHECK
+                const uint32_t s0 = sr[MERGED ? 0 : j], e0 = er[MERGED ? 0 : j];
                 bad = bad || ((j > 0 || b > 0) && s0 < ps) || s0 >= e0;
-#else
-                bad = bad || (uint32_t)(s64 >> 32) != bh || sl < bl || ((j > 0 || b > 0) && s0 < ps) || s0 >= e0;
-#endif
                 const uint32_t e = min(e0, Er), s = min(s0, e);
                 const uint32_t loKM = max(runKM, s);
                 runKM = max(runKM, e);
