@@ -637,7 +637,10 @@ __global__ void __launch_bounds__(kDT) rd_sums(const __grid_constant__ RegParams
         int32_t owner = (p.owner && cur >= 0 && cur < p.dev_ids) ? p.owner[cur] : -1;
         Walk wk;
         wk.init = false;
-        int sq = -1;                       // cursor into the staged intervals (-1: not located yet)
+        // cursor into the staged intervals, located ONCE per thread before the record loop
+        // (every lane together): the thread's first start is <= every piece start x of
+        // the first device, and stage_overlap moves the cursor forward from there
+        int sq = (S.count > 0 && nv > 0 && cur == S.dev) ? stage_locate(S, T.s[b]) : 0;
         for (int q = 0; q < nv; ++q) {
             const int i = b + q;
             const int32_t pr = i > 0 ? T.r[i - 1] : prev_r;
@@ -649,7 +652,6 @@ __global__ void __launch_bounds__(kDT) rd_sums(const __grid_constant__ RegParams
                 cur = r;
                 owner = (p.owner && r >= 0 && r < p.dev_ids) ? p.owner[r] : -1;
                 wk.init = false;
-                sq = -1;
             }
             const u64 s = T.s[i], e = T.e[i];
             const u64 x = umax(runKM, s), y = umax(runKM, e);
@@ -657,7 +659,6 @@ __global__ void __launch_bounds__(kDT) rd_sums(const __grid_constant__ RegParams
             if (T.k[i] == 0) sa.v[0] += umax(runK, e) - umax(runK, s);
             if (x < y && owner >= 0 && owner < p.host_ids) {
                 if (S.count >= 0 && cur == S.dev) {
-                    if (sq < 0) sq = stage_locate(S, x);
                     sa.v[2] += stage_overlap(S, sq, x, y);
                 } else {
                     if (!wk.init) {
