@@ -1294,12 +1294,7 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
     return true;
 }
 
-#ifdef HB_GENERAL_NOINLINE
-#define DEV_GENERAL_ATTR __device__ __noinline__
-#else
-#define DEV_GENERAL_ATTR __device__ __forceinline__
-#endif
-DEV_GENERAL_ATTR void dev_general(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
+__device__ __forceinline__ void dev_general(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
                                   u64 &E_cache, bool &E_known, bool &signalled, int &k, Phases &ph);
 
 __device__ __forceinline__ void dev_compute(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
@@ -1321,7 +1316,7 @@ __device__ __forceinline__ void dev_compute(const Params &p, const StageSmem &sm
 }
 
 // tiles holding several devices (or leaving the 2^32 window): segmented scans, 64-bit fallback
-DEV_GENERAL_ATTR void dev_general(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
+__device__ __forceinline__ void dev_general(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
                                   u64 &E_cache, bool &E_known, bool &signalled, int &k, Phases &ph)
 {
     ph.mark();

@@ -255,28 +255,6 @@ __global__ void sub_flags(const u64 *__restrict__ as, const u64 *__restrict__ ae
     }
 }
 
-// exclusive prefix (in place, u32 -> int64 positions) -- one block, sequential chunks per thread
-__global__ void __launch_bounds__(1024) prefix_u32(const uint32_t *__restrict__ f, int64_t n,
-                                                   int64_t *__restrict__ out)
-{
-    __shared__ int64_t part[1024];
-    const int tid = threadIdx.x;
-    const int64_t per = (n + 1023) / 1024, a = tid * per, b = a + per < n ? a + per : n;
-    int64_t c = 0;
-    for (int64_t i = a; i < b; ++i) c += f[i];
-    part[tid] = c;
-    __syncthreads();
-    if (tid == 0) {
-        int64_t run = 0;
-        for (int t = 0; t < 1024; ++t) { const int64_t v = part[t]; part[t] = run; run += v; }
-    }
-    __syncthreads();
-    int64_t run = part[tid];
-    for (int64_t i = a; i < b; ++i) { out[i] = run; run += f[i]; }
-    if (b == n && a < b) out[n] = run;
-    if (n == 0 && tid == 0) out[0] = 0;
-}
-
 // multi-block exclusive prefix of u32 flags into int64 positions (out[n] = total):
 // per-block sums, a scan of the block sums (scan_counts), per-block apply
 __global__ void __launch_bounds__(kT) flag_sums(const uint32_t *__restrict__ f, int64_t n, uint32_t *__restrict__ bsum)
