@@ -157,7 +157,7 @@ def run_reference(args, world, rank):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    _emit(line)
 
 
 # ---------------------------------------------------------------------------
@@ -377,12 +377,28 @@ def run_engine(args, world, rank, local):
         line["cpu_baseline"] = {"value": k / sec, "unit": UNIT, "cores": threads, "kind": "port",
                                 "sample": f"C oracle on first {n} of {cfg.n_ranks} ranks of {cfg.name} "
                                           f"({k} intervals), {reps} reps"}
-    print(json.dumps(line), flush=True)
+    _emit(line)
     if dist:
         dist.destroy_process_group()
 
 
+_JSON_OUT = None
+
+
+def _emit(line: dict) -> None:
+    """The one JSON line, on the ORIGINAL stdout (see main)."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    # stdout carries exactly one JSON line: keep a duplicate of it for that line and point
+    # fd 1 at stderr, so banners native libraries print (NCCL's version line, ...) never mix in
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
