@@ -909,9 +909,75 @@ __device__ __forceinline__ bool host_fast32(const StageSmem &sm, int b, int nv, 
     return !out;
 }
 
+// Single-rank host tile (the common case: ~9 tiles per rank at C2): no segment
+// flags or head pieces, every thread's records continue one rank, the per-thread
+// 32-bit sums leave through REDUX (two 16-bit limbs) and one RED per field per warp.
+// Per warp: returns false (nothing emitted) if some lane leaves its 2^32 window --
+// that warp then runs the general path (host tiles need no CTA barrier).
+__device__ __forceinline__ bool host_single(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc,
+                                            int tid, Phases &ph)
+{
+    ph.mark();
+    const int lane = tid & 31;
+    const int b = tid * kItems;
+    const int nv = max(0, min(kItems, tc.cnt - b));
+    const int64_t gi0 = tc.gbase + (int64_t)b;
+    const int32_t r0 = sm.r[0];
+    const bool has_prev = c->has_prev[tc.st] != 0;
+    const int32_t prev_res = c->prev_res[tc.st];
+    bool cont = true, ovl = false, rare = false;
+    u64 ps = 0, pe = 0;   // previous start; end of the previous USABLE record of the rank
+    if (nv > 0) {
+        if (b == 0) {
+            cont = has_prev && prev_res == r0;
+            ps = c->prev_start[tc.st];
+            pe = c->prev_end[tc.st];
+            ovl = cont && ps >= pe;                     // previous record not usable: conservative
+            rare = has_prev && !cont && r0 < prev_res;  // rank order across the tile boundary
+        } else {
+            ps = sm.s[b - 1];
+            int q = b - 1;
+            while (q >= 0 && sm.s[q] >= sm.e[q]) --q;   // rare: skip non-usable records
+            if (q >= 0) pe = sm.e[q];
+            else ovl = has_prev && prev_res == r0;
+        }
+        rare = rare || !declared(p.host_decl, p.host_ids, p.n, r0);
+    }
+    u64 off = 0, mpi = 0, last = 0;
+    const bool ok = nv == 0 || host_fast32(sm, b, nv, cont, ps, pe, rare, ovl, off, mpi, last);
+    if (!__all_sync(0xffffffffu, ok)) return false;
+    u64 tmax = last;
+    if (ovl && !*(volatile unsigned *)&p.g->ovl_suspect) atomicOr(&p.g->ovl_suspect, 1u);
+    if (rare || ovl) tmax = host_rare(p, sm, c, tc.st, b, nv, gi0);
+    ph.add(ph.hb);
+    // 32-bit thread sums (disjoint durations inside one 2^32 window)
+    const u64 so = warp_sum32((uint32_t)off), sp = warp_sum32((uint32_t)mpi);
+    const u64 sl = warp_max_rx(last), wm = warp_max_rx(tmax);
+    if (lane == 0) {
+        if (r0 >= 0 && r0 < p.host_ids) {
+            if (so) red_add(p.h_off + r0, so);
+            if (sp) red_add(p.h_mpi + r0, sp);
+            if (sl) red_max(p.h_span + r0, sl);
+        }
+        // tile max end for E (summarize.py:88-89): warp max -> CTA (smem) -> one RED per tile
+        atomicMax(&c->h_max[tc.st], wm);
+        __threadfence_block();
+        if (atomicAdd(&c->h_cnt[tc.st], 1u) == kComputeWarps - 1) {
+            const u64 m = atomicExch(&c->h_max[tc.st], 0ull);
+            c->h_cnt[tc.st] = 0;
+            red_max(&p.g->host_max_end, m);
+        }
+    }
+    ph.add(ph.hemit);
+    return true;
+}
+
 __device__ __forceinline__ void host_compute(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc,
                                              int tid, Phases &ph)
 {
+#ifndef HB_NO_HOST_SINGLE
+    if (tc.cnt > 0 && sm.r[0] == sm.r[tc.cnt - 1] && host_single(p, sm, c, tc, tid, ph)) return;
+#endif
     ph.mark();
     const int warp = tid >> 5, lane = tid & 31;
     const int b = tid * kItems;
