@@ -54,7 +54,11 @@ constexpr int kHC = 256;             // host records per checkpoint chunk
 #define HB_REG_DT 128
 #endif
 #ifndef HB_REG_STAGE
-#define HB_REG_STAGE 1024
+// staged offload intervals per tile.  Measured on C4 (region call 17.5 -> 16.0 ms; 640,
+// 704, 832, 896 and 1024 all ~17.5 ms): likely because five ~39 KB CTAs fit the 196 KB
+// shared-memory carveout, leaving ~60 KB of L1 for the staging loop's second read of the
+// owner's host records
+#define HB_REG_STAGE 768
 #endif
 constexpr int kDT = HB_REG_DT;       // device tile threads
 constexpr int kDI = 9;               // device records per thread (odd: conflict-free smem)
@@ -605,7 +609,9 @@ __global__ void __launch_bounds__(kDT) rd_sums(const __grid_constant__ RegParams
             const int64_t per = (n + kDT - 1) / kDT;
             const int64_t a0 = q0 + umin((u64)(tid * per), (u64)n), a1 = q0 + umin((u64)((tid + 1) * per), (u64)n);
             uint32_t c = 0;
-            for (int64_t i = a0; i < a1; ++i) c += (__ldg(p.hk + i) == 1 && __ldg(p.hs + i) < __ldg(p.he + i));
+            // every offload record is staged (zero-length ones contribute nothing and keep the
+            // staged ends non-decreasing), so the count reads one byte per record
+            for (int64_t i = a0; i < a1; ++i) c += __ldg(p.hk + i) == 1;
             uint32_t inc = c;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
@@ -623,7 +629,7 @@ __global__ void __launch_bounds__(kDT) rd_sums(const __grid_constant__ RegParams
             if (all <= (uint32_t)kStage) {
                 for (int64_t i = a0; i < a1; ++i) {
                     const u64 hs = __ldg(p.hs + i), he = __ldg(p.he + i);
-                    if (__ldg(p.hk + i) == 1 && hs < he) { S.s[pos] = hs; S.e[pos] = he; ++pos; }
+                    if (__ldg(p.hk + i) == 1) { S.s[pos] = hs; S.e[pos] = he; ++pos; }
                 }
             }
             __syncthreads();
