@@ -12,6 +12,8 @@ gpurun snapshot) holding
 
 Usage (here, where /root/reference exists):   python tools/ref_suite.py assemble
 Then on the GPU box:                            python tools/ref_suite.py run
+Afterwards, here:                               python tools/ref_suite.py clean
+(the scratch copy of the reference's tests is not kept in the working tree).
 Nothing in the product imports ``_refsuite``; it is test infrastructure only.
 """
 from __future__ import annotations
@@ -130,5 +132,7 @@ if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "run"
     if what == "assemble":
         assemble()
+    elif what == "clean":
+        shutil.rmtree(OUT, ignore_errors=True)
     else:
         sys.exit(run(sys.argv[2:]))
