@@ -175,7 +175,131 @@ static PyObject *is_canonical(PyObject *self, PyObject *args)
     return PyBool_FromLong(ok == 1);
 }
 
+/* make_records(rec_cls, iv_cls, res_name, kind_name, members, res, kinds, starts, ends,
+ *              stream_name, streams) -> list
+ * Native columns (read_trace / import_mapped) -> record objects, exactly what the frozen
+ * dataclasses' generated __init__ does (object.__new__ + object.__setattr__ per field),
+ * without running Python bytecode per record.  res int64, kinds u8 (code -> members[code]),
+ * starts / ends u64, streams int64 (< 0 -> None) or None when the class has no stream. */
+static PyObject *s_e_start, *s_e_end;
+
+static PyObject *new_obj(PyObject *cls)
+{
+    static PyObject *empty = NULL;
+    if (!empty && !(empty = PyTuple_New(0))) return NULL;
+    return PyBaseObject_Type.tp_new((PyTypeObject *)cls, empty, NULL);
+}
+
+static PyObject *make_records(PyObject *self, PyObject *args)
+{
+    PyObject *rec_cls, *iv_cls, *res_name, *kind_name, *members, *stream_name, *streams_obj;
+    Py_buffer br, bk, bs, be, bt;
+    (void)self;
+    if (!PyArg_ParseTuple(args, "OOUUO!y*y*y*y*OO", &rec_cls, &iv_cls, &res_name, &kind_name, &PyTuple_Type, &members,
+                          &br, &bk, &bs, &be, &stream_name, &streams_obj))
+        return NULL;
+    PyObject *out = NULL;
+    int have_streams = streams_obj != Py_None;
+    bt.buf = NULL;
+    if (have_streams && PyObject_GetBuffer(streams_obj, &bt, PyBUF_SIMPLE) < 0) goto done;
+    const Py_ssize_t n = bs.len / 8;
+    if (br.len < n * 8 || bk.len < n || be.len < n * 8 || (have_streams && bt.len < n * 8)) {
+        PyErr_SetString(PyExc_ValueError, "column lengths disagree");
+        goto done;
+    }
+    const int64_t *R = (const int64_t *)br.buf, *T = have_streams ? (const int64_t *)bt.buf : NULL;
+    const uint8_t *K = (const uint8_t *)bk.buf;
+    const uint64_t *S = (const uint64_t *)bs.buf, *E = (const uint64_t *)be.buf;
+    const Py_ssize_t nm = PyTuple_GET_SIZE(members);
+    out = PyList_New(n);
+    if (!out) goto done;
+    for (Py_ssize_t i = 0; i < n; ++i) {
+        if (K[i] >= nm) { PyErr_SetString(PyExc_ValueError, "kind code out of range"); goto fail; }
+        PyObject *iv = new_obj(iv_cls);
+        if (!iv) goto fail;
+        PyObject *a = PyLong_FromUnsignedLongLong(S[i]), *b = PyLong_FromUnsignedLongLong(E[i]);
+        int bad = !a || !b || PyObject_GenericSetAttr(iv, s_e_start, a) < 0 || PyObject_GenericSetAttr(iv, s_e_end, b) < 0;
+        Py_XDECREF(a);
+        Py_XDECREF(b);
+        if (bad) { Py_DECREF(iv); goto fail; }
+        PyObject *rec = new_obj(rec_cls);
+        if (!rec) { Py_DECREF(iv); goto fail; }
+        PyObject *r = PyLong_FromLongLong(R[i]);
+        bad = !r || PyObject_GenericSetAttr(rec, res_name, r) < 0 ||
+              PyObject_GenericSetAttr(rec, kind_name, PyTuple_GET_ITEM(members, K[i])) < 0 ||
+              PyObject_GenericSetAttr(rec, s_interval, iv) < 0;
+        Py_XDECREF(r);
+        Py_DECREF(iv);
+        if (!bad && stream_name != Py_None) {
+            PyObject *st = (T && T[i] >= 0) ? PyLong_FromLongLong(T[i]) : (Py_INCREF(Py_None), Py_None);
+            bad = !st || PyObject_GenericSetAttr(rec, stream_name, st) < 0;
+            Py_XDECREF(st);
+        }
+        if (bad) { Py_DECREF(rec); goto fail; }
+        PyList_SET_ITEM(out, i, rec);   /* steals */
+    }
+    goto done;
+fail:
+    Py_CLEAR(out);
+done:
+    PyBuffer_Release(&br);
+    PyBuffer_Release(&bk);
+    PyBuffer_Release(&bs);
+    PyBuffer_Release(&be);
+    if (bt.buf) PyBuffer_Release(&bt);
+    return out;
+}
+
+/* sort_keys(records, res_attr, kind_attr, members_by_value, stream_attr_or_None,
+ *           res_out i64, start_out u64, end_out u64, kind_out u8, stream_out i64) -> bool
+ * The canonical-order key columns of every record (key_of above), for a stable numpy
+ * lexsort; False when some key is not decidable in 64-bit integers (the caller sorts
+ * with the key function instead). */
+static PyObject *sort_keys(PyObject *self, PyObject *args)
+{
+    PyObject *seq, *res_attr, *kind_attr, *members, *stream_attr;
+    Py_buffer br, bs, be, bk, bt;
+    (void)self;
+    if (!PyArg_ParseTuple(args, "OUUO!Ow*w*w*w*w*", &seq, &res_attr, &kind_attr, &PyTuple_Type, &members, &stream_attr,
+                          &br, &bs, &be, &bk, &bt))
+        return NULL;
+    PyObject *fast = PySequence_Fast(seq, "records must be a sequence");
+    int ok = 0;
+    if (fast) {
+        const Py_ssize_t n = PySequence_Fast_GET_SIZE(fast);
+        PyObject **items = PySequence_Fast_ITEMS(fast);
+        if (br.len < n * 8 || bs.len < n * 8 || be.len < n * 8 || bk.len < n || bt.len < n * 8) {
+            PyErr_SetString(PyExc_ValueError, "output buffers too small");
+        } else {
+            int64_t *R = (int64_t *)br.buf, *T = (int64_t *)bt.buf;
+            uint64_t *S = (uint64_t *)bs.buf, *E = (uint64_t *)be.buf;
+            uint8_t *K = (uint8_t *)bk.buf;
+            long long key[5];
+            ok = 1;
+            for (Py_ssize_t i = 0; i < n && ok == 1; ++i) {
+                ok = key_of(items[i], res_attr, kind_attr, members, stream_attr, key);
+                if (ok != 1) break;
+                R[i] = key[0];
+                S[i] = (uint64_t)key[1] ^ 0x8000000000000000ull;
+                E[i] = (uint64_t)key[2] ^ 0x8000000000000000ull;
+                K[i] = (uint8_t)key[3];
+                T[i] = key[4];
+            }
+        }
+        Py_DECREF(fast);
+    }
+    PyBuffer_Release(&br);
+    PyBuffer_Release(&bs);
+    PyBuffer_Release(&be);
+    PyBuffer_Release(&bk);
+    PyBuffer_Release(&bt);
+    if (ok < 0 || PyErr_Occurred()) return NULL;
+    return PyBool_FromLong(ok == 1);
+}
+
 static PyMethodDef methods[] = {
+    {"sort_keys", sort_keys, METH_VARARGS, "canonical-order key columns (64-bit decidable?)"},
+    {"make_records", make_records, METH_VARARGS, "native columns -> record objects (the dataclasses' own __init__ effect)"},
     {"pack_side", pack_side, METH_VARARGS, "records -> (start, end, dense id, kind) columns; False: use the exact path"},
     {"is_canonical", is_canonical, METH_VARARGS, "records already in canonical Trace order (64-bit decidable)?"},
     {NULL, NULL, 0, NULL},
@@ -188,6 +312,8 @@ PyMODINIT_FUNC PyInit__pack(void)
     s_interval = PyUnicode_InternFromString("interval");
     s_start = PyUnicode_InternFromString("start");
     s_end = PyUnicode_InternFromString("end");
+    s_e_start = s_start;
+    s_e_end = s_end;
     if (!s_interval || !s_start || !s_end) return NULL;
     return PyModule_Create(&module);
 }

@@ -94,6 +94,25 @@ def _already_canonical(records, res_attr, kind_attr, members, stream_attr) -> bo
     return _pack.is_canonical(records, res_attr, kind_attr, members, stream_attr)
 
 
+def _native_sorted(records, res_attr, kind_attr, members, stream_attr, key) -> tuple:
+    """``tuple(sorted(records, key=key))`` -- by a stable numpy lexsort over natively
+    extracted key columns when every key fits 64-bit integers (csrc/pack.c)."""
+    try:
+        from . import _pack
+    except ImportError:
+        _pack = None
+    if _pack is not None:
+        import numpy as np
+
+        n = len(records)
+        cols = (np.empty(n, np.int64), np.empty(n, np.uint64), np.empty(n, np.uint64), np.empty(n, np.uint8),
+                np.empty(n, np.int64))
+        if _pack.sort_keys(records, res_attr, kind_attr, members, stream_attr, *cols):
+            order = np.lexsort((cols[4], cols[3], cols[2], cols[1], cols[0]))   # stable, last key primary
+            return tuple(map(records.__getitem__, order.tolist()))
+    return tuple(sorted(records, key=key))
+
+
 def _canonical_host(rec: HostRecord):
     iv = rec.interval
     return (rec.rank, iv.start, iv.end, rec.state.value)
@@ -128,9 +147,9 @@ class Trace:
         # records that already arrive in canonical order (files, time-ordered generators)
         # skip the key-function sort: one native pass decides it (csrc/pack.c)
         if not _already_canonical(hr, "rank", "state", _HOST_BY_VALUE, None):
-            hr = tuple(sorted(hr, key=_canonical_host))
+            hr = _native_sorted(hr, "rank", "state", _HOST_BY_VALUE, None, _canonical_host)
         if not _already_canonical(dr, "device_id", "kind", _DEV_BY_VALUE, "stream"):
-            dr = tuple(sorted(dr, key=_canonical_device))
+            dr = _native_sorted(dr, "device_id", "kind", _DEV_BY_VALUE, "stream", _canonical_device)
         set_(self, "host_records", hr)
         set_(self, "device_records", dr)
 

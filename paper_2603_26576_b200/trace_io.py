@@ -195,22 +195,41 @@ def read_trace(data, nthreads: int | None = None) -> Trace:
     if cols is None:
         return _parse_py(data)
     ranks = cols["host_rank"].tolist()
-    hoff = cols["host_off"].tolist()
-    hk, hs, he = cols["h_kind"].tolist(), cols["h_start"].tolist(), cols["h_end"].tolist()
-    hrecs = []
-    for i, r in enumerate(ranks):
-        for j in range(hoff[i], hoff[i + 1]):
-            hrecs.append(HostRecord(r, _HOST_CODE_STATE[hk[j]], Interval(hs[j], he[j])))
-    ids, owners, doff = cols["dev_id"].tolist(), cols["dev_owner"].tolist(), cols["dev_off"].tolist()
-    dk, dst, ds, de = cols["d_kind"].tolist(), cols["d_stream"].tolist(), cols["d_start"].tolist(), cols["d_end"].tolist()
-    decls, drecs = [], []
-    for i, d in enumerate(ids):
-        decls.append(DeviceDecl(d, None if owners[i] < 0 else owners[i]))
-        for j in range(doff[i], doff[i + 1]):
-            drecs.append(DeviceRecord(d, _DEV_CODE_KIND[dk[j]], Interval(ds[j], de[j]),
-                                      None if dst[j] < 0 else dst[j]))
+    ids, owners = cols["dev_id"].tolist(), cols["dev_owner"].tolist()
+    decls = [DeviceDecl(d, None if o < 0 else o) for d, o in zip(ids, owners)]
+    hres = np.repeat(cols["host_rank"], np.diff(cols["host_off"]))
+    dres = np.repeat(cols["dev_id"], np.diff(cols["dev_off"]))
+    hrecs = _records(HostRecord, "rank", "state", _HOST_CODE_STATE, hres, cols["h_kind"], cols["h_start"],
+                     cols["h_end"])
+    drecs = _records(DeviceRecord, "device_id", "kind", _DEV_CODE_KIND, dres, cols["d_kind"], cols["d_start"],
+                     cols["d_end"], cols["d_stream"])
     return Trace(host_processes=tuple(ranks), devices=tuple(decls), host_records=tuple(hrecs),
                  device_records=tuple(drecs))
+
+
+try:   # native record builder (csrc/pack.c); the Python loop below is the same construction
+    from . import _pack
+except ImportError:
+    _pack = None
+
+
+def _records(cls, res_name, kind_name, members, res, kinds, starts, ends, streams=None):
+    """Record objects from native columns: ``cls(res, members[kind], Interval(start, end)[, stream])``
+    with ``stream`` < 0 -> None (what the reference's reader builds, ``trace_io.py:96-158``)."""
+    if _pack is not None and (res.size == 0 or int(res.max()) < 2 ** 63):
+        c = lambda a, t: np.ascontiguousarray(a, dtype=t)   # noqa: E731
+        return _pack.make_records(cls, Interval, res_name, kind_name, tuple(members), c(res, np.int64),
+                                  c(kinds, np.uint8), c(starts, np.uint64), c(ends, np.uint64),
+                                  "stream" if cls is DeviceRecord else None,
+                                  None if streams is None else c(streams, np.int64))
+    out = []
+    for j, (r, kd, a, b) in enumerate(zip(res.tolist(), kinds.tolist(), starts.tolist(), ends.tolist())):
+        if streams is None:
+            out.append(cls(r, members[kd], Interval(a, b)))
+        else:
+            st = int(streams[j])
+            out.append(cls(r, members[kd], Interval(a, b), None if st < 0 else st))
+    return out
 
 
 def _dense_ids(declared: np.ndarray):
@@ -471,8 +490,6 @@ def import_mapped(data, mapping: CategoryMapping, nthreads: int | None = None, c
         res = _arr(v.res, k, np.uint64)
         st = _arr(v.start, k, np.uint64)
         en = _arr(v.end, k, np.uint64)
-        if not columns:
-            is_dev, kind, res, st, en = (x.tolist() for x in (is_dev, kind, res, st, en))
         um = _arr(v.unmapped, u, np.int64).tolist()
         no = _arr(v.name_off, u, np.int64).tolist()
         nl = _arr(v.name_len, u, np.int64).tolist()
@@ -480,12 +497,9 @@ def import_mapped(data, mapping: CategoryMapping, nthreads: int | None = None, c
         lib.heteff_imported_free(handle)
     if columns:
         return (is_dev, kind, res, st, en), [(i, raw[o:o + n].decode("utf-8")) for i, o, n in zip(um, no, nl)]
-    hrecs, drecs = [], []
-    for d, kd, r, a, b in zip(is_dev, kind, res, st, en):
-        if d:
-            drecs.append(DeviceRecord(r, _DEV_CODE_KIND[kd], Interval(a, b)))
-        else:
-            hrecs.append(HostRecord(r, _HOST_CODE_STATE[kd], Interval(a, b)))
+    h, d = is_dev == 0, is_dev == 1
+    hrecs = _records(HostRecord, "rank", "state", _HOST_CODE_STATE, res[h], kind[h], st[h], en[h])
+    drecs = _records(DeviceRecord, "device_id", "kind", _DEV_CODE_KIND, res[d], kind[d], st[d], en[d])
     unmapped = [(i, raw[o:o + n].decode("utf-8")) for i, o, n in zip(um, no, nl)]
     return _assemble(hrecs, drecs, unmapped, mapping)
 
