@@ -86,3 +86,25 @@ def test_native_packer_defers_unusual_timestamps_to_the_exact_path(bad, monkeypa
         t2 = t
         object.__setattr__(t2, "host_records", tuple(host))
     _same(*_packed_both(t2, monkeypatch))
+
+
+def test_native_records_equal_the_dataclass_constructors():
+    from paper_2603_26576_b200 import trace_io
+
+    res = np.array([0, 5, 2 ** 62], np.uint64)
+    kinds = np.array([0, 1, 0], np.uint8)
+    st = np.array([0, 7, 2 ** 64 - 3], np.uint64)
+    en = np.array([0, 9, 2 ** 64 - 1], np.uint64)
+    streams = np.array([-1, 3, 0], np.int64)
+    got = trace_io._records(hb.DeviceRecord, "device_id", "kind", trace_io._DEV_CODE_KIND, res, kinds, st, en, streams)
+    ref = [hb.DeviceRecord(0, DK[0], hb.Interval(0, 0), None), hb.DeviceRecord(5, DK[1], hb.Interval(7, 9), 3),
+           hb.DeviceRecord(2 ** 62, DK[0], hb.Interval(2 ** 64 - 3, 2 ** 64 - 1), 0)]
+    assert got == ref and [hash(x) for x in got] == [hash(x) for x in ref] and repr(got) == repr(ref)
+    host = trace_io._records(hb.HostRecord, "rank", "state", trace_io._HOST_CODE_STATE, res[:2], np.array([2, 1], np.uint8),
+                             st[:2], en[:2])
+    assert host == [hb.HostRecord(0, trace_io._HOST_CODE_STATE[2], hb.Interval(0, 0)),
+                    hb.HostRecord(5, trace_io._HOST_CODE_STATE[1], hb.Interval(7, 9))]
+    # ids beyond int64: the Python construction path
+    big = trace_io._records(hb.HostRecord, "rank", "state", trace_io._HOST_CODE_STATE,
+                            np.array([2 ** 64 - 1], np.uint64), np.array([0], np.uint8), st[:1], en[:1])
+    assert big == [hb.HostRecord(2 ** 64 - 1, trace_io._HOST_CODE_STATE[0], hb.Interval(0, 0))]
