@@ -1,0 +1,109 @@
+"""Randomized engine-vs-oracle stress run (test infrastructure): random trace shapes --
+counts around tile boundaries, time ranges crossing 2^32 or near U64_MAX, overlapping
+streams, zero-length / malformed records, empty resources -- through the engine's
+columnar path in REPORT / VALIDATE / SUMMARIZE_DEVICE mode against the C oracle.
+Usage: python tools/stress.py SECONDS [SEED]"""
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "tests"))
+from oracle import oracle as O  # noqa: E402
+from paper_2603_26576_b200 import _native as N  # noqa: E402
+from paper_2603_26576_b200.engine import analyze_packed  # noqa: E402
+from paper_2603_26576_b200.packing import PackedTrace, RecordColumns  # noqa: E402
+
+TILE = 15 * 32 * 11
+
+
+def canonical(s, e, r, k, host):
+    kr = np.array([2, 1, 0], dtype=np.uint8)[k] if host else k
+    o = np.lexsort((kr, e, s, r))
+    return s[o], e[o], r[o], k[o]
+
+
+def side(rng, n_res, host):
+    if n_res == 0:
+        return np.zeros(0, np.uint64), np.zeros(0, np.uint64), np.zeros(0, np.int32), np.zeros(0, np.uint8)
+    pick = rng.integers(0, 4)
+    if pick == 0:
+        counts = rng.integers(0, 6, n_res)
+    elif pick == 1:
+        counts = rng.choice([TILE - 1, TILE, TILE + 1, 2 * TILE - 3, 1, 0, 31, 32, 33], n_res)
+    else:
+        counts = rng.integers(0, 3 * TILE, n_res)
+    r = np.repeat(np.arange(n_res, dtype=np.int32), counts)
+    k = r.size
+    scale = rng.choice([10 ** 3, 10 ** 6, 2 ** 33, 2 ** 40])
+    base = rng.choice([0, 2 ** 32 - 10 ** 6, 2 ** 63, 2 ** 64 - 2 ** 41])
+    if host:   # a serialized chain per rank (valid), with a few anomalies
+        g = rng.integers(0, 20, k).astype(np.uint64)
+        d = rng.integers(1, 200, k).astype(np.uint64)
+        cs = np.cumsum(g + d)
+        offs = np.concatenate([[0], np.cumsum(counts)])
+        b0 = np.zeros(n_res, np.uint64)
+        nz = offs[:-1] > 0
+        b0[nz] = cs[offs[:-1][nz] - 1]
+        s = cs - np.repeat(b0, counts) - d
+        e = s + d
+    else:
+        s = rng.integers(0, max(2, int(scale)), k, dtype=np.uint64)
+        e = s + rng.integers(1, max(2, int(scale) // max(1, k // max(n_res, 1)) * int(rng.choice([1, 4, 16]))), k,
+                             dtype=np.uint64)
+    s = s + np.uint64(base)
+    e = np.minimum(e + np.uint64(base), np.uint64(2 ** 64 - 1))
+    if rng.random() < 0.3 and k:
+        z = rng.random(k) < 0.01
+        e[z] = s[z]
+    if rng.random() < 0.1 and k:
+        bad = rng.random(k) < 0.001
+        e[bad] = s[bad] - np.minimum(s[bad], np.uint64(3))
+    kind = rng.integers(0, 3 if host else 2, k, dtype=np.uint8)
+    return canonical(s, e, r, kind, host)
+
+
+def one(rng):
+    n, m = int(rng.integers(0, 6)), int(rng.integers(0, 6))
+    if n == 0 and m == 0:
+        m = 1
+    h, d = side(rng, n, True), side(rng, m, False)
+    packed = PackedTrace(RecordColumns(*h), RecordColumns(*d), list(range(n)), list(range(m)),
+                         np.arange(n, dtype=np.int32), np.arange(m, dtype=np.int32), n, m, n, m)
+    modes = [(N.MODE_REPORT, 0), (N.MODE_VALIDATE, 0)]
+    if m:
+        top = int(max([int(d[1].max()) if d[1].size else 1, int(h[1].max()) if h[1].size else 1]))
+        modes.append((N.MODE_SUMMARIZE_DEVICE, max(1, int(rng.random() * top))))
+    for mode, el in modes:
+        got = analyze_packed(packed, mode, el, want_lists=True, capacity=1 << 18)
+        ref = O.analyze(h, d, n, m, mode=mode, elapsed=el, cap=1 << 18)
+        assert got.status == ref.status, (mode, got.status, ref.status)
+        lists = (0, 1, 2, 4, 5, 6, 7) if mode != N.MODE_SUMMARIZE_DEVICE else (0, 1, 2, 4, 5, 6)
+        assert [got.counts[c] for c in lists + (3,)] == [ref.counts[c] for c in lists + (3,)], mode
+        if ref.status == 0 and mode != N.MODE_VALIDATE:   # the oracle's validate mode computes no E
+            assert got.elapsed == ref.elapsed, (mode, got.elapsed, ref.elapsed)
+            assert np.array_equal(got.host_sum, ref.host_sum) and np.array_equal(got.dev_sum, ref.dev_sum), mode
+            assert got.host_metrics == ref.host_metrics and got.device_metrics == ref.device_metrics, mode
+    return h[0].size + d[0].size
+
+
+def main():
+    seconds = float(sys.argv[1]) if len(sys.argv) > 1 else 60.0
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+    rng = np.random.default_rng(seed)
+    t0, cases, recs = time.time(), 0, 0
+    while time.time() - t0 < seconds:
+        case_seed = int(rng.integers(0, 2 ** 31))
+        try:
+            recs += one(np.random.default_rng(case_seed))
+        except AssertionError as e:
+            print(f"MISMATCH seed={case_seed}: {e}", flush=True)
+            raise
+        cases += 1
+    print(f"stress ok: {cases} random traces ({recs} records), 2-3 modes each, engine == oracle", flush=True)
+
+
+if __name__ == "__main__":
+    main()
