@@ -89,9 +89,51 @@ def one(rng):
     return h[0].size + d[0].size
 
 
+def one_regions(rng):
+    """K5/K6: random windows (whole range, empty, beyond the span, random) and random
+    owners (some devices unowned) against the oracle's composition restatement."""
+    import torch
+
+    from paper_2603_26576_b200.engine import DeviceTrace, analyze_regions
+
+    n, m = int(rng.integers(0, 5)), int(rng.integers(1, 5))
+    h, d = side(rng, n, True), side(rng, m, False)
+    owner = np.array([int(rng.integers(-1, n)) if n else -1 for _ in range(m)], np.int32)
+    top = int(max([int(x[1].max()) for x in (h, d) if x[1].size] + [1]))
+    lo = int(min([int(x[0].min()) for x in (h, d) if x[0].size] + [0]))
+    win = [(0, 2 ** 64 - 1), (lo, lo), (top + 5, top + 50)]
+    for _ in range(int(rng.integers(1, 20))):
+        a = lo + int(rng.random() * max(1, top - lo))
+        win.append((a, min(2 ** 64 - 1, a + 1 + int(rng.random() * max(1, top - a)))))
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64) if a.dtype == np.uint64  # noqa: E731
+                                    else np.ascontiguousarray(a)).cuda()
+    dt = DeviceTrace(*(cu(x) for x in (*h, *d)), n, m)
+    run = analyze_regions(dt, win, owner)
+    whole = O.analyze(h, d, n, m, mode=N.MODE_REPORT, cap=0)
+    if whole.status == N.INVALID_TRACE:   # invalid traces fail the call as a whole
+        assert run.status == N.INVALID_TRACE, run.status
+        return h[0].size + d[0].size
+    assert run.status == N.OK, run.status   # per-region analysis errors are the regions' own
+    ref = O.regions(h, d, n, m, win, owner)
+    for j in range(len(win)):
+        g = run.regions[j]
+        assert g.status == int(ref.status[j]), ("status", j)
+        if g.status != N.OK:
+            continue
+        assert g.elapsed == int(ref.elapsed[j]), ("E", j)
+        assert np.array_equal(g.host_sum, ref.host_sum[j]) and np.array_equal(g.dev_sum, ref.dev_sum[j]), ("sums", j)
+        assert np.array_equal(g.offload_busy, ref.busy[j]), ("busy", j)
+        assert g.host_metrics == ref.host_metrics[j] and g.device_metrics == ref.device_metrics[j], ("metrics", j)
+        assert g.offload_busy_fraction == ref.busy_frac[j], ("frac", j)
+    return h[0].size + d[0].size
+
+
 def main():
     seconds = float(sys.argv[1]) if len(sys.argv) > 1 else 60.0
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+    if len(sys.argv) > 3 and sys.argv[3] == "regions":
+        global one
+        one = one_regions
     rng = np.random.default_rng(seed)
     t0, cases, recs = time.time(), 0, 0
     while time.time() - t0 < seconds:
@@ -102,7 +144,8 @@ def main():
             print(f"MISMATCH seed={case_seed}: {e}", flush=True)
             raise
         cases += 1
-    print(f"stress ok: {cases} random traces ({recs} records), 2-3 modes each, engine == oracle", flush=True)
+    what = "region sets" if one is one_regions else "traces, 2-3 modes each"
+    print(f"stress ok: {cases} random {what} ({recs} records), engine == oracle", flush=True)
 
 
 if __name__ == "__main__":
