@@ -128,12 +128,102 @@ def one_regions(rng):
     return h[0].size + d[0].size
 
 
+def _iv_cols(rng, n):
+    scale = int(rng.choice([10, 10 ** 3, 10 ** 6, 2 ** 40]))
+    base = np.uint64(int(rng.choice([0, 2 ** 32 - 500, 2 ** 63, 2 ** 64 - 2 ** 41])))
+    st = base + rng.integers(0, scale, n, dtype=np.uint64)
+    d = rng.integers(0, max(2, scale // max(1, n) * int(rng.choice([1, 3, 30]))), n, dtype=np.uint64)
+    return st, st + np.minimum(d, np.uint64(2 ** 64 - 1) - st)   # ends never wrap past u64
+
+
+def one_intervals(rng):
+    """flatten / subtract / intersect / total_duration through the C ABI on device arrays
+    against the oracle's restatement of intervals.py:40-105."""
+    import ctypes as C
+
+    import torch
+
+    lib, ctx = N.load(), N.context()
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).cuda()   # noqa: E731
+    u64 = lambda t: t.cpu().numpy().view(np.uint64)   # noqa: E731
+    n = int(rng.choice([0, 1, 2, 31, 33, 1000, 3 * TILE + 7, int(rng.integers(1, 300_000))]))
+    s, e = _iv_cols(rng, n)
+    if n and rng.random() < 0.1:
+        j = int(rng.integers(0, n))
+        s[j], e[j] = e[j] + np.uint64(1), s[j]   # malformed
+    S, E = cu(s), cu(e)
+    os_, oe = torch.empty(max(n, 1), dtype=torch.int64, device="cuda"), torch.empty(max(n, 1), dtype=torch.int64,
+                                                                                    device="cuda")
+    k, bad = C.c_int64(0), C.c_int64(-1)
+    rc = lib.heteff_flatten(ctx, S.data_ptr() if n else None, E.data_ptr() if n else None, n, os_.data_ptr(),
+                            oe.data_ptr(), C.byref(k), C.byref(bad), None)
+    try:
+        rs, re_ = O.iv_flatten(s, e)
+    except ValueError as x:
+        assert rc == N.VALUE_ERROR and bad.value == int(x.args[0]), (rc, bad.value, x.args)
+        return n
+    assert rc == N.OK and np.array_equal(u64(os_[:k.value]), rs) and np.array_equal(u64(oe[:k.value]), re_), "flatten"
+    a_s, a_e = rs, re_
+    t, u = _iv_cols(rng, int(rng.integers(0, max(2, n))))
+    b_s, b_e = O.iv_flatten(t, u)
+    out_s = torch.empty(len(a_s) + len(b_s) + 1, dtype=torch.int64, device="cuda")
+    out_e = torch.empty_like(out_s)
+    A_s, A_e, B_s, B_e = cu(a_s), cu(a_e), cu(b_s), cu(b_e)
+    p_ = lambda x, m: x.data_ptr() if m else None   # noqa: E731
+    rc = lib.heteff_subtract(ctx, p_(A_s, len(a_s)), p_(A_e, len(a_s)), len(a_s), p_(B_s, len(b_s)), p_(B_e, len(b_s)),
+                             len(b_s), out_s.data_ptr(), out_e.data_ptr(), C.byref(k), None)
+    ws, we = O.iv_subtract(a_s, a_e, b_s, b_e)
+    assert rc == N.OK and np.array_equal(u64(out_s[:k.value]), ws) and np.array_equal(u64(out_e[:k.value]), we), "sub"
+    if len(a_s):
+        lo = int(a_s[0]) + int(rng.random() * max(1, int(a_e[-1]) - int(a_s[0])))
+        hi = min(2 ** 64 - 1, lo + int(rng.random() * max(1, int(a_e[-1]) - lo + 10)))
+        rc = lib.heteff_intersect(ctx, A_s.data_ptr(), A_e.data_ptr(), len(a_s), lo, hi, out_s.data_ptr(),
+                                  out_e.data_ptr(), C.byref(k), None)
+        xs, xe = O.iv_intersect(a_s, a_e, lo, hi)
+        assert rc == N.OK and np.array_equal(u64(out_s[:k.value]), xs) and np.array_equal(u64(out_e[:k.value]), xe), \
+            "intersect"
+        tot = (C.c_uint64 * 2)()
+        rc = lib.heteff_total_duration(ctx, A_s.data_ptr(), A_e.data_ptr(), len(a_s), C.cast(tot, C.c_void_p), None)
+        assert rc == N.OK and int(tot[0]) + (int(tot[1]) << 64) == O.iv_total(a_s, a_e), "total"
+    return n
+
+
+def one_sort(rng):
+    """K3 on random columns (resource counts, start ranges, durations that do / do not fit
+    the key's spare bits, malformed records, kinds > 3) against a stable lexsort."""
+    import torch
+
+    from paper_2603_26576_b200.engine import sort_records
+
+    n = int(rng.choice([1, 2, 31, 33, 5631, 5632, 5633, int(rng.integers(1, 400_000))]))
+    ids = int(rng.choice([1, 2, 7, 1000, 70_000]))
+    span = int(rng.choice([1, 100, 10 ** 6, 2 ** 40, 2 ** 62]))
+    s = rng.integers(0, span, n, dtype=np.uint64) if span > 1 else np.zeros(n, np.uint64)
+    if rng.random() < 0.3:
+        s = np.sort(s)   # start-ordered input: the res-only path
+    d = rng.integers(0, int(rng.choice([2, 1000, 2 ** 30, 2 ** 50])), n, dtype=np.uint64)
+    e = s + d
+    if rng.random() < 0.1:
+        e[int(rng.integers(0, n))] = s[0] - np.minimum(s[0], np.uint64(1))   # a malformed record
+    r = rng.integers(0, ids, n, dtype=np.int32) - (int(rng.integers(0, 3)) if rng.random() < 0.2 else 0)
+    k = rng.integers(0, 256 if rng.random() < 0.05 else 2, n, dtype=np.int32).astype(np.uint8)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64) if a.dtype == np.uint64  # noqa: E731
+                                    else np.ascontiguousarray(a)).cuda()
+    got = sort_records(cu(s), cu(e), cu(r), cu(k))
+    perm = np.lexsort((s, r.astype(np.int64)))
+    assert np.array_equal(got.perm.cpu().numpy(), perm), "perm"
+    assert np.array_equal(got.start.cpu().numpy().view(np.uint64), s[perm]), "start"
+    assert np.array_equal(got.end.cpu().numpy().view(np.uint64), e[perm]), "end"
+    assert np.array_equal(got.res.cpu().numpy(), r[perm]) and np.array_equal(got.kind.cpu().numpy(), k[perm]), "res/kind"
+    return n
+
+
 def main():
     seconds = float(sys.argv[1]) if len(sys.argv) > 1 else 60.0
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-    if len(sys.argv) > 3 and sys.argv[3] == "regions":
-        global one
-        one = one_regions
+    global one
+    mode = sys.argv[3] if len(sys.argv) > 3 else "analysis"
+    one = {"analysis": one, "regions": one_regions, "intervals": one_intervals, "sort": one_sort}[mode]
     rng = np.random.default_rng(seed)
     t0, cases, recs = time.time(), 0, 0
     while time.time() - t0 < seconds:
@@ -144,7 +234,8 @@ def main():
             print(f"MISMATCH seed={case_seed}: {e}", flush=True)
             raise
         cases += 1
-    what = "region sets" if one is one_regions else "traces, 2-3 modes each"
+    what = {"analysis": "traces, 2-3 modes each", "regions": "region sets", "intervals": "interval-algebra cases",
+            "sort": "sort cases"}[mode]
     print(f"stress ok: {cases} random {what} ({recs} records), engine == oracle", flush=True)
 
 
