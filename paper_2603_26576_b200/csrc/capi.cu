@@ -52,6 +52,9 @@ struct heteff_ctx {
     DevBuf out_blk;
     void *out_pin = nullptr;
     size_t out_pin_bytes = 0;
+    // small host-buffer calls: every input column gathered into one pinned block, one H2D
+    void *in_pin = nullptr;
+    size_t in_pin_bytes = 0;
 };
 
 static int fail(heteff_ctx *ctx, int code, const std::string &msg)
@@ -127,6 +130,7 @@ void heteff_destroy(heteff_ctx *ctx)
     if (ctx->res_d) cudaFree(ctx->res_d);
     if (ctx->res_h) cudaFreeHost(ctx->res_h);
     if (ctx->out_pin) cudaFreeHost(ctx->out_pin);
+    if (ctx->in_pin) cudaFreeHost(ctx->in_pin);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     delete ctx;
@@ -707,12 +711,27 @@ static int analyze_host_impl(heteff_ctx *ctx, const heteff_trace *trace, const i
     const size_t total = 2 * hb8 + hb4 + hb1 + 2 * db8 + db4 + db1 + hd + dd + hs8 + ds8;
     CK(ensure(ctx->stage, total, false), "alloc staging");
     uint8_t *b = static_cast<uint8_t *>(ctx->stage.p);
+    // small inputs (the drop-in API on ordinary traces, usually pageable numpy memory):
+    // gather every column into one pinned block and issue ONE copy instead of one
+    // driver-staged copy per column; large inputs are copied column by column at PCIe rate
+    const bool gather = total <= ((size_t)8 << 20);
+    if (gather && ctx->in_pin_bytes < total) {
+        if (ctx->in_pin) cudaFreeHost(ctx->in_pin);
+        ctx->in_pin = nullptr;
+        ctx->in_pin_bytes = 0;
+        CK(cudaMallocHost(&ctx->in_pin, total), "alloc pinned inputs");
+        ctx->in_pin_bytes = total;
+    }
+    uint8_t *hpin = gather ? static_cast<uint8_t *>(ctx->in_pin) : nullptr;
     heteff_trace d = *trace;
     size_t o = 0;
     auto put = [&](const void *src, size_t bytes, size_t room) -> void * {
         void *dst = b + o;
+        if (bytes && src) {
+            if (gather) memcpy(hpin + o, src, bytes);
+            else cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+        }
         o += room;
-        if (bytes && src) cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
         return dst;
     };
     d.host.start = static_cast<const uint64_t *>(put(trace->host.start, (size_t)hn * 8, hb8));
@@ -729,14 +748,11 @@ static int analyze_host_impl(heteff_ctx *ctx, const heteff_trace *trace, const i
     d.dev_decl = trace->dev_decl
                      ? static_cast<const int32_t *>(put(trace->dev_decl, (size_t)trace->dev_ids * 4, dd))
                      : nullptr;
-    if (hseg) {
-        const int64_t *g = static_cast<const int64_t *>(put(hseg, ((size_t)trace->host_ids + 1) * 8, hs8));
-        CK(hb::launch_expand_res(g, trace->host_ids, hn, const_cast<int32_t *>(d.host.res), s), "expand host res");
-    }
-    if (dseg) {
-        const int64_t *g = static_cast<const int64_t *>(put(dseg, ((size_t)trace->dev_ids + 1) * 8, ds8));
-        CK(hb::launch_expand_res(g, trace->dev_ids, dn, const_cast<int32_t *>(d.dev.res), s), "expand dev res");
-    }
+    const int64_t *hg = hseg ? static_cast<const int64_t *>(put(hseg, ((size_t)trace->host_ids + 1) * 8, hs8)) : nullptr;
+    const int64_t *dg = dseg ? static_cast<const int64_t *>(put(dseg, ((size_t)trace->dev_ids + 1) * 8, ds8)) : nullptr;
+    if (gather && o) CK(cudaMemcpyAsync(b, hpin, o, cudaMemcpyHostToDevice, s), "h2d");
+    if (hg) CK(hb::launch_expand_res(hg, trace->host_ids, hn, const_cast<int32_t *>(d.host.res), s), "expand host res");
+    if (dg) CK(hb::launch_expand_res(dg, trace->dev_ids, dn, const_cast<int32_t *>(d.dev.res), s), "expand dev res");
     CK(cudaGetLastError(), "h2d");
     return run_analysis(ctx, &d, opt, result, out, s);
 }
