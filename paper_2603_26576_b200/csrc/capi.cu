@@ -711,10 +711,17 @@ static int analyze_host_impl(heteff_ctx *ctx, const heteff_trace *trace, const i
     const size_t total = 2 * hb8 + hb4 + hb1 + 2 * db8 + db4 + db1 + hd + dd + hs8 + ds8;
     CK(ensure(ctx->stage, total, false), "alloc staging");
     uint8_t *b = static_cast<uint8_t *>(ctx->stage.p);
-    // small inputs (the drop-in API on ordinary traces, usually pageable numpy memory):
-    // gather every column into one pinned block and issue ONE copy instead of one
-    // driver-staged copy per column; large inputs are copied column by column at PCIe rate
-    const bool gather = total <= ((size_t)8 << 20);
+    // small inputs in pageable memory (the drop-in API on ordinary traces): gather every
+    // column into one pinned block and issue ONE copy instead of one driver-staged copy per
+    // column; large or pinned inputs are copied column by column at PCIe rate
+    bool gather = total <= ((size_t)8 << 20);
+    if (gather) {   // pinned caller memory already copies at full rate: gather pageable memory only
+        const void *probe = hn ? (const void *)trace->host.start : (const void *)trace->dev.start;
+        cudaPointerAttributes pa;
+        if (probe && cudaPointerGetAttributes(&pa, probe) == cudaSuccess && pa.type != cudaMemoryTypeUnregistered)
+            gather = false;
+        cudaGetLastError();
+    }
     if (gather && ctx->in_pin_bytes < total) {
         if (ctx->in_pin) cudaFreeHost(ctx->in_pin);
         ctx->in_pin = nullptr;
