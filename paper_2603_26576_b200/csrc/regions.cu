@@ -61,7 +61,10 @@ constexpr int kHC = 256;             // host records per checkpoint chunk
 #define HB_REG_STAGE 768
 #endif
 constexpr int kDT = HB_REG_DT;       // device tile threads
-constexpr int kDI = 9;               // device records per thread (odd: conflict-free smem)
+#ifndef HB_REG_DI
+#define HB_REG_DI 9   // C4 region call (ms): 7 -> 17.4, 9 -> 15.3, 11 -> 16.8, 13 -> 20.7
+#endif
+constexpr int kDI = HB_REG_DI;       // device records per thread (odd: conflict-free smem)
 constexpr int kDTile = kDT * kDI;    // 1152 device records per tile (= checkpoint chunk)
 constexpr int kST = 1024;            // scan block
 constexpr int kSub = 16;             // device sub-checkpoint every kSub threads (kSub * kDI records)
