@@ -8,6 +8,10 @@ import subprocess
 import sys
 from pathlib import Path
 
+import pytest
+
+from conftest import gpu_available
+
 ROOT = Path(__file__).resolve().parent.parent
 
 KEYS = {"impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
@@ -26,3 +30,21 @@ def test_reference_arm_prints_one_json_line():
     assert d["unit"] == "intervals/s" and d["config"]["workload"] == "c2"
     assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")
+def test_engine_arm_prints_one_json_line_with_roofline_and_e2e():
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--steps", "5", "--warmup", "3", "--e2e-steps", "2",
+                          "--no-cpu-baseline"], capture_output=True, text=True, timeout=900, cwd=str(ROOT))
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert (KEYS - {"impl", "cpu_baseline"}) | {"roofline", "clocks", "gpu_launches"} <= set(d)
+    assert d["gpu_launches"] > 0 and d["value"] > 0 and d["scaling"] == "weak"
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.2 and r["achieved"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0 and d["e2e"]["value"] > 0
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
