@@ -30,6 +30,8 @@
  *   res   i32[count]                      dense resource id in [0, ids)
  *   kind  u8 [count]                      host: 0 useful 1 offload 2 mpi
  *                                         dev : 0 kernel 1 memory   (model.py:24-36)
+ * (or, instead of res, CSR offsets per dense id: heteff_trace.host_seg /
+ * dev_seg, 17 bytes per record).
  * Records must be grouped by res in ascending order and start-sorted
  * within a group -- the reference's canonical order (model.py:74-80,
  * 99-107) once dense ids follow the reference id order.  Violations are
@@ -47,7 +49,7 @@
 extern "C" {
 #endif
 
-#define HETEFF_ABI_VERSION 1
+#define HETEFF_ABI_VERSION 2
 
 typedef enum {
     HETEFF_OK = 0,
@@ -107,6 +109,13 @@ typedef struct {
     int32_t n;                  /* number of distinct declared ranks   */
     int32_t m;                  /* number of distinct declared devices */
     uint64_t host_elapsed_floor;/* max end of host records kept out of the SoA (0 if none) */
+    /* CSR alternative to the res columns (same memory space as the record columns):
+       records [seg[r], seg[r+1]) have dense id r; seg[0] = 0, non-decreasing,
+       seg[ids] = count (host_seg: host_ids + 1 entries, dev_seg: dev_ids + 1).
+       When non-NULL the side's res column is not read (17 instead of 21 bytes per
+       record stream through the analysis: start, end, kind). */
+    const int64_t *host_seg;
+    const int64_t *dev_seg;
 } heteff_trace;
 
 /* heteff_options.flags bits */
@@ -157,6 +166,12 @@ heteff_ctx *heteff_create(int device);
 void heteff_destroy(heteff_ctx *ctx);
 const char *heteff_last_error(const heteff_ctx *ctx);
 
+/* Tuning / test knob: CTAs of the persistent analysis launch (0 = one per SM x
+   resident CTAs, the default).  Any positive value is correct -- the kernel makes
+   progress without co-residency; a grid larger than one wave only runs slower.
+   The environment variable HETEFF_GRID sets the same at heteff_create. */
+int heteff_set_grid(heteff_ctx *ctx, int grid);
+
 /* trace columns in device memory */
 int heteff_analyze(heteff_ctx *ctx, const heteff_trace *trace, const heteff_options *opt,
                    heteff_result *result, const heteff_outputs *out, void *stream);
@@ -165,11 +180,12 @@ int heteff_analyze(heteff_ctx *ctx, const heteff_trace *trace, const heteff_opti
 int heteff_analyze_host(heteff_ctx *ctx, const heteff_trace *trace, const heteff_options *opt,
                         heteff_result *result, const heteff_outputs *out, void *stream);
 
-/* heteff_analyze_host with the res columns given as CSR offsets instead: records
-   [seg[r], seg[r+1]) have dense id r (seg[0] = 0, non-decreasing, seg[ids] = count;
-   host_seg has host_ids + 1 entries, dev_seg dev_ids + 1).  trace->host.res /
-   trace->dev.res are ignored; the ids are expanded on the device, so 4 bytes per
-   record less cross PCIe ("SoA arrays plus CSR offsets").
+/* heteff_analyze_host with the res columns given as CSR offsets (HOST memory) instead:
+   records [seg[r], seg[r+1]) have dense id r (seg[0] = 0, non-decreasing, seg[ids] =
+   count; host_seg has host_ids + 1 entries, dev_seg dev_ids + 1).  trace->host.res /
+   trace->dev.res are ignored; the offsets travel with the columns and the kernel reads
+   them directly, so 4 bytes per record less cross PCIe and stream through HBM
+   ("SoA arrays plus CSR offsets").
    Replaces the same reference entry points as heteff_analyze (compute_report,
    metrics.py:125-154, and the stage functions). */
 int heteff_analyze_host_csr(heteff_ctx *ctx, const heteff_trace *trace, const int64_t *host_seg,

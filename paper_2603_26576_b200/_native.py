@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import threading
 from pathlib import Path
 
 LIB_PATH = Path(os.environ.get("HETEFF_LIB", Path(__file__).resolve().parent / "libheteff_b200.so"))
@@ -38,6 +39,7 @@ class TraceABI(C.Structure):
         ("host_decl", _p), ("dev_decl", _p),
         ("n", C.c_int32), ("m", C.c_int32),
         ("host_elapsed_floor", C.c_uint64),
+        ("host_seg", _p), ("dev_seg", _p),
     ]
 
 
@@ -111,7 +113,7 @@ EXPORTED = (
     "heteff_flatten", "heteff_subtract", "heteff_intersect", "heteff_total_duration",
     "heteff_parse_trace", "heteff_parsed_info", "heteff_parsed_free",
     "heteff_import_events", "heteff_imported_info", "heteff_imported_free",
-    "heteff_analyze_into", "heteff_merge_shards",
+    "heteff_analyze_into", "heteff_merge_shards", "heteff_set_grid",
 )
 
 _lib = None
@@ -180,6 +182,9 @@ def load() -> C.CDLL:
     lib.heteff_merge_shards.restype = C.c_int
     lib.heteff_merge_shards.argtypes = [_p, _p, C.c_int32, C.c_size_t, C.c_int32, C.c_int32, _p, _p, _p,
                                         C.POINTER(Result), C.POINTER(Outputs), _p]
+    if hasattr(lib, "heteff_set_grid"):   # (older builds loaded through HETEFF_LIB for A/B runs)
+        lib.heteff_set_grid.restype = C.c_int
+        lib.heteff_set_grid.argtypes = [_p, C.c_int]
     lib.heteff_generate.restype = C.c_int
     lib.heteff_generate.argtypes = [_p, C.POINTER(GenSide), _p, _p, _p, _p, _p]
     _lib = lib
@@ -190,20 +195,29 @@ class NativeError(RuntimeError):
     """The engine reported a CUDA / argument failure (not a trace property)."""
 
 
-_ctx: dict[int, int] = {}
+_tls = threading.local()
 
 
 def context(device: int | None = None) -> int:
-    """Per-process engine context for ``device`` (default: $HETEFF_DEVICE or 0)."""
+    """Engine context for ``device`` (default: $HETEFF_DEVICE or 0), one per THREAD.
+
+    A context owns device workspace, pinned staging and the grid-wide counters of
+    its launches, so it is not thread-safe (include/heteff_b200.h); ctypes drops
+    the GIL during native calls, so threads sharing one would race.  Each thread
+    gets its own, which keeps the drop-in API as safe to call from threads as
+    the pure-Python reference (SPEC.md's "safe to share")."""
     if device is None:
         device = int(os.environ.get("HETEFF_DEVICE", "0"))
-    if device not in _ctx:
+    cache = getattr(_tls, "ctx", None)
+    if cache is None:
+        cache = _tls.ctx = {}
+    if device not in cache:
         lib = load()
         h = lib.heteff_create(device)
         if not h:
             raise NativeError(f"heteff_create({device}) failed: no usable CUDA device")
-        _ctx[device] = h
-    return _ctx[device]
+        cache[device] = h
+    return cache[device]
 
 
 def last_error(ctx: int) -> str:

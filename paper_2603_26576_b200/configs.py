@@ -66,6 +66,11 @@ class Config:
     def _count(self, per: int, extra: int, lo: int, hi: int) -> int:
         return per * (hi - lo) + max(0, min(hi, extra) - min(lo, extra))
 
+    def block_intervals(self, r0: int, r1: int) -> int:
+        """Records of ranks [r0, r1) and the devices they own (one shard of a rank-sharded run)."""
+        g = self.gpus_per_rank
+        return self.host_side(r0, r1).count + self.dev_side(r0 * g, r1 * g).count
+
     def host_side(self, r0: int = 0, r1: int | None = None) -> GenSideParams:
         r1 = self.n_ranks if r1 is None else r1
         per, extra = self._split(self.host_records, self.n_ranks)

@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/heteff_b200.h"
@@ -55,6 +56,8 @@ struct heteff_ctx {
     // small host-buffer calls: every input column gathered into one pinned block, one H2D
     void *in_pin = nullptr;
     size_t in_pin_bytes = 0;
+    // CSR inputs on the paths that need res columns (error path, K3 sort, regions)
+    DevBuf csr_res;
 };
 
 static int fail(heteff_ctx *ctx, int code, const std::string &msg)
@@ -116,14 +119,25 @@ heteff_ctx *heteff_create(int device)
     cudaEventCreate(&ctx->ev1);
     ctx->grid = hb::analyze_grid(device);
     if (ctx->grid <= 0) { heteff_destroy(ctx); return nullptr; }   // tile geometry does not fit this GPU
+    if (const char *g = getenv("HETEFF_GRID")) {
+        const int v = atoi(g);
+        if (v > 0) ctx->grid = v;
+    }
     return ctx;
+}
+
+int heteff_set_grid(heteff_ctx *ctx, int grid)
+{
+    if (!ctx || grid < 0) return fail(ctx, HETEFF_BAD_ARG, "bad grid");
+    ctx->grid = grid > 0 ? grid : hb::analyze_grid(ctx->device);
+    return HETEFF_OK;
 }
 
 void heteff_destroy(heteff_ctx *ctx)
 {
     if (!ctx) return;
     DevBuf *bufs[] = {&ctx->host_acc, &ctx->dev_acc, &ctx->host_tiles, &ctx->dev_tiles, &ctx->host_out,
-                      &ctx->dev_out, &ctx->lists, &ctx->stage, &ctx->aux, &ctx->sort_ws, &ctx->sorted, &ctx->reg_ws, &ctx->reg_out, &ctx->iv_ws, &ctx->out_blk};
+                      &ctx->dev_out, &ctx->lists, &ctx->stage, &ctx->aux, &ctx->sort_ws, &ctx->sorted, &ctx->reg_ws, &ctx->reg_out, &ctx->iv_ws, &ctx->out_blk, &ctx->csr_res};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->g) cudaFree(ctx->g);
@@ -201,6 +215,9 @@ static int run_once(heteff_ctx *ctx, const heteff_trace *t, const heteff_options
     memset(&p, 0, sizeof(p));
     p.hs = (const u64 *)t->host.start; p.he = (const u64 *)t->host.end; p.hr = t->host.res; p.hk = t->host.kind; p.hn = t->host.count;
     p.ds = (const u64 *)t->dev.start; p.de = (const u64 *)t->dev.end; p.dr = t->dev.res; p.dk = t->dev.kind; p.dn = t->dev.count;
+    p.hseg = t->host_seg; p.dseg = t->dev_seg;
+    if (p.hseg) p.hr = nullptr;
+    if (p.dseg) p.dr = nullptr;
     p.host_ids = t->host_ids; p.dev_ids = t->dev_ids;
     p.host_decl = t->host_decl; p.dev_decl = t->dev_decl;
     p.n = t->n; p.m = t->m;
@@ -210,9 +227,12 @@ static int run_once(heteff_ctx *ctx, const heteff_trace *t, const heteff_options
     p.cap = opt->list_capacity;
     p.host_tiles = ht; p.dev_tiles = dt;
     p.epoch = ctx->epoch;
+    if ((t->host.count > 0 && ((!p.hr && !p.hseg) || (p.hseg && t->host_ids < 1))) ||
+        (t->dev.count > 0 && ((!p.dr && !p.dseg) || (p.dseg && t->dev_ids < 1))))
+        return fail(ctx, HETEFF_BAD_ARG, "records need a res column or CSR offsets");
     const void *cols[8] = {p.hs, p.he, p.hr, p.hk, p.ds, p.de, p.dr, p.dk};
     bool al = true;
-    for (const void *c : cols) al = al && aligned16(c);
+    for (const void *c : cols) al = al && (!c || aligned16(c));
     p.use_tma = al ? 1 : 0;
     u64 *ha = static_cast<u64 *>(ctx->host_acc.p);
     const size_t hc = (size_t)ctx->host_ids_cap;
@@ -256,6 +276,12 @@ static int run_once(heteff_ctx *ctx, const heteff_trace *t, const heteff_options
     CK(cudaStreamSynchronize(s), "analysis");
     if (reinterpret_cast<const hb::ResultDev *>(ctx->out_pin)->status == -1) {
         // some host records overlap: exact overlap findings, then the finalize
+        if (p.hseg) {   // the error-path kernels walk a res column: expand the offsets once
+            CK(ensure(ctx->csr_res, (size_t)t->host.count * 4 + 256, false), "alloc res column");
+            CK(hb::launch_expand_res(p.hseg, t->host_ids, t->host.count, static_cast<int32_t *>(ctx->csr_res.p), s),
+               "expand host res");
+            p.hr = static_cast<const int32_t *>(ctx->csr_res.p);
+        }
         CK(ensure(ctx->aux, (size_t)(ht + 1) * 3 * sizeof(u64), false), "alloc overlap scratch");
         CK(hb::launch_overlap_pass(p, static_cast<u64 *>(ctx->aux.p), s), "launch overlap pass");
         CK(cudaMemcpyAsync(ctx->out_pin, blk, ob_copy, cudaMemcpyDeviceToHost, s), "d2h results");
@@ -331,10 +357,40 @@ static int sort_side(heteff_ctx *ctx, const heteff_records &in, heteff_columns &
     return HETEFF_OK;
 }
 
-static int run_analysis(heteff_ctx *ctx, const heteff_trace *t, const heteff_options *opt, heteff_result *result,
+// CSR offsets -> res columns in ctx->csr_res (for the paths that walk res: K3, regions)
+static int materialize_res(heteff_ctx *ctx, const heteff_trace *t, heteff_trace *o, cudaStream_t s)
+{
+    *o = *t;
+    if (!t->host_seg && !t->dev_seg) return HETEFF_OK;
+    const int64_t hn = t->host_seg ? t->host.count : 0, dn = t->dev_seg ? t->dev.count : 0;
+    const size_t hb = ((size_t)hn * 4 + 255) & ~(size_t)255;
+    CK(ensure(ctx->csr_res, hb + (size_t)dn * 4 + 256, false), "alloc res columns");
+    int32_t *b = static_cast<int32_t *>(ctx->csr_res.p);
+    if (t->host_seg) {
+        CK(hb::launch_expand_res(t->host_seg, t->host_ids, hn, b, s), "expand host res");
+        o->host.res = b;
+        o->host_seg = nullptr;
+    }
+    if (t->dev_seg) {
+        int32_t *d = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(b) + hb);
+        CK(hb::launch_expand_res(t->dev_seg, t->dev_ids, dn, d, s), "expand dev res");
+        o->dev.res = d;
+        o->dev_seg = nullptr;
+    }
+    return HETEFF_OK;
+}
+
+static int run_analysis(heteff_ctx *ctx, const heteff_trace *t0, const heteff_options *opt, heteff_result *result,
                         const heteff_outputs *out, cudaStream_t s)
 {
-    if (!(opt->flags & HETEFF_FLAG_SORT_IF_NEEDED)) return run_once(ctx, t, opt, result, out, s);
+    if (!(opt->flags & HETEFF_FLAG_SORT_IF_NEEDED)) return run_once(ctx, t0, opt, result, out, s);
+    heteff_trace tcol;   // the order check and K3 walk res columns
+    {
+        CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+        const int rc = materialize_res(ctx, t0, &tcol, s);
+        if (rc != HETEFF_OK) return rc;
+    }
+    const heteff_trace *t = &tcol;
     // canonical-order check of both sides (12 B/record), then sort only what needs it
     CK(cudaSetDevice(ctx->device), "cudaSetDevice");
     CK(ensure(ctx->aux, 256, false), "alloc order flags");
@@ -404,6 +460,12 @@ int heteff_analyze_regions(heteff_ctx *ctx, const heteff_trace *t, const heteff_
     o0.mode = HETEFF_MODE_REPORT;
     heteff_result r0{};
     int rc = run_analysis(ctx, t, &o0, &r0, nullptr, s);
+    heteff_trace tcol;   // the region kernels walk res columns
+    if (rc == HETEFF_OK || rc == HETEFF_ANALYSIS_ERROR) {
+        const int mr = materialize_res(ctx, t, &tcol, s);
+        if (mr != HETEFF_OK) return mr;
+        t = &tcol;
+    }
     if (rc != HETEFF_OK && rc != HETEFF_ANALYSIS_ERROR) return rc;
     out->kernel_ms = 0.0;
     if (rg->count == 0) return HETEFF_OK;
@@ -708,7 +770,7 @@ static int analyze_host_impl(heteff_ctx *ctx, const heteff_trace *trace, const i
     const size_t dd = up((size_t)(trace->dev_decl ? trace->dev_ids : 0) * 4);
     const size_t hs8 = hseg ? up(((size_t)trace->host_ids + 1) * 8) : 0;
     const size_t ds8 = dseg ? up(((size_t)trace->dev_ids + 1) * 8) : 0;
-    const size_t total = 2 * hb8 + hb4 + hb1 + 2 * db8 + db4 + db1 + hd + dd + hs8 + ds8;
+    const size_t total = 2 * hb8 + (hseg ? 0 : hb4) + hb1 + 2 * db8 + (dseg ? 0 : db4) + db1 + hd + dd + hs8 + ds8;
     CK(ensure(ctx->stage, total, false), "alloc staging");
     uint8_t *b = static_cast<uint8_t *>(ctx->stage.p);
     // small inputs in pageable memory (the drop-in API on ordinary traces): gather every
@@ -743,11 +805,11 @@ static int analyze_host_impl(heteff_ctx *ctx, const heteff_trace *trace, const i
     };
     d.host.start = static_cast<const uint64_t *>(put(trace->host.start, (size_t)hn * 8, hb8));
     d.host.end = static_cast<const uint64_t *>(put(trace->host.end, (size_t)hn * 8, hb8));
-    d.host.res = static_cast<const int32_t *>(put(hseg ? nullptr : trace->host.res, (size_t)hn * 4, hb4));
+    d.host.res = static_cast<const int32_t *>(put(hseg ? nullptr : trace->host.res, (size_t)hn * 4, hseg ? 0 : hb4));
     d.host.kind = static_cast<const uint8_t *>(put(trace->host.kind, (size_t)hn, hb1));
     d.dev.start = static_cast<const uint64_t *>(put(trace->dev.start, (size_t)dn * 8, db8));
     d.dev.end = static_cast<const uint64_t *>(put(trace->dev.end, (size_t)dn * 8, db8));
-    d.dev.res = static_cast<const int32_t *>(put(dseg ? nullptr : trace->dev.res, (size_t)dn * 4, db4));
+    d.dev.res = static_cast<const int32_t *>(put(dseg ? nullptr : trace->dev.res, (size_t)dn * 4, dseg ? 0 : db4));
     d.dev.kind = static_cast<const uint8_t *>(put(trace->dev.kind, (size_t)dn, db1));
     d.host_decl = trace->host_decl
                       ? static_cast<const int32_t *>(put(trace->host_decl, (size_t)trace->host_ids * 4, hd))
@@ -758,8 +820,10 @@ static int analyze_host_impl(heteff_ctx *ctx, const heteff_trace *trace, const i
     const int64_t *hg = hseg ? static_cast<const int64_t *>(put(hseg, ((size_t)trace->host_ids + 1) * 8, hs8)) : nullptr;
     const int64_t *dg = dseg ? static_cast<const int64_t *>(put(dseg, ((size_t)trace->dev_ids + 1) * 8, ds8)) : nullptr;
     if (gather && o) CK(cudaMemcpyAsync(b, hpin, o, cudaMemcpyHostToDevice, s), "h2d");
-    if (hg) CK(hb::launch_expand_res(hg, trace->host_ids, hn, const_cast<int32_t *>(d.host.res), s), "expand host res");
-    if (dg) CK(hb::launch_expand_res(dg, trace->dev_ids, dn, const_cast<int32_t *>(d.dev.res), s), "expand dev res");
+    d.host_seg = hg;   // the kernel reads the offsets directly (no res column)
+    d.dev_seg = dg;
+    if (hg) d.host.res = nullptr;
+    if (dg) d.dev.res = nullptr;
     CK(cudaGetLastError(), "h2d");
     return run_analysis(ctx, &d, opt, result, out, s);
 }
@@ -767,7 +831,11 @@ static int analyze_host_impl(heteff_ctx *ctx, const heteff_trace *trace, const i
 int heteff_analyze_host(heteff_ctx *ctx, const heteff_trace *trace, const heteff_options *opt, heteff_result *result,
                         const heteff_outputs *out, void *stream)
 {
-    return analyze_host_impl(ctx, trace, nullptr, nullptr, opt, result, out, stream);
+    if (!trace) return fail(ctx, HETEFF_BAD_ARG, "null argument");
+    if ((trace->host_seg && !seg_ok(trace->host_seg, trace->host_ids, trace->host.count)) ||
+        (trace->dev_seg && !seg_ok(trace->dev_seg, trace->dev_ids, trace->dev.count)))
+        return fail(ctx, HETEFF_BAD_ARG, "CSR offsets must start at 0, never decrease and end at the record count");
+    return analyze_host_impl(ctx, trace, trace->host_seg, trace->dev_seg, opt, result, out, stream);
 }
 
 int heteff_analyze_host_csr(heteff_ctx *ctx, const heteff_trace *trace, const int64_t *host_seg,

@@ -99,9 +99,32 @@ struct StageSmem {
 
 constexpr int kRing = 8;       // device-tile epilogue descriptors in flight
 
+// claimed tiles handed from the locator warp to the producer warp
+constexpr int kLoc = 4;
+
+struct LocSlot {
+    int64_t t;
+    int32_t prev_r, r0;
+    u64 prev_s, prev_e;
+    int64_t w[32];
+};
+
+// CSR offset-table sample per side (see csr_locate)
+#ifndef HB_SAMPLES
+#define HB_SAMPLES 256
+#endif
+constexpr int kSamples = HB_SAMPLES;
+
+struct CsrSample {
+    int64_t v[kSamples];
+    int32_t stride, count;
+};
+
 struct TileInfo {
     int64_t t;                 // global tile index, -1 = end
-    int32_t cnt, head, tf, pad;
+    int32_t cnt, head, tf;
+    int32_t hcnt;              // CSR: records of the first resource in the tile (-1: res column)
+    int32_t r0, pad;           // CSR: the first resource
     u64 t0, t1;
 };
 
@@ -116,6 +139,9 @@ struct Ctrl {
     int32_t has_prev[kStages];
     int32_t prev_res[kStages];
     int32_t is_last;
+    int32_t r0[kStages];       // CSR: first resource of the tile, leading records of it
+    int32_t r0cnt[kStages];
+    int32_t uni[kStages];      // CSR tile of ONE resource: its id (the stage's res column is not written), else -1
     u64 prev_start[kStages];
     u64 prev_end[kStages];
     // host tiles: per-stage max end and finished-warp count (smem atomics)
@@ -131,13 +157,23 @@ struct Ctrl {
     u64 w_v1[kStages][kComputeWarps];
     u64 w_mn[kStages][kComputeWarps];
     u64 w_mx[kStages][kComputeWarps];
+    CsrSample csr[2];          // host, device (locator warp only)
+    // locator warp -> producer warp: claimed tiles, located ahead of their refill
+    uint64_t loc_full[kLoc];
+    uint64_t loc_empty[kLoc];
+    LocSlot loc[kLoc];
 };
 
-size_t analyze_smem_bytes() { return sizeof(StageSmem) * kStages + sizeof(Ctrl) + 128; }
+constexpr size_t kSmemBytes = sizeof(StageSmem) * kStages + sizeof(Ctrl) + 128;
+static_assert(kSmemBytes <= 227 * 1024, "stages + control exceed the 227 KB of shared memory per CTA");
+size_t analyze_smem_bytes() { return kSmemBytes; }
 
 // -------------------------------------------------------------------------
 // small helpers
 // -------------------------------------------------------------------------
+// dense id of stage record i: the uniform id of a one-resource CSR tile, else the stage column
+__device__ __forceinline__ int32_t rid(const StageSmem &sm, int32_t uni, int i) { return uni >= 0 ? uni : sm.r[i]; }
+
 __device__ __forceinline__ bool declared(const int32_t *decl, int32_t ids, int32_t n, int32_t r)
 {
     if (r < 0 || r >= ids) return false;
@@ -211,20 +247,25 @@ __device__ __forceinline__ u64 warp_sum(u64 v)
     return v;
 }
 
-// E for device tiles: the explicit window, the max host end (after every CTA
-// finished its host tiles, host_phase_done), or "no clamp" for device-only traces
-// one release per CTA when its compute warps are past their last host tile
-// (tiles are claimed in order): all their host max-end REDs become visible
-__device__ __forceinline__ void host_phase_done(const Params &p)
+// E for device tiles: the explicit window, the max host end (once every host
+// tile is finished), or "no clamp" for device-only traces.  Progress does not
+// depend on co-residency: tiles are claimed in order by running CTAs and host
+// tiles never wait, so every claimed host tile completes whether or not the
+// whole grid is resident (MPS limits, green contexts, co-running kernels, a
+// grid larger than one wave).  A CTA releases the count of host tiles it
+// finished once, when its compute warps move on to device tiles (after the
+// CTA barrier of its first device tile) or end; E is known once the count
+// reaches host_tiles.
+__device__ __forceinline__ void host_tiles_done(const Params &p, int count)
 {
-    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(&p.g->host_done) : "memory");
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(&p.g->host_done), "l"((u64)count) : "memory");
 }
 
 __device__ u64 device_window(const Params &p)
 {
     if (p.mode == kSummarizeDevice) return p.elapsed_ptr ? ld_relaxed(p.elapsed_ptr) : p.elapsed_arg;
     if ((p.mode == kReport || p.mode == kValidate) && p.n >= 1) {
-        while (ld_acquire64(&p.g->host_done) < (u64)gridDim.x) __nanosleep(64);
+        while (ld_acquire64(&p.g->host_done) < (u64)p.host_tiles) __nanosleep(64);
         return umax(ld_relaxed(&p.g->host_max_end), p.host_elapsed_floor);
     }
     return ~0ull;
@@ -254,12 +295,106 @@ __device__ __forceinline__ void issue_bulk(T *dst, const T *src, int cnt, bool t
     if (b) tma_load_1d(dst, src, b, bar, pol);
 }
 
+// ---- CSR resource offsets ("SoA arrays plus CSR offsets") ----
+// Records [seg[r], seg[r+1]) belong to dense id r.  Instead of streaming a
+// 4-byte res column (21 -> 17 B per record), the producer locates each tile's
+// first resource with a 128-ary search over seg (4 probes per lane, one L2
+// round trip per level: 2 levels up to 16384 ids) and writes the tile's res
+// values into shared memory itself -- the compute warps see the same stage as
+// with a res column.
+__device__ __forceinline__ int32_t csr_find(const int64_t *seg, int32_t lo, int32_t hi, int64_t i, int lane)
+{
+    // seg[lo] <= i (seg[0] = 0 <= i); the answer lies in [lo, hi]
+    while (lo < hi) {
+        const int64_t step = ((int64_t)hi - lo + 128) / 128;   // ceil(span / 128)
+        int64_t v[4];
+        bool in[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {   // probe k = 4 lane + q at lo + k step (k = 0: lo itself)
+            const int k = 4 * lane + q;
+            const int64_t pos = lo + (int64_t)k * step;
+            in[q] = k > 0 && pos <= hi;
+            v[q] = in[q] ? __ldg(seg + pos) : 0;
+        }
+        int K = 0;   // seg is non-decreasing: the probes with seg <= i are k = 1..K
+#pragma unroll
+        for (int q = 0; q < 4; ++q) K += __popc(__ballot_sync(0xffffffffu, in[q] && v[q] <= i));
+        const int64_t nlo = lo + (int64_t)K * step;
+        const int64_t nhi = nlo + step - 1;
+        lo = (int32_t)nlo;
+        hi = nhi < hi ? (int32_t)nhi : hi;
+    }
+    return lo;
+}
+
+// window of 32 offsets seg[rc + lane] (past the table: "never")
+__device__ __forceinline__ int64_t csr_window(const int64_t *seg, int32_t ids, int32_t rc, int lane)
+{
+    return (int64_t)rc + lane <= (int64_t)ids ? __ldg(seg + rc + lane) : LLONG_MAX;
+}
+
+// Per-CTA sample of each offset table (shared memory, filled once by the
+// producer warp): samp[j] = seg[j * stride], stride = ceil(ids / kSamples).
+// It narrows a tile's first resource to one stride, so up to kSamples * 64 ids
+// a single L2 round trip (3 offsets per lane) yields both the resource and the
+// 32-offset window after it.
+
+__device__ void csr_sample_fill(const int64_t *seg, int32_t ids, CsrSample &cs, int lane)
+{
+    if (!seg) return;
+    const int32_t stride = ids <= kSamples ? 1 : (int32_t)(((int64_t)ids + kSamples - 1) / kSamples);
+    const int32_t count = (int32_t)(((int64_t)ids + stride - 1) / stride);
+    for (int j = lane; j < count; j += 32) cs.v[j] = __ldg(seg + (int64_t)j * stride);
+    if (lane == 0) { cs.stride = stride; cs.count = count; }
+    __syncwarp();
+}
+
+// the tile's first resource r0 (last r with seg[r] <= base) and w = seg[r0 + lane]
+#ifndef HB_CSR_INLINE
+#define HB_CSR_INLINE __forceinline__
+#endif
+__device__ HB_CSR_INLINE void csr_locate(const int64_t *seg, int32_t ids, const CsrSample &cs, int64_t base,
+                                           int lane, int32_t &r0, int64_t &w)
+{
+    int K = 0;   // samples <= base (a prefix: the table never decreases)
+#pragma unroll
+    for (int q = 0; q < (kSamples + 31) / 32; ++q) {
+        const int j = q * 32 + lane;
+        K += __popc(__ballot_sync(0xffffffffu, j < cs.count && cs.v[j] <= base));
+    }
+    const int32_t lo = (K > 0 ? K - 1 : 0) * cs.stride;
+    const int32_t hi = min(ids - 1, lo + cs.stride - 1);
+    if (cs.stride <= 64) {
+        int64_t v[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {   // seg[lo .. lo + 95]: r0 <= lo + 63, its window <= lo + 94
+            const int64_t pos = (int64_t)lo + lane + 32 * q;
+            v[q] = pos <= ids ? __ldg(seg + pos) : LLONG_MAX;
+        }
+        int k = 0;
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+            k += __popc(__ballot_sync(0xffffffffu, lo + lane + 32 * q <= hi && v[q] <= base));
+        r0 = lo + (k > 0 ? k - 1 : 0);
+        const int e = r0 - lo + lane;   // entry of seg[r0 + lane] in the loaded block
+        const int64_t a = __shfl_sync(0xffffffffu, v[0], e & 31), b = __shfl_sync(0xffffffffu, v[1], e & 31),
+                      c = __shfl_sync(0xffffffffu, v[2], e & 31);
+        w = e < 32 ? a : (e < 64 ? b : c);
+    } else {
+        r0 = csr_find(seg, lo, hi, base, lane);
+        w = csr_window(seg, ids, r0, lane);
+    }
+}
+
 // the record before a tile (for segment / order checks), loaded one
-// iteration ahead of the refill so its latency is hidden
+// iteration ahead of the refill so its latency is hidden; CSR: the tile's
+// first resource and the offset window after it
 struct Claim {
     int64_t t;
     int32_t prev_r;
+    int32_t r0;        // CSR: resource of the tile's first record
     u64 prev_s, prev_e;
+    int64_t w;         // CSR: seg[r0 + lane]
 };
 
 __device__ __forceinline__ int64_t claim_issue(const Params &p, int lane)
@@ -270,25 +405,82 @@ __device__ __forceinline__ int64_t claim_issue(const Params &p, int lane)
 }
 
 // the claimed index (issued earlier by lane 0) and the record before the tile
-__device__ __forceinline__ Claim claim_finish(const Params &p, int64_t issued)
+template <bool CSR>
+__device__ __forceinline__ Claim claim_finish(const Params &p, const CsrSample *cs, int64_t issued, int lane)
 {
     Claim cl;
     cl.t = __shfl_sync(0xffffffffu, issued, 0);
     cl.prev_r = 0;
+    cl.r0 = 0;
     cl.prev_s = 0;
     cl.prev_e = 0;
+    cl.w = LLONG_MAX;
     if (cl.t < p.host_tiles + p.dev_tiles) {
         const bool dev = cl.t >= p.host_tiles;
         const int64_t base = (dev ? cl.t - p.host_tiles : cl.t) * kTile;
+        const int64_t *seg = CSR ? (dev ? p.dseg : p.hseg) : nullptr;
         if (base > 0) {
-            cl.prev_r = __ldcg((dev ? p.dr : p.hr) + base - 1);
             cl.prev_s = __ldcg((dev ? p.ds : p.hs) + base - 1);
             cl.prev_e = __ldcg((dev ? p.de : p.he) + base - 1);
+        }
+        if (seg) {
+            const int32_t ids = dev ? p.dev_ids : p.host_ids;
+            csr_locate(seg, ids, cs[dev ? 1 : 0], base, lane, cl.r0, cl.w);
+            // the record before the tile belongs to r0 unless r0 starts at the tile
+            // (then to an earlier id: only inequality / order against r0 is ever used)
+            const int64_t s0 = __shfl_sync(0xffffffffu, cl.w, 0);
+            cl.prev_r = s0 < base ? cl.r0 : cl.r0 - 1;
+        } else if (base > 0) {
+            cl.prev_r = __ldcg((dev ? p.dr : p.hr) + base - 1);
         }
     }
     return cl;
 }
 
+// r[a, z) = v, 32 lanes, 16-byte stores in the middle (r is 16-byte aligned)
+__device__ __forceinline__ void fill_range(int32_t *r, int a, int z, int32_t v, int lane)
+{
+    const int a4 = min(z, (a + 3) & ~3);
+    if (lane < a4 - a) r[a + lane] = v;
+    const int z4 = max(a4, z & ~3);
+    const int4 vv = make_int4(v, v, v, v);
+    for (int i = a4 + 4 * lane; i < z4; i += 128) *reinterpret_cast<int4 *>(r + i) = vv;
+    if (lane < z - z4) r[z4 + lane] = v;
+}
+
+// CSR: write the tile's res values into the stage; returns the number of leading
+// records of the first resource.  Resource rc + l covers [w_l, w_{l+1}) (l < 31).
+// Offsets that decrease, do not start at 0 or do not end at the record count
+// (where a tile sees them) set `bad` (HETEFF_CONTRACT, never an out-of-range access).
+__device__ HB_CSR_INLINE int csr_fill(const int64_t *seg, int32_t ids, int64_t base, int cnt, int64_t n,
+                                        const Claim &cl, int32_t *r, int lane, bool &bad)
+{
+    int32_t rc = cl.r0;
+    int64_t w = cl.w;
+    int first = -1;
+    bool b = lane == 0 && (w > base || (base == 0 && w != 0));
+    for (;;) {
+        const int64_t wn = __shfl_down_sync(0xffffffffu, w, 1);
+        b = b || (lane < 31 && wn < w);
+        if ((int64_t)rc + lane == (int64_t)ids) b = b || w < base + cnt || (base + cnt == n && w != n);
+        const int lo = (int)(w <= base ? 0 : (w - base < cnt ? w - base : cnt));
+        const int hi = (int)(wn <= base ? 0 : (wn - base < cnt ? wn - base : cnt));
+        if (first < 0) first = __shfl_sync(0xffffffffu, hi, 0);
+        unsigned live = __ballot_sync(0xffffffffu, lane < 31 && hi > lo);
+        while (live) {
+            const int l = __ffs(live) - 1;
+            live &= live - 1;
+            fill_range(r, __shfl_sync(0xffffffffu, lo, l), __shfl_sync(0xffffffffu, hi, l), rc + l, lane);
+        }
+        if (__shfl_sync(0xffffffffu, hi, 30) >= cnt) break;
+        rc += 31;   // 31 resources started inside the tile: the next window
+        w = csr_window(seg, ids, rc, lane);
+    }
+    bad = __any_sync(0xffffffffu, b);
+    return first;
+}
+
+template <bool CSR>
 __device__ void produce(const Params &p, StageSmem *stages, Ctrl *c, int st, const Claim &cl, int lane, uint64_t pol)
 {
     const int64_t t = cl.t;
@@ -307,36 +499,95 @@ __device__ void produce(const Params &p, StageSmem *stages, Ctrl *c, int st, con
     const int cnt = (int)((n - base) < kTile ? (n - base) : kTile);
     const u64 *S = (dev ? p.ds : p.hs) + base;
     const u64 *E = (dev ? p.de : p.he) + base;
-    const int32_t *R = (dev ? p.dr : p.hr) + base;
     const uint8_t *K = (dev ? p.dk : p.hk) + base;
     StageSmem &sm = stages[st];
     const bool tma = p.use_tma != 0;
-    if (lane == 0) {
-        c->tile[st] = t;
-        c->cnt[st] = cnt;
-        c->has_prev[st] = base > 0;
-        c->prev_res[st] = cl.prev_r;
-        c->prev_start[st] = cl.prev_s;
-        c->prev_end[st] = cl.prev_e;
-    }
-    copy_tail(sm.s, S, cnt, tma, lane);
-    copy_tail(sm.e, E, cnt, tma, lane);
-    copy_tail(sm.r, R, cnt, tma, lane);
-    copy_tail(sm.k, K, cnt, tma, lane);
-    __syncwarp();
-    if (lane == 0) {
-        const uint32_t tx =
-            bulk_bytes<u64>(cnt, tma) * 2 + bulk_bytes<int32_t>(cnt, tma) + bulk_bytes<uint8_t>(cnt, tma);
-        if (tx) {
-            fence_proxy_async_smem();   // generic accesses of this stage -> async-proxy writes
-            mbar_arrive_expect_tx(&c->full[st], tx);
-            issue_bulk(sm.s, S, cnt, tma, &c->full[st], pol);
-            issue_bulk(sm.e, E, cnt, tma, &c->full[st], pol);
-            issue_bulk(sm.r, R, cnt, tma, &c->full[st], pol);
-            issue_bulk(sm.k, K, cnt, tma, &c->full[st], pol);
-        } else {
-            mbar_arrive(&c->full[st]);
+    if constexpr (!CSR) {
+        const int32_t *R = (dev ? p.dr : p.hr) + base;
+        copy_tail(sm.s, S, cnt, tma, lane);
+        copy_tail(sm.e, E, cnt, tma, lane);
+        copy_tail(sm.r, R, cnt, tma, lane);
+        copy_tail(sm.k, K, cnt, tma, lane);
+        if (lane == 0) {
+            c->tile[st] = t;
+            c->cnt[st] = cnt;
+            c->has_prev[st] = base > 0;
+            c->prev_res[st] = cl.prev_r;
+            c->prev_start[st] = cl.prev_s;
+            c->prev_end[st] = cl.prev_e;
+            c->r0cnt[st] = -1;
+            c->r0[st] = 0;
+            c->uni[st] = -1;
         }
+        __syncwarp();
+        if (lane == 0) {
+            const uint32_t tx =
+                bulk_bytes<u64>(cnt, tma) * 2 + bulk_bytes<int32_t>(cnt, tma) + bulk_bytes<uint8_t>(cnt, tma);
+            if (tx) {
+                fence_proxy_async_smem();   // generic accesses of this stage -> async-proxy writes
+                mbar_arrive_expect_tx(&c->full[st], tx);
+                issue_bulk(sm.s, S, cnt, tma, &c->full[st], pol);
+                issue_bulk(sm.e, E, cnt, tma, &c->full[st], pol);
+                issue_bulk(sm.r, R, cnt, tma, &c->full[st], pol);
+                issue_bulk(sm.k, K, cnt, tma, &c->full[st], pol);
+            } else {
+                mbar_arrive(&c->full[st]);
+            }
+        }
+    } else {
+        const int64_t *seg = dev ? p.dseg : p.hseg;
+        const int32_t *R = seg ? nullptr : (dev ? p.dr : p.hr) + base;
+        // the bulk copies go out first (tx count only); the full barrier's single
+        // arrival comes after the tails / CSR ids are in shared memory
+        if (lane == 0) {
+            const uint32_t tx = bulk_bytes<u64>(cnt, tma) * 2 + (R ? bulk_bytes<int32_t>(cnt, tma) : 0u) +
+                                bulk_bytes<uint8_t>(cnt, tma);
+            if (tx) {
+                fence_proxy_async_smem();
+                mbar_expect_tx(&c->full[st], tx);
+                issue_bulk(sm.s, S, cnt, tma, &c->full[st], pol);
+                issue_bulk(sm.e, E, cnt, tma, &c->full[st], pol);
+                if (R) issue_bulk(sm.r, R, cnt, tma, &c->full[st], pol);
+                issue_bulk(sm.k, K, cnt, tma, &c->full[st], pol);
+            }
+        }
+        copy_tail(sm.s, S, cnt, tma, lane);
+        copy_tail(sm.e, E, cnt, tma, lane);
+        copy_tail(sm.k, K, cnt, tma, lane);
+        int r0cnt = -1;
+        int32_t uni = -1;
+        if (R) {
+            copy_tail(sm.r, R, cnt, tma, lane);
+        } else {
+            const int32_t ids = dev ? p.dev_ids : p.host_ids;
+            bool bad = false;
+            if (__shfl_sync(0xffffffffu, cl.w, 1) >= base + cnt) {
+                // one resource: the compute warps take its id from uni, the column stays unwritten;
+                // the offset checks of csr_fill on this window
+                const int64_t wn = __shfl_down_sync(0xffffffffu, cl.w, 1);
+                bool b = (lane == 0 && (cl.w > base || (base == 0 && cl.w != 0))) || (lane < 31 && wn < cl.w);
+                if ((int64_t)cl.r0 + lane == (int64_t)ids) b = b || cl.w < base + cnt || (base + cnt == n && cl.w != n);
+                bad = __any_sync(0xffffffffu, b);
+                uni = cl.r0;
+                r0cnt = cnt;
+            } else {
+                r0cnt = csr_fill(seg, ids, base, cnt, n, cl, sm.r, lane, bad);
+            }
+            if (bad && lane == 0) contract(p, dev ? 2u : 1u, base);
+        }
+        if (lane == 0) {
+            c->tile[st] = t;
+            c->cnt[st] = cnt;
+            c->has_prev[st] = base > 0;
+            c->prev_res[st] = cl.prev_r;
+            c->prev_start[st] = cl.prev_s;
+            c->prev_end[st] = cl.prev_e;
+            c->r0cnt[st] = r0cnt;
+            c->r0[st] = cl.r0;
+            c->uni[st] = uni;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&c->full[st]);
     }
 }
 
@@ -522,7 +773,8 @@ __device__ __forceinline__ TileView tile_view(const Ctrl *c, int st, int warp, i
 // starts in the tile -- its tail prefix is then local -- else A), the host
 // max end for E, and hand the producer what its epilogue needs.
 // hand a device tile's epilogue to the epilogue warp (descriptor ring)
-__device__ __forceinline__ void post_info(Ctrl *c, int &k, int64_t t, int cnt, bool head, bool tf, u64 t0, u64 t1)
+__device__ __forceinline__ void post_info(Ctrl *c, int &k, int64_t t, int cnt, bool head, bool tf, u64 t0, u64 t1,
+                                          int st = -1)
 {
     const int slot = k % kRing;
     if (k >= kRing) mbar_wait(&c->info_empty[slot], (uint32_t)(((k / kRing) - 1) & 1));
@@ -531,6 +783,8 @@ __device__ __forceinline__ void post_info(Ctrl *c, int &k, int64_t t, int cnt, b
     x.cnt = cnt;
     x.head = head;
     x.tf = tf;
+    x.hcnt = st >= 0 ? c->r0cnt[st] : -1;
+    x.r0 = st >= 0 ? c->r0[st] : 0;
     x.t0 = t0;
     x.t1 = t1;
     mbar_arrive(&c->info_full[slot]);
@@ -541,10 +795,11 @@ template <bool DEV>
 __device__ __forceinline__ void publish_tile(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc,
                                              const TileView &tv, int &k)
 {
-    const bool head = tc.cnt > 0 && c->has_prev[tc.st] && sm.r[0] == c->prev_res[tc.st];
+    const int32_t uni = c->uni[tc.st];   // CSR tile of one resource: its id (sm.r not filled)
+    const bool head = tc.cnt > 0 && c->has_prev[tc.st] && rid(sm, uni, 0) == c->prev_res[tc.st];
     if (DEV) publish<2>(tv.tf ? p.d_slotP + 4 * tc.lt : p.d_slotA + 4 * tc.lt, p.epoch, tv.t0, tv.t1);
     else publish<1>(tv.tf ? p.h_slotP + 2 * tc.lt : p.h_slotA + 2 * tc.lt, p.epoch, tv.t0, 0);
-    if (head) post_info(c, k, tc.lt, tc.cnt, head, tv.tf, tv.t0, tv.t1);
+    if (head) post_info(c, k, tc.lt, tc.cnt, head, tv.tf, tv.t0, tv.t1, tc.st);
 }
 
 // Emit per-resource totals.  A thread's records split into a head piece
@@ -635,6 +890,7 @@ template <bool DEV>
 __device__ __forceinline__ void phase_a(const StageSmem &sm, const Ctrl *c, int st, int b, int nv, uint32_t &sfm,
                                         u64 &v0, u64 &v1, u64 &mn, u64 &mx)
 {
+    const int32_t uni = c->uni[st];   // CSR tile of one resource: its id (sm.r not filled)
     sfm = 0;
     v0 = v1 = 0;
     mn = ~0ull;
@@ -647,13 +903,13 @@ __device__ __forceinline__ void phase_a(const StageSmem &sm, const Ctrl *c, int 
         pr = c->prev_res[st];
     } else {
         hp = true;
-        pr = sm.r[b - 1];
+        pr = rid(sm, uni, b - 1);
     }
     mn = sm.s[b];
 #pragma unroll kUnrollG
     for (int j = 0; j < kItems; ++j) {
         if (j < nv) {
-            const int32_t r = sm.r[b + j];
+            const int32_t r = rid(sm, uni, b + j);
             const u64 e = sm.e[b + j];
             if ((j == 0 && !hp) || r != pr) {
                 sfm |= 1u << j;
@@ -738,6 +994,7 @@ template <bool DEV>
 __device__ __noinline__ void rescan(const Params &p, const StageSmem &sm, const Ctrl *c, int st, int b, int nv,
                                     u64 x0, u64 E, bool late_check, int64_t gi0)
 {
+    const int32_t uni = c->uni[st];   // CSR tile of one resource: its id (sm.r not filled)
     bool hp = true;
     int32_t pr = 0;
     u64 ps = 0;
@@ -746,15 +1003,15 @@ __device__ __noinline__ void rescan(const Params &p, const StageSmem &sm, const 
         pr = c->prev_res[st];
         ps = c->prev_start[st];
     } else {
-        pr = sm.r[b - 1];
+        pr = rid(sm, uni, b - 1);
         ps = sm.s[b - 1];
     }
-    int32_t r = sm.r[b];
+    int32_t r = rid(sm, uni, b);
     bool decl = DEV ? declared(p.dev_decl, p.dev_ids, p.m, r) : declared(p.host_decl, p.host_ids, p.n, r);
     u64 run = x0;
     int bad = -1;
     for (int j = 0; j < nv; ++j) {
-        const int32_t rj = sm.r[b + j];
+        const int32_t rj = rid(sm, uni, b + j);
         const u64 s = sm.s[b + j], e = sm.e[b + j];
         const bool h = j > 0 || hp;
         if (!h || rj != pr) {
@@ -803,6 +1060,7 @@ __device__ __noinline__ void rescan(const Params &p, const StageSmem &sm, const 
 __device__ __noinline__ u64 host_rare(const Params &p, const StageSmem &sm, const Ctrl *c, int st, int b, int nv,
                                       int64_t gi0)
 {
+    const int32_t uni = c->uni[st];   // CSR tile of one resource: its id (sm.r not filled)
     bool hp = true;
     int32_t pr = 0;
     u64 ps = 0;
@@ -811,7 +1069,7 @@ __device__ __noinline__ u64 host_rare(const Params &p, const StageSmem &sm, cons
         pr = c->prev_res[st];
         ps = c->prev_start[st];
     } else {
-        pr = sm.r[b - 1];
+        pr = rid(sm, uni, b - 1);
         ps = sm.s[b - 1];
     }
     bool decl = false, ovl = false;
@@ -822,15 +1080,15 @@ __device__ __noinline__ u64 host_rare(const Params &p, const StageSmem &sm, cons
     bool pe_known = true;
     {
         int q = b - 1;
-        while (q >= 0 && sm.r[q] == sm.r[b] && sm.s[q] >= sm.e[q]) --q;
-        if (q >= 0 && sm.r[q] == sm.r[b]) pe = sm.e[q];
-        else if (q < 0 && hp && pr == sm.r[b]) {
+        while (q >= 0 && rid(sm, uni, q) == rid(sm, uni, b) && sm.s[q] >= sm.e[q]) --q;
+        if (q >= 0 && rid(sm, uni, q) == rid(sm, uni, b)) pe = sm.e[q];
+        else if (q < 0 && hp && pr == rid(sm, uni, b)) {
             if (b == 0 && c->prev_start[st] < c->prev_end[st]) pe = c->prev_end[st];
             else pe_known = false;
         }
     }
     for (int j = 0; j < nv; ++j) {
-        const int32_t r = sm.r[b + j];
+        const int32_t r = rid(sm, uni, b + j);
         const u64 s = sm.s[b + j], e = sm.e[b + j];
         const bool h = j > 0 || hp;
         const bool start = !h || r != pr;
@@ -917,12 +1175,13 @@ __device__ __forceinline__ bool host_fast32(const StageSmem &sm, int b, int nv, 
 __device__ __forceinline__ bool host_single(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc,
                                             int tid, Phases &ph)
 {
+    const int32_t uni = c->uni[tc.st];   // CSR tile of one resource: its id (sm.r not filled)
     ph.mark();
     const int lane = tid & 31;
     const int b = tid * kItems;
     const int nv = max(0, min(kItems, tc.cnt - b));
     const int64_t gi0 = tc.gbase + (int64_t)b;
-    const int32_t r0 = sm.r[0];
+    const int32_t r0 = rid(sm, uni, 0);
     const bool has_prev = c->has_prev[tc.st] != 0;
     const int32_t prev_res = c->prev_res[tc.st];
     bool cont = true, ovl = false, rare = false;
@@ -975,8 +1234,9 @@ __device__ __forceinline__ bool host_single(const Params &p, const StageSmem &sm
 __device__ __forceinline__ void host_compute(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc,
                                              int tid, Phases &ph)
 {
+    const int32_t uni = c->uni[tc.st];   // CSR tile of one resource: its id (sm.r not filled)
 #ifndef HB_NO_HOST_SINGLE
-    if (tc.cnt > 0 && sm.r[0] == sm.r[tc.cnt - 1] && host_single(p, sm, c, tc, tid, ph)) return;
+    if (tc.cnt > 0 && rid(sm, uni, 0) == rid(sm, uni, tc.cnt - 1) && host_single(p, sm, c, tc, tid, ph)) return;
 #endif
     ph.mark();
     const int warp = tid >> 5, lane = tid & 31;
@@ -993,36 +1253,36 @@ __device__ __forceinline__ void host_compute(const Params &p, const StageSmem &s
             ps = c->prev_start[tc.st];
             pe = c->prev_end[tc.st];
             // previous record not usable: its predecessors are not at hand -> conservative
-            ovl = hp && ps >= pe && sm.r[0] == pr;
+            ovl = hp && ps >= pe && rid(sm, uni, 0) == pr;
         } else {
-            pr = sm.r[b - 1];
+            pr = rid(sm, uni, b - 1);
             ps = sm.s[b - 1];
             int q = b - 1;
-            while (q >= 0 && sm.r[q] == pr && sm.s[q] >= sm.e[q]) --q;   // rare: skip non-usable records
-            if (q >= 0 && sm.r[q] == pr) pe = sm.e[q];
-            else ovl = c->has_prev[tc.st] && sm.r[0] == c->prev_res[tc.st] && sm.r[0] == pr;
+            while (q >= 0 && rid(sm, uni, q) == pr && sm.s[q] >= sm.e[q]) --q;   // rare: skip non-usable records
+            if (q >= 0 && rid(sm, uni, q) == pr) pe = sm.e[q];
+            else ovl = c->has_prev[tc.st] && rid(sm, uni, 0) == c->prev_res[tc.st] && rid(sm, uni, 0) == pr;
         }
     }
     Pieces3 P;
     P.head[0] = P.head[1] = P.head[2] = 0;
     P.cur[0] = P.cur[1] = P.cur[2] = 0;
     P.head_open = true;
-    P.cur_r = P.first_r = nv ? sm.r[b] : 0;
+    P.cur_r = P.first_r = nv ? rid(sm, uni, b) : 0;
     P.cur_decl = nv ? declared(p.host_decl, p.host_ids, p.n, P.cur_r) : false;
     uint32_t sfm = 0;
     bool rare = nv > 0 && !P.cur_decl;
     u64 off = 0, mpi = 0, last = 0, tmax = 0;
     // one rank inside the thread (and in one 2^32 window): the 32-bit fast path
     bool done = false;
-    if (nv > 0 && sm.r[b] == sm.r[b + nv - 1]) {
-        const bool cont = hp && pr == sm.r[b];
+    if (nv > 0 && rid(sm, uni, b) == rid(sm, uni, b + nv - 1)) {
+        const bool cont = hp && pr == rid(sm, uni, b);
         bool r2 = rare, o2 = ovl;
         u64 of2, mp2, la2;
         if (host_fast32(sm, b, nv, cont, ps, pe, r2, o2, of2, mp2, la2)) {
             if (!cont) {
                 sfm = 1u;
                 P.head_open = false;
-                r2 = r2 || (hp && sm.r[b] < pr);   // rank order across the segment start
+                r2 = r2 || (hp && rid(sm, uni, b) < pr);   // rank order across the segment start
             }
             rare = r2;
             ovl = o2;
@@ -1035,7 +1295,7 @@ __device__ __forceinline__ void host_compute(const Params &p, const StageSmem &s
 #pragma unroll kUnrollG
     for (int j = 0; j < kItems; ++j) {
         if (!done && j < nv) {
-            const int32_t r = sm.r[b + j];
+            const int32_t r = rid(sm, uni, b + j);
             const u64 s = sm.s[b + j], e = sm.e[b + j];
             const uint8_t k = sm.k[b + j];
             if ((j == 0 && !hp) || r != pr) {
@@ -1083,7 +1343,7 @@ __device__ __forceinline__ void host_compute(const Params &p, const StageSmem &s
         if (atomicAdd(&c->h_cnt[tc.st], 1u) == kComputeWarps - 1) {
             const u64 m = atomicExch(&c->h_max[tc.st], 0ull);
             c->h_cnt[tc.st] = 0;
-            red_max(&p.g->host_max_end, m);   // host_done is signalled once per CTA (host_phase_done)
+            red_max(&p.g->host_max_end, m);
         }
     }
     ph.add(ph.hemit);
@@ -1098,6 +1358,7 @@ template <typename T>
 __device__ __forceinline__ bool dev_phase_b(const Params &p, const StageSmem &sm, const Ctrl *c, int st, int b, int nv,
                                             uint32_t sfm, const TileView &tv, Pieces3 &P, u64 E)
 {
+    const int32_t uni = c->uni[st];   // CSR tile of one resource: its id (sm.r not filled)
     const Dom<T> D(tv.base, tv.top);
     const T Er = D.rel(E);                  // <= top - base: also catches ends that wrap below the base
     bool rare = E < tv.base;                // every record of the tile ends after E
@@ -1109,7 +1370,7 @@ __device__ __forceinline__ bool dev_phase_b(const Params &p, const StageSmem &sm
         pr = c->prev_res[st];
         rare = rare || (hp && nv > 0 && !(sfm & 1u) && sm.s[0] < c->prev_start[st]);
     } else {
-        pr = sm.r[b - 1];
+        pr = rid(sm, uni, b - 1);
         ps = D.ld(sm.s, b - 1);
     }
 #pragma unroll kUnrollG
@@ -1118,7 +1379,7 @@ __device__ __forceinline__ bool dev_phase_b(const Params &p, const StageSmem &sm
             const T s0 = D.ld(sm.s, b + j), e0 = D.ld(sm.e, b + j);
             const uint8_t k = sm.k[b + j];
             if ((sfm >> j) & 1u) {
-                const int32_t r = sm.r[b + j];
+                const int32_t r = rid(sm, uni, b + j);
                 rare = rare || ((j > 0 || hp) && r < pr);
                 if (j > 0) {
                     P.cur[0] = cK; P.cur[1] = cKM; P.cur[2] = D.abs(runKM);
@@ -1150,13 +1411,13 @@ __device__ __forceinline__ bool dev_phase_b(const Params &p, const StageSmem &sm
     return rare;
 }
 
-// E once per warp (and the CTA's host-phase release), after the CTA barrier
+// E once per warp, after the CTA barrier
 __device__ __forceinline__ u64 device_E(const Params &p, int tid, int lane, u64 &E_cache, bool &E_known,
-                                        bool &signalled)
+                                        int &hpend)
 {
     if (!E_known) {
-        if (tid == 0 && !signalled) host_phase_done(p);   // every warp of this CTA is past its host tiles
-        signalled = true;
+        if (tid == 0 && hpend > 0) host_tiles_done(p, hpend);   // every warp of this CTA is past its host tiles
+        hpend = 0;
         u64 E = 0;
         if (lane == 0) E = device_window(p);
         E_cache = __shfl_sync(0xffffffffu, E, 0);
@@ -1188,9 +1449,10 @@ __device__ __forceinline__ u64 device_E(const Params &p, int tid, int lane, u64 
 // -------------------------------------------------------------------------
 template <bool MERGED>
 __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
-                                           u64 &E_cache, bool &E_known, bool &signalled, int &kq, bool &one_pass,
+                                           u64 &E_cache, bool &E_known, int &hpend, int &kq, bool &one_pass,
                                            Phases &ph)
 {
+    const int32_t uni = c->uni[tc.st];   // CSR tile of one resource: its id (sm.r not filled)
     ph.mark();
     const int warp = tid >> 5, lane = tid & 31;
     const int b = tid * kItems;
@@ -1252,7 +1514,7 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
     ph.add(ph.a);
     bar_compute();
     ph.add(ph.hn2);
-    const u64 E = device_E(p, tid, lane, E_cache, E_known, signalled);
+    const u64 E = device_E(p, tid, lane, E_cache, E_known, hpend);
     // tile-wide: all warps in the window?  cross-warp exclusive prefix
     uint32_t wK = 0, wKM = 0;
     bool fit = true;
@@ -1265,7 +1527,7 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
     if (lane == 0) { xK = 0; xKM = 0; }
     xK = max(xK, xwK);
     xKM = max(xKM, xwKM);
-    const bool head = c->has_prev[tc.st] && sm.r[0] == c->prev_res[tc.st];
+    const bool head = c->has_prev[tc.st] && rid(sm, uni, 0) == c->prev_res[tc.st];
     ph.add(ph.bar);
     if (warp == 0) {
         // tile aggregate (warp 0 only): the max over every warp
@@ -1273,12 +1535,12 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
         if (lane == 0) {
             // a segment starts here iff the tile does not continue one
             publish<2>(!head ? p.d_slotP + 4 * tc.lt : p.d_slotA + 4 * tc.lt, p.epoch, base + tK, base + tKM);
-            if (head) post_info(c, kq, tc.lt, tc.cnt, true, false, base + tK, base + tKM);
+            if (head) post_info(c, kq, tc.lt, tc.cnt, true, false, base + tK, base + tKM, tc.st);
         }
     }
     ph.add(ph.hb);
     const uint32_t Er = E <= base ? 0u : (E - base > 0xffffffffull ? 0xffffffffu : (uint32_t)(E - base));
-    const int32_t r0 = sm.r[0];
+    const int32_t r0 = rid(sm, uni, 0);
     const bool decl = declared(p.dev_decl, p.dev_ids, p.m, r0);
     const bool clamp = nv > 0 && (E < base || runKM > Er);   // some end beyond E
     bool rare = clamp || !decl;
@@ -1361,30 +1623,32 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
 }
 
 __device__ __forceinline__ void dev_general(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
-                                  u64 &E_cache, bool &E_known, bool &signalled, int &k, Phases &ph);
+                                  u64 &E_cache, bool &E_known, int &hpend, int &k, Phases &ph);
 
 __device__ __forceinline__ void dev_compute(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
-                                            u64 &E_cache, bool &E_known, bool &signalled, int &k, bool &one_pass,
+                                            u64 &E_cache, bool &E_known, int &hpend, int &k, bool &one_pass,
                                             Phases &ph)
 {
-    if (tc.cnt > 0 && sm.r[0] == sm.r[tc.cnt - 1]) {
+    const int32_t uni = c->uni[tc.st];   // CSR tile of one resource: its id (sm.r not filled)
+    if (tc.cnt > 0 && rid(sm, uni, 0) == rid(sm, uni, tc.cnt - 1)) {
 #if HB_DEV_SCHED == 0
-        const bool done = dev_single<false>(p, sm, c, tc, tid, E_cache, E_known, signalled, k, one_pass, ph);
+        const bool done = dev_single<false>(p, sm, c, tc, tid, E_cache, E_known, hpend, k, one_pass, ph);
 #elif HB_DEV_SCHED == 1
-        const bool done = dev_single<true>(p, sm, c, tc, tid, E_cache, E_known, signalled, k, one_pass, ph);
+        const bool done = dev_single<true>(p, sm, c, tc, tid, E_cache, E_known, hpend, k, one_pass, ph);
 #else
-        const bool done = one_pass ? dev_single<true>(p, sm, c, tc, tid, E_cache, E_known, signalled, k, one_pass, ph)
-                                   : dev_single<false>(p, sm, c, tc, tid, E_cache, E_known, signalled, k, one_pass, ph);
+        const bool done = one_pass ? dev_single<true>(p, sm, c, tc, tid, E_cache, E_known, hpend, k, one_pass, ph)
+                                   : dev_single<false>(p, sm, c, tc, tid, E_cache, E_known, hpend, k, one_pass, ph);
 #endif
         if (done) return;
     }
-    dev_general(p, sm, c, tc, tid, E_cache, E_known, signalled, k, ph);
+    dev_general(p, sm, c, tc, tid, E_cache, E_known, hpend, k, ph);
 }
 
 // tiles holding several devices (or leaving the 2^32 window): segmented scans, 64-bit fallback
 __device__ __forceinline__ void dev_general(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
-                                  u64 &E_cache, bool &E_known, bool &signalled, int &k, Phases &ph)
+                                  u64 &E_cache, bool &E_known, int &hpend, int &k, Phases &ph)
 {
+    const int32_t uni = c->uni[tc.st];   // CSR tile of one resource: its id (sm.r not filled)
     ph.mark();
     const int warp = tid >> 5, lane = tid & 31;
     const int b = tid * kItems;
@@ -1401,7 +1665,7 @@ __device__ __forceinline__ void dev_general(const Params &p, const StageSmem &sm
     if (lane == 0) { c->w_mn[tc.st][warp] = mn; c->w_mx[tc.st][warp] = mx; }
     ph.add(ph.a);
     bar_compute();
-    device_E(p, tid, lane, E_cache, E_known, signalled);
+    device_E(p, tid, lane, E_cache, E_known, hpend);
     const u64 E = E_cache;
     const bool late_check = (p.mode == kReport || p.mode == kValidate) && p.n >= 1;
     const TileView tv = tile_view(c, tc.st, warp, lane, in_f, in0, in1);
@@ -1411,7 +1675,7 @@ __device__ __forceinline__ void dev_general(const Params &p, const StageSmem &sm
     P.head[0] = P.head[1] = P.head[2] = 0;
     P.cur[0] = P.cur[1] = P.cur[2] = 0;
     P.head_open = !(sfm & 1u);
-    P.cur_r = P.first_r = nv ? sm.r[b] : 0;
+    P.cur_r = P.first_r = nv ? rid(sm, uni, b) : 0;
     P.cur_decl = nv ? declared(p.dev_decl, p.dev_ids, p.m, P.cur_r) : false;
     const bool rare = tv.fits32 ? dev_phase_b<uint32_t>(p, sm, c, tc.st, b, nv, sfm, tv, P, E)
                                 : dev_phase_b<u64>(p, sm, c, tc.st, b, nv, sfm, tv, P, E);
@@ -1434,12 +1698,16 @@ __device__ void dev_epilogue(const Params &p, const TileInfo &x, int lane, u64 &
     // the first 32 records are loaded before the look-back (overlapped round trips)
     const int64_t g0 = x.t * kTile;
     const u64 *S = p.ds + g0, *En = p.de + g0;
-    const int32_t *R = p.dr + g0;
+    const bool csr = x.hcnt >= 0;   // CSR: the head segment is the tile's first hcnt records
+    const int32_t *R = csr ? nullptr : p.dr + g0;
     const uint8_t *K = p.dk + g0;
     int32_t rj = -1;
     u64 sj = 0, ej = 0;
     uint8_t kj = 1;
-    if (lane < x.cnt) { rj = __ldcg(R + lane); sj = __ldcg(S + lane); ej = __ldcg(En + lane); kj = __ldcg(K + lane); }
+    if (lane < x.cnt) {
+        rj = csr ? (lane < x.hcnt ? x.r0 : -1) : __ldcg(R + lane);
+        sj = __ldcg(S + lane); ej = __ldcg(En + lane); kj = __ldcg(K + lane);
+    }
     u64 ck, ckm;
     look_back<2>(p.d_slotA, p.d_slotP, x.t, p.epoch, lane, ck, ckm);
     if (!x.tf && lane == 0) publish<2>(p.d_slotP + 4 * x.t, p.epoch, umax(ck, x.t0), umax(ckm, x.t1));
@@ -1462,7 +1730,10 @@ __device__ void dev_epilogue(const Params &p, const TileInfo &x, int lane, u64 &
         u64 e = 0, s = 0;
         bool kern = false;
         if (in) {
-            if (base > 0) { rj = __ldcg(R + j); sj = __ldcg(S + j); ej = __ldcg(En + j); kj = __ldcg(K + j); }
+            if (base > 0) {
+                rj = csr ? (j < x.hcnt ? x.r0 : -1) : __ldcg(R + j);
+                sj = __ldcg(S + j); ej = __ldcg(En + j); kj = __ldcg(K + j);
+            }
             in = rj == r0;
             const u64 e0 = ej, s0 = sj;
             kern = kj == 0;
@@ -1608,6 +1879,7 @@ __device__ void finalize(const Params &p, u128 *scratch, int tid)
 #ifndef HB_MINB
 #define HB_MINB 1   // resident CTAs per SM the register budget is sized for
 #endif
+template <bool CSR>
 __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid_constant__ Params p)
 {
     extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -1617,6 +1889,10 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
     const int warp = tid >> 5, lane = tid & 31;
 
     if (tid == 0) {
+        for (int s = 0; s < kLoc; ++s) {
+            mbar_init(&c->loc_full[s], 1);
+            mbar_init(&c->loc_empty[s], 1);
+        }
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&c->full[s], 1);
             mbar_init(&c->empty[s], kComputeWarps);
@@ -1632,13 +1908,14 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
     __syncthreads();
     u64 E_cache = 0;
     bool E_known = false;
-    if (warp == kComputeWarps) {
+    if (warp == kComputeWarps && !CSR) {
         // ---------------- TMA warp: keep every stage in flight ----------------
         const uint64_t pol = l2_policy_evict_first();
-        for (int s = 0; s < kStages; ++s) produce(p, stages, c, s, claim_finish(p, claim_issue(p, lane)), lane, pol);
+        for (int s = 0; s < kStages; ++s)
+            produce<false>(p, stages, c, s, claim_finish<false>(p, nullptr, claim_issue(p, lane), lane), lane, pol);
         // claims run ahead of use: the atomic is issued one refill before its index is
         // needed and the previous-record loads one refill before the TMA issue
-        Claim next = claim_finish(p, claim_issue(p, lane));
+        Claim next = claim_finish<false>(p, nullptr, claim_issue(p, lane), lane);
         int64_t pend = claim_issue(p, lane);
         PROF_DECL(pa); PROF_DECL(pb); PROF_DECL(pn);
         for (int it = 0;; ++it) {
@@ -1649,8 +1926,8 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
             mbar_wait(&c->empty[st], ph);
             PROF_ADD(pa, t0);
             t0 = PROF_NOW();
-            produce(p, stages, c, st, next, lane, pol);
-            next = claim_finish(p, pend);
+            produce<false>(p, stages, c, st, next, lane, pol);
+            next = claim_finish<false>(p, nullptr, pend, lane);
             pend = claim_issue(p, lane);
             PROF_ADD(pb, t0);
 #ifdef HB_PROF
@@ -1664,11 +1941,86 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
             o[8] = pa; o[9] = pb; o[12] = pn;
         }
 #endif
-    } else if (warp > kComputeWarps) {
+    } else if (warp == kComputeWarps) {
+        // ---------------- TMA warp (CSR offsets): claimed tiles come located from the
+        // locator warp (ring of kLoc slots); refill every stage as soon as it is free
+        const uint64_t pol = l2_policy_evict_first();
+        int k = 0;
+        auto pop = [&]() {
+            const int slot = k % kLoc;
+            mbar_wait(&c->loc_full[slot], (uint32_t)((k / kLoc) & 1));
+            const LocSlot &x = c->loc[slot];
+            Claim cl;
+            cl.t = x.t;
+            cl.prev_r = x.prev_r;
+            cl.r0 = x.r0;
+            cl.prev_s = x.prev_s;
+            cl.prev_e = x.prev_e;
+            cl.w = x.w[lane];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&c->loc_empty[slot]);
+            ++k;
+            return cl;
+        };
+        for (int s = 0; s < kStages; ++s) produce<true>(p, stages, c, s, pop(), lane, pol);
+        PROF_DECL(pa); PROF_DECL(pb); PROF_DECL(pn);
+        for (int it = 0;; ++it) {
+            const int st = it % kStages;
+            const uint32_t ph = (uint32_t)((it / kStages) & 1);
+            if (c->tile[st] < 0) break;
+            long long t0 = PROF_NOW();
+            mbar_wait(&c->empty[st], ph);
+            PROF_ADD(pa, t0);
+            t0 = PROF_NOW();
+            produce<true>(p, stages, c, st, pop(), lane, pol);
+            PROF_ADD(pb, t0);
+#ifdef HB_PROF
+            ++pn;
+#endif
+            (void)t0;
+        }
+#ifdef HB_PROF
+        if (lane == 0) {
+            unsigned long long *o = hb_prof_buf + blockIdx.x * kProfSlots;
+            o[8] = pa; o[9] = pb; o[12] = pn;
+        }
+#endif
+    } else if (warp == kComputeWarps + 1) {
+        // ---------------- locator warp (CSR only): claim tiles in order, load the record
+        // before each tile and locate its resources, kLoc tiles ahead of the producer.
+        // The producer pops exactly kStages end markers (see its loop), so emit as many.
+        if constexpr (CSR) {
+            csr_sample_fill(p.hseg, p.host_ids, c->csr[0], lane);
+            csr_sample_fill(p.dseg, p.dev_ids, c->csr[1], lane);
+            const int64_t total = p.host_tiles + p.dev_tiles;
+            int64_t pend = claim_issue(p, lane);
+            for (int k = 0, ends = 0; ends < kStages; ++k) {
+                const int slot = k % kLoc;
+                const Claim cl = claim_finish<true>(p, c->csr, pend, lane);
+                if (cl.t < total) pend = claim_issue(p, lane);   // the next claim is in flight meanwhile
+                if (k >= kLoc) mbar_wait(&c->loc_empty[slot], (uint32_t)(((k / kLoc) - 1) & 1));
+                LocSlot &x = c->loc[slot];
+                if (lane == 0) {
+                    x.t = cl.t;   // >= total: end marker
+                    x.prev_r = cl.prev_r;
+                    x.r0 = cl.r0;
+                    x.prev_s = cl.prev_s;
+                    x.prev_e = cl.prev_e;
+                }
+                x.w[lane] = cl.w;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&c->loc_full[slot]);
+                if (cl.t >= total) {
+                    ++ends;
+                    pend = total;   // no more claims: the remaining markers are ends too
+                }
+            }
+        }
+    } else if (warp > kComputeWarps + 1) {
         // ---------------- epilogue warps: look-back + carry fix-up of device tiles ----------------
         // descriptor k goes to epilogue warp k % kEpiWarps
         PROF_DECL(pc); PROF_DECL(pw);
-        for (int k = warp - kComputeWarps - 1;; k += kEpiWarps) {
+        for (int k = warp - kComputeWarps - 2;; k += kEpiWarps) {
             const int slot = k % kRing;
             long long t0 = PROF_NOW();
             mbar_wait(&c->info_full[slot], (uint32_t)((k / kRing) & 1));
@@ -1683,7 +2035,7 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
             (void)t0;
         }
 #ifdef HB_PROF
-        if (lane == 0 && warp == kComputeWarps + 1) {
+        if (lane == 0 && warp == kComputeWarps + 2) {
             unsigned long long *o = hb_prof_buf + blockIdx.x * kProfSlots;
             o[10] = pc; o[11] = pw;
         }
@@ -1692,7 +2044,8 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
         // ---------------- compute warps ----------------
         PROF_DECL(ca); PROF_DECL(cb); PROF_DECL(cn);
         Phases phs;
-        bool signalled = false, one_pass = true;
+        bool one_pass = true;
+        int hpend = 0;   // host tiles finished by this CTA, not yet released
         int k = 0;
         for (int it = 0;; ++it) {
             const int st = it % kStages;
@@ -1708,8 +2061,11 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
             tc.lt = dev ? t - p.host_tiles : t;
             tc.gbase = tc.lt * kTile;
             t0 = PROF_NOW();
-            if (!dev) host_compute(p, stages[st], c, tc, tid, phs);
-            else dev_compute(p, stages[st], c, tc, tid, E_cache, E_known, signalled, k, one_pass, phs);
+            if (!dev) {
+                host_compute(p, stages[st], c, tc, tid, phs);
+                ++hpend;
+            }
+            else dev_compute(p, stages[st], c, tc, tid, E_cache, E_known, hpend, k, one_pass, phs);
 #ifdef HB_PROF
             if (dev) ++phs.dn; else ++phs.hn;
 #endif
@@ -1724,7 +2080,7 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
         bar_compute();   // every compute warp is done with its last tile (incl. host max-end REDs)
         if (tid == 0) {
             for (int e = 0; e < kEpiWarps; ++e) post_info(c, k, -1, 0, false, false, 0, 0);   // end of stream
-            if (!signalled) host_phase_done(p);             // CTAs without device tiles
+            if (hpend > 0) host_tiles_done(p, hpend);       // CTAs that saw no device tile
         }
 #ifdef HB_PROF
         if (tid == 0) {
@@ -1969,9 +2325,11 @@ int analyze_grid(int device)
 {
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    if (cudaFuncSetAttribute(analyze_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(analyze_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)analyze_smem_bytes()) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, analyze_kernel, kThreads, analyze_smem_bytes()) !=
+        cudaFuncSetAttribute(analyze_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)analyze_smem_bytes()) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, analyze_kernel<true>, kThreads, analyze_smem_bytes()) !=
             cudaSuccess) {
         cudaGetLastError();   // not sticky: clear it so later launches report their own status
         return 0;
@@ -1981,7 +2339,9 @@ int analyze_grid(int device)
 
 cudaError_t launch_analyze(const Params &p, int grid, cudaStream_t s)
 {
-    analyze_kernel<<<grid, kThreads, analyze_smem_bytes(), s>>>(p);
+    // CSR offsets on either side: the instantiation with the locator warp
+    if (p.hseg || p.dseg) analyze_kernel<true><<<grid, kThreads, analyze_smem_bytes(), s>>>(p);
+    else analyze_kernel<false><<<grid, kThreads, analyze_smem_bytes(), s>>>(p);
     return cudaGetLastError();
 }
 

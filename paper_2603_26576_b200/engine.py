@@ -141,6 +141,29 @@ class DeviceTrace:
     n: int                 # declared ranks (dense ids 0..n-1)
     m: int                 # declared devices
     host_elapsed_floor: int = 0
+    # CSR offsets (int64 [n + 1] / [m + 1], same memory as the columns): when present the
+    # analysis reads them instead of the res columns -- 17 instead of 21 B per interval
+    h_seg: object = None
+    d_seg: object = None
+
+    def columns_only(self) -> "DeviceTrace":
+        """The same trace addressed through its res columns (no CSR offsets)."""
+        return DeviceTrace(self.h_start, self.h_end, self.h_res, self.h_kind, self.d_start, self.d_end, self.d_res,
+                           self.d_kind, self.n, self.m, self.host_elapsed_floor)
+
+    def with_csr(self) -> "DeviceTrace":
+        """Attach CSR offsets computed from the res columns (ids 0..n-1 / 0..m-1, grouped)."""
+        import torch
+
+        def seg(res, k):
+            out = torch.zeros(k + 1, dtype=torch.int64, device=res.device)
+            if res.numel():
+                torch.cumsum(torch.bincount(res.long(), minlength=k)[:k], 0, out=out[1:])
+            return out
+
+        return DeviceTrace(self.h_start, self.h_end, self.h_res, self.h_kind, self.d_start, self.d_end, self.d_res,
+                           self.d_kind, self.n, self.m, self.host_elapsed_floor, seg(self.h_res, self.n),
+                           seg(self.d_res, self.m))
 
     @property
     def host_count(self) -> int:
@@ -155,11 +178,18 @@ def _dptr(t) -> int | None:
     return t.data_ptr() if t is not None and t.numel() > 0 else None
 
 
+def _segptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
 def device_trace_abi(dt: DeviceTrace) -> N.TraceABI:
+    hs, ds = _segptr(dt.h_seg), _segptr(dt.d_seg)
     return N.TraceABI(
-        N.Records(_dptr(dt.h_start), _dptr(dt.h_end), _dptr(dt.h_res), _dptr(dt.h_kind), dt.host_count),
-        N.Records(_dptr(dt.d_start), _dptr(dt.d_end), _dptr(dt.d_res), _dptr(dt.d_kind), dt.dev_count),
-        dt.n, dt.m, None, None, dt.n, dt.m, dt.host_elapsed_floor)
+        N.Records(_dptr(dt.h_start), _dptr(dt.h_end), None if hs else _dptr(dt.h_res), _dptr(dt.h_kind),
+                  dt.host_count),
+        N.Records(_dptr(dt.d_start), _dptr(dt.d_end), None if ds else _dptr(dt.d_res), _dptr(dt.d_kind),
+                  dt.dev_count),
+        dt.n, dt.m, None, None, dt.n, dt.m, dt.host_elapsed_floor, hs, ds)
 
 
 def analyze_device(dt: DeviceTrace, mode: int = N.MODE_REPORT, elapsed: int = 0, stream: int | None = None,

@@ -86,7 +86,11 @@ def combine(f, dist, tensor_device, recompute_device, metrics_fn, n_max: int | N
 
     parts = gather(buf)
     E = int(max(int(p[0]) for p in parts))
-    status = max(int(p[2]) for p in parts)
+    # a shard whose ranks recorded nothing has local E = 0 and reports ANALYSIS_ERROR on its
+    # own; for the job only the GLOBAL E decides that (metrics.py:136-137), like merge_kernel
+    status = max((int(p[2]) for p in parts if int(p[2]) != 2), default=0)
+    if status == 0 and E == 0:
+        status = 2
     n_of = [int(p[3]) for p in parts]
     m_of = [int(p[4]) for p in parts]
     host_rows = [p[H:H + 4 * n_of[r]].reshape(-1, 4) for r, p in enumerate(parts)]
@@ -144,7 +148,7 @@ class DeviceMerge:
         import torch
 
         from . import _native as N
-        from .engine import _dptr
+        from .engine import device_trace_abi
 
         self.N, self.C, self.dist, self.dt, self.device, self.stream = N, C, dist, dt, device, stream
         self.lib, self.ctx = N.load(), N.context(device)
@@ -157,11 +161,11 @@ class DeviceMerge:
         self.block = torch.zeros(self.bytes // 8, dtype=torch.int64, device=dev)
         self.gathered = torch.zeros(self.world * self.bytes // 8, dtype=torch.int64, device=dev)
         self.e = torch.zeros(1, dtype=torch.int64, device=dev)
-        hrec = N.Records(_dptr(dt.h_start), _dptr(dt.h_end), _dptr(dt.h_res), _dptr(dt.h_kind), dt.host_count)
-        drec = N.Records(_dptr(dt.d_start), _dptr(dt.d_end), _dptr(dt.d_res), _dptr(dt.d_kind), dt.dev_count)
+        full = device_trace_abi(dt)   # res columns or CSR offsets, as the trace carries them
         none = N.Records(None, None, None, None, 0)
-        self.t_host = N.TraceABI(hrec, none, dt.n, 0, None, None, dt.n, 0, dt.host_elapsed_floor)
-        self.t_dev = N.TraceABI(none, drec, 0, dt.m, None, None, 0, dt.m, 0)
+        self.t_host = N.TraceABI(full.host, none, dt.n, 0, None, None, dt.n, 0, dt.host_elapsed_floor,
+                                 full.host_seg, None)
+        self.t_dev = N.TraceABI(none, full.dev, 0, dt.m, None, None, 0, dt.m, 0, None, full.dev_seg)
         self.o_host = N.Options(N.MODE_SUMMARIZE_HOST, 0, 0, 0)
         self.o_dev = N.Options(N.MODE_SUMMARIZE_DEVICE, N.FLAG_ELAPSED_DEVICE_PTR, self.e.data_ptr(), 0)
         self.res = N.Result()

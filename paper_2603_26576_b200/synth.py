@@ -40,7 +40,20 @@ def generate(cfg: Config, r0: int = 0, r1: int | None = None, device: int = 0) -
     lib = N.load()
     ctx = N.context(device)
     stream = torch.cuda.current_stream(device).cuda_stream
-    hs, he, hr, hk = _side(lib, ctx, cfg.host_side(r0, r1), device, stream)
-    ds, de, dr, dk = _side(lib, ctx, cfg.dev_side(r0 * g, r1 * g), device, stream)
+    hp, dp = cfg.host_side(r0, r1), cfg.dev_side(r0 * g, r1 * g)
+    hs, he, hr, hk = _side(lib, ctx, hp, device, stream)
+    ds, de, dr, dk = _side(lib, ctx, dp, device, stream)
     torch.cuda.synchronize(device)
-    return DeviceTrace(hs, he, hr, hk, ds, de, dr, dk, r1 - r0, (r1 - r0) * g)
+    return DeviceTrace(hs, he, hr, hk, ds, de, dr, dk, r1 - r0, (r1 - r0) * g, 0, _seg(hp, device), _seg(dp, device))
+
+
+def _seg(p: GenSideParams, device):
+    """CSR offsets of one generated side: resource i holds per_res records (+1 below extra_below)."""
+    import torch
+
+    gids = torch.arange(p.res_base, p.res_base + p.n_res, dtype=torch.int64)
+    counts = p.per_res + (gids < p.extra_below).to(torch.int64)
+    seg = torch.zeros(p.n_res + 1, dtype=torch.int64)
+    torch.cumsum(counts, 0, out=seg[1:])
+    assert int(seg[-1]) == p.count
+    return seg.to(torch.device("cuda", device))

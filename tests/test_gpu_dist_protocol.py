@@ -29,8 +29,10 @@ def test_merge_protocol_across_processes(world, cfg, ranks, port):
     assert line["identical_to_single_process"], line
 
 
-@pytest.mark.parametrize("cfg,world,port", [("c2", 2, 29621), ("c1", 2, 29622), ("c2", 8, 29623)])
-def test_bench_under_torchrun(cfg, world, port):
+@pytest.mark.parametrize("cfg,world,port,scaling", [("c2", 2, 29621, "weak"), ("c1", 2, 29622, "weak"),
+                                                    ("c2", 8, 29623, "weak"), ("c2", 2, 29624, "strong"),
+                                                    ("c1", 3, 29625, "strong")])
+def test_bench_under_torchrun(cfg, world, port, scaling):
     """bench.py exactly as the driver's scaling run launches it (torchrun, W ranks), with
     the collectives on gloo so the ranks can share the one GPU: it must finish and print
     one JSON line for the whole job."""
@@ -39,11 +41,32 @@ def test_bench_under_torchrun(cfg, world, port):
     env = dict(os.environ, HETEFF_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py"), "--gpus", str(world),
-           "--config", cfg, "--steps", "5", "--warmup", "3", "--e2e-steps", "2", "--no-cpu-baseline"]
+           "--config", cfg, "--scaling", scaling, "--steps", "5", "--warmup", "3", "--e2e-steps", "2",
+           "--no-cpu-baseline"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=str(ROOT), env=env)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, out.stdout
     d = json.loads(lines[0])
-    assert d["n_gpus"] == world and d["value"] > 0 and d["e2e"]["value"] > 0
-    assert d["config"]["intervals"] == world * d["config"]["intervals_per_gpu"]
+    assert d["n_gpus"] == world and d["value"] > 0 and d["e2e"]["value"] > 0 and d["scaling"] == scaling
+    from paper_2603_26576_b200.configs import CONFIGS
+    c = CONFIGS[cfg]
+    if scaling == "weak":   # every rank a C-sized block of a world-times larger trace
+        assert d["config"]["intervals"] == world * d["roofline"]["per_gpu_intervals"] == world * c.intervals
+    else:                   # the one trace split by rank blocks (rank 0's block: the first n // world ranks)
+        assert d["config"]["intervals"] == c.intervals
+        assert d["roofline"]["per_gpu_intervals"] == c.block_intervals(0, c.n_ranks // world)
+
+
+def test_bench_gpus_without_torchrun_spawns_the_ranks():
+    """--gpus N without torchrun re-launches itself under torch.distributed.run (N ranks)."""
+    import os
+
+    env = dict(os.environ, HETEFF_DIST_BACKEND="gloo")
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--config", "c1", "--steps", "3", "--warmup", "3",
+           "--e2e-steps", "1", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=str(ROOT), env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    assert json.loads(lines[0])["n_gpus"] == 2

@@ -23,7 +23,7 @@ def test_library_exports_every_declared_symbol():
     assert declared == set(N.EXPORTED)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.heteff_abi_version() == 1
+    assert lib.heteff_abi_version() == 2
 
 
 def test_library_is_built_for_sm100a():
@@ -38,6 +38,7 @@ def test_struct_layouts_match_the_header():
     # offsets fixed by include/heteff_b200.h (x86-64, natural alignment)
     assert C.sizeof(N.Records) == 40
     assert N.TraceABI.n.offset == 104 and N.TraceABI.host_elapsed_floor.offset == 112
+    assert N.TraceABI.host_seg.offset == 120 and C.sizeof(N.TraceABI) == 136
     assert C.sizeof(N.Options) == 24
     assert N.Result.counts.offset == 128 and C.sizeof(N.Result) == 200
     assert C.sizeof(N.GenSide) == 64

@@ -14,6 +14,8 @@ from paper_2603_26576_b200.synth import generate  # noqa: E402
 
 cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
 dt = generate(cfg)
+if len(sys.argv) > 2 and sys.argv[2] == "col":   # res columns instead of CSR offsets
+    dt = dt.columns_only()
 for _ in range(3):
     f = analyze_device(dt)
 buf = np.zeros(1024 * 32, dtype=np.uint64)
