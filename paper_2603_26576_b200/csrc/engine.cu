@@ -48,7 +48,7 @@
 #define HB_DEV_SCHED 2   // single-segment device tiles: 0 two passes, 1 one pass + correction, 2 per-warp adaptive
 #endif
 #ifndef HB_UNROLL_G
-#define HB_UNROLL_G HB_ITEMS
+#define HB_UNROLL_G 1   // general paths (~10% of tiles): compact code -- the hot set outgrows the 32 KB I-cache
 #endif
 #ifndef HB_UNROLL_A
 #define HB_UNROLL_A HB_ITEMS
@@ -99,17 +99,7 @@ struct StageSmem {
 
 constexpr int kRing = 8;       // device-tile epilogue descriptors in flight
 
-// claimed tiles handed from the locator warp to the producer warp
-constexpr int kLoc = 4;
-
-struct LocSlot {
-    int64_t t;
-    int32_t prev_r, r0;
-    u64 prev_s, prev_e;
-    int64_t w[32];
-};
-
-// CSR offset-table sample per side (see csr_locate)
+// CSR offset-table sample per side (see csr_start)
 #ifndef HB_SAMPLES
 #define HB_SAMPLES 256
 #endif
@@ -118,6 +108,11 @@ constexpr int kSamples = HB_SAMPLES;
 struct CsrSample {
     int64_t v[kSamples];
     int32_t stride, count;
+};
+
+struct ClaimStage {      // shared memory of the CSR claim in flight
+    int64_t v[96];       // seg[lo + i] (stride <= 64), past the table: LLONG_MAX
+    u64 prev[2];         // start, end of the record before the tile
 };
 
 struct TileInfo {
@@ -157,11 +152,8 @@ struct Ctrl {
     u64 w_v1[kStages][kComputeWarps];
     u64 w_mn[kStages][kComputeWarps];
     u64 w_mx[kStages][kComputeWarps];
-    CsrSample csr[2];          // host, device (locator warp only)
-    // locator warp -> producer warp: claimed tiles, located ahead of their refill
-    uint64_t loc_full[kLoc];
-    uint64_t loc_empty[kLoc];
-    LocSlot loc[kLoc];
+    CsrSample csr[2];          // host, device (producer warp only)
+    ClaimStage claim;          // the CSR claim in flight (producer warp only)
 };
 
 constexpr size_t kSmemBytes = sizeof(StageSmem) * kStages + sizeof(Ctrl) + 128;
@@ -350,38 +342,59 @@ __device__ void csr_sample_fill(const int64_t *seg, int32_t ids, CsrSample &cs, 
 }
 
 // the tile's first resource r0 (last r with seg[r] <= base) and w = seg[r0 + lane]
-#ifndef HB_CSR_INLINE
-#define HB_CSR_INLINE __forceinline__
-#endif
-__device__ HB_CSR_INLINE void csr_locate(const int64_t *seg, int32_t ids, const CsrSample &cs, int64_t base,
-                                           int lane, int32_t &r0, int64_t &w)
+// A claimed tile in flight (CSR): its offset-window and previous-record loads are
+// issued as cp.async copies into shared memory when the claim resolves and read one
+// refill later, so the L2 round trip overlaps the producer's wait for the next free
+// stage and no register stays live across it.
+struct PendClaim {
+    int64_t t;
+    int32_t lo, hi;      // the tile's first resource lies in [lo, hi]
+};
+
+__device__ __forceinline__ void cp_async8(void *dst, const void *src)
 {
-    int K = 0;   // samples <= base (a prefix: the table never decreases)
-#pragma unroll
-    for (int q = 0; q < (kSamples + 31) / 32; ++q) {
-        const int j = q * 32 + lane;
-        K += __popc(__ballot_sync(0xffffffffu, j < cs.count && cs.v[j] <= base));
-    }
-    const int32_t lo = (K > 0 ? K - 1 : 0) * cs.stride;
-    const int32_t hi = min(ids - 1, lo + cs.stride - 1);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// stage 1: narrow with the CTA's sample (shared memory), issue the offset copies
+__device__ __forceinline__ void csr_start(const int64_t *seg, int32_t ids, const CsrSample &cs, int64_t base,
+                                          int lane, PendClaim &pc, ClaimStage &st)
+{
+    // samples <= base form a prefix (the table never decreases): count them in two
+    // rounds, every 8th sample first, then the 8 after the last one that passed
+    static_assert(kSamples == 256, "two-round sample scan");
+    const int j1 = 8 * lane;
+    const int K1 = __popc(__ballot_sync(0xffffffffu, j1 < cs.count && cs.v[j1] <= base));
+    const int g = K1 > 0 ? K1 - 1 : 0;
+    const int j2 = 8 * g + (lane & 7);
+    const int K2 = __popc(__ballot_sync(0xffffffffu, lane < 8 && j2 < cs.count && cs.v[j2] <= base));
+    const int K = 8 * g + K2;   // K1 = 0 only if sample 0 > base (a broken table): then K2 = 0 too
+    pc.lo = (K > 0 ? K - 1 : 0) * cs.stride;
+    pc.hi = min(ids - 1, pc.lo + cs.stride - 1);
     if (cs.stride <= 64) {
-        int64_t v[3];
 #pragma unroll
         for (int q = 0; q < 3; ++q) {   // seg[lo .. lo + 95]: r0 <= lo + 63, its window <= lo + 94
-            const int64_t pos = (int64_t)lo + lane + 32 * q;
-            v[q] = pos <= ids ? __ldg(seg + pos) : LLONG_MAX;
+            const int64_t pos = (int64_t)pc.lo + lane + 32 * q;
+            if (pos <= ids) cp_async8(&st.v[lane + 32 * q], seg + pos);
+            else st.v[lane + 32 * q] = LLONG_MAX;
         }
+    }
+}
+
+// stage 2: the first resource r0 (last r with seg[r] <= base) and w = seg[r0 + lane]
+__device__ __forceinline__ void csr_finish(const int64_t *seg, int32_t ids, const CsrSample &cs, int64_t base,
+                                           int lane, const PendClaim &pc, const ClaimStage &st, int32_t &r0,
+                                           int64_t &w)
+{
+    if (cs.stride <= 64) {
         int k = 0;
 #pragma unroll
         for (int q = 0; q < 3; ++q)
-            k += __popc(__ballot_sync(0xffffffffu, lo + lane + 32 * q <= hi && v[q] <= base));
-        r0 = lo + (k > 0 ? k - 1 : 0);
-        const int e = r0 - lo + lane;   // entry of seg[r0 + lane] in the loaded block
-        const int64_t a = __shfl_sync(0xffffffffu, v[0], e & 31), b = __shfl_sync(0xffffffffu, v[1], e & 31),
-                      c = __shfl_sync(0xffffffffu, v[2], e & 31);
-        w = e < 32 ? a : (e < 64 ? b : c);
-    } else {
-        r0 = csr_find(seg, lo, hi, base, lane);
+            k += __popc(__ballot_sync(0xffffffffu, pc.lo + lane + 32 * q <= pc.hi && st.v[lane + 32 * q] <= base));
+        r0 = pc.lo + (k > 0 ? k - 1 : 0);
+        w = st.v[r0 - pc.lo + lane];   // seg[r0 + lane]: r0 - lo <= 63
+    } else {   // > kSamples * 64 ids: a 128-ary search inside the stride
+        r0 = csr_find(seg, pc.lo, pc.hi, base, lane);
         w = csr_window(seg, ids, r0, lane);
     }
 }
@@ -405,8 +418,7 @@ __device__ __forceinline__ int64_t claim_issue(const Params &p, int lane)
 }
 
 // the claimed index (issued earlier by lane 0) and the record before the tile
-template <bool CSR>
-__device__ __forceinline__ Claim claim_finish(const Params &p, const CsrSample *cs, int64_t issued, int lane)
+__device__ __forceinline__ Claim claim_finish(const Params &p, int64_t issued)
 {
     Claim cl;
     cl.t = __shfl_sync(0xffffffffu, issued, 0);
@@ -418,22 +430,65 @@ __device__ __forceinline__ Claim claim_finish(const Params &p, const CsrSample *
     if (cl.t < p.host_tiles + p.dev_tiles) {
         const bool dev = cl.t >= p.host_tiles;
         const int64_t base = (dev ? cl.t - p.host_tiles : cl.t) * kTile;
-        const int64_t *seg = CSR ? (dev ? p.dseg : p.hseg) : nullptr;
         if (base > 0) {
+            cl.prev_r = __ldcg((dev ? p.dr : p.hr) + base - 1);
             cl.prev_s = __ldcg((dev ? p.ds : p.hs) + base - 1);
             cl.prev_e = __ldcg((dev ? p.de : p.he) + base - 1);
         }
+    }
+    return cl;
+}
+
+// CSR claims, two stages: start (index resolved, copies issued) -> done (one refill later)
+__device__ __forceinline__ PendClaim claim_start(const Params &p, const CsrSample *cs, ClaimStage &st,
+                                                 int64_t issued, int lane)
+{
+    PendClaim pc;
+    pc.t = __shfl_sync(0xffffffffu, issued, 0);
+    pc.lo = pc.hi = 0;
+    if (pc.t < p.host_tiles + p.dev_tiles) {
+        const bool dev = pc.t >= p.host_tiles;
+        const int64_t base = (dev ? pc.t - p.host_tiles : pc.t) * kTile;
+        if (base > 0 && lane < 2) cp_async8(&st.prev[lane], (lane ? (dev ? p.de : p.he) : (dev ? p.ds : p.hs)) + base - 1);
+        const int64_t *seg = dev ? p.dseg : p.hseg;
+        if (seg) csr_start(seg, dev ? p.dev_ids : p.host_ids, cs[dev ? 1 : 0], base, lane, pc, st);
+        else if (base > 0) pc.lo = __ldcg((dev ? p.dr : p.hr) + base - 1);   // a side with a res column
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    return pc;
+}
+
+__device__ __forceinline__ Claim claim_done(const Params &p, const CsrSample *cs, const PendClaim &pc,
+                                            const ClaimStage &st, int lane)
+{
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    Claim cl;
+    cl.t = pc.t;
+    cl.prev_r = 0;
+    cl.r0 = 0;
+    cl.prev_s = 0;
+    cl.prev_e = 0;
+    cl.w = LLONG_MAX;
+    if (pc.t < p.host_tiles + p.dev_tiles) {
+        const bool dev = pc.t >= p.host_tiles;
+        const int64_t base = (dev ? pc.t - p.host_tiles : pc.t) * kTile;
+        if (base > 0) {
+            cl.prev_s = st.prev[0];
+            cl.prev_e = st.prev[1];
+        }
+        const int64_t *seg = dev ? p.dseg : p.hseg;
         if (seg) {
-            const int32_t ids = dev ? p.dev_ids : p.host_ids;
-            csr_locate(seg, ids, cs[dev ? 1 : 0], base, lane, cl.r0, cl.w);
+            csr_finish(seg, dev ? p.dev_ids : p.host_ids, cs[dev ? 1 : 0], base, lane, pc, st, cl.r0, cl.w);
             // the record before the tile belongs to r0 unless r0 starts at the tile
             // (then to an earlier id: only inequality / order against r0 is ever used)
             const int64_t s0 = __shfl_sync(0xffffffffu, cl.w, 0);
             cl.prev_r = s0 < base ? cl.r0 : cl.r0 - 1;
-        } else if (base > 0) {
-            cl.prev_r = __ldcg((dev ? p.dr : p.hr) + base - 1);
+        } else {
+            cl.prev_r = pc.lo;
         }
     }
+    __syncwarp();   // every lane has read the stage before the next claim's copies land
     return cl;
 }
 
@@ -452,7 +507,7 @@ __device__ __forceinline__ void fill_range(int32_t *r, int a, int z, int32_t v, 
 // records of the first resource.  Resource rc + l covers [w_l, w_{l+1}) (l < 31).
 // Offsets that decrease, do not start at 0 or do not end at the record count
 // (where a tile sees them) set `bad` (HETEFF_CONTRACT, never an out-of-range access).
-__device__ HB_CSR_INLINE int csr_fill(const int64_t *seg, int32_t ids, int64_t base, int cnt, int64_t n,
+__device__ __noinline__ int csr_fill(const int64_t *seg, int32_t ids, int64_t base, int cnt, int64_t n,
                                         const Claim &cl, int32_t *r, int lane, bool &bad)
 {
     int32_t rc = cl.r0;
@@ -1889,10 +1944,6 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
     const int warp = tid >> 5, lane = tid & 31;
 
     if (tid == 0) {
-        for (int s = 0; s < kLoc; ++s) {
-            mbar_init(&c->loc_full[s], 1);
-            mbar_init(&c->loc_empty[s], 1);
-        }
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&c->full[s], 1);
             mbar_init(&c->empty[s], kComputeWarps);
@@ -1912,10 +1963,10 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
         // ---------------- TMA warp: keep every stage in flight ----------------
         const uint64_t pol = l2_policy_evict_first();
         for (int s = 0; s < kStages; ++s)
-            produce<false>(p, stages, c, s, claim_finish<false>(p, nullptr, claim_issue(p, lane), lane), lane, pol);
+            produce<false>(p, stages, c, s, claim_finish(p, claim_issue(p, lane)), lane, pol);
         // claims run ahead of use: the atomic is issued one refill before its index is
         // needed and the previous-record loads one refill before the TMA issue
-        Claim next = claim_finish<false>(p, nullptr, claim_issue(p, lane), lane);
+        Claim next = claim_finish(p, claim_issue(p, lane));
         int64_t pend = claim_issue(p, lane);
         PROF_DECL(pa); PROF_DECL(pb); PROF_DECL(pn);
         for (int it = 0;; ++it) {
@@ -1927,7 +1978,7 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
             PROF_ADD(pa, t0);
             t0 = PROF_NOW();
             produce<false>(p, stages, c, st, next, lane, pol);
-            next = claim_finish<false>(p, nullptr, pend, lane);
+            next = claim_finish(p, pend);
             pend = claim_issue(p, lane);
             PROF_ADD(pb, t0);
 #ifdef HB_PROF
@@ -1942,27 +1993,23 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
         }
 #endif
     } else if (warp == kComputeWarps) {
-        // ---------------- TMA warp (CSR offsets): claimed tiles come located from the
-        // locator warp (ring of kLoc slots); refill every stage as soon as it is free
+        // ---------------- TMA warp (CSR offsets): claims run two refills ahead -- the
+        // atomic, then the offset-window copies (resolved one refill later) -- so the
+        // resource lookup never delays a refill
         const uint64_t pol = l2_policy_evict_first();
-        int k = 0;
-        auto pop = [&]() {
-            const int slot = k % kLoc;
-            mbar_wait(&c->loc_full[slot], (uint32_t)((k / kLoc) & 1));
-            const LocSlot &x = c->loc[slot];
-            Claim cl;
-            cl.t = x.t;
-            cl.prev_r = x.prev_r;
-            cl.r0 = x.r0;
-            cl.prev_s = x.prev_s;
-            cl.prev_e = x.prev_e;
-            cl.w = x.w[lane];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&c->loc_empty[slot]);
-            ++k;
-            return cl;
-        };
-        for (int s = 0; s < kStages; ++s) produce<true>(p, stages, c, s, pop(), lane, pol);
+        csr_sample_fill(p.hseg, p.host_ids, c->csr[0], lane);
+        csr_sample_fill(p.dseg, p.dev_ids, c->csr[1], lane);
+        for (int s = 0; s < kStages; ++s) {
+            const PendClaim pc = claim_start(p, c->csr, c->claim, claim_issue(p, lane), lane);
+            produce<true>(p, stages, c, s, claim_done(p, c->csr, pc, c->claim, lane), lane, pol);
+        }
+        Claim next;
+        {
+            const PendClaim pc = claim_start(p, c->csr, c->claim, claim_issue(p, lane), lane);
+            next = claim_done(p, c->csr, pc, c->claim, lane);
+        }
+        PendClaim mid = claim_start(p, c->csr, c->claim, claim_issue(p, lane), lane);
+        int64_t pend = claim_issue(p, lane);
         PROF_DECL(pa); PROF_DECL(pb); PROF_DECL(pn);
         for (int it = 0;; ++it) {
             const int st = it % kStages;
@@ -1972,7 +2019,10 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
             mbar_wait(&c->empty[st], ph);
             PROF_ADD(pa, t0);
             t0 = PROF_NOW();
-            produce<true>(p, stages, c, st, pop(), lane, pol);
+            produce<true>(p, stages, c, st, next, lane, pol);
+            next = claim_done(p, c->csr, mid, c->claim, lane);
+            mid = claim_start(p, c->csr, c->claim, pend, lane);
+            pend = claim_issue(p, lane);
             PROF_ADD(pb, t0);
 #ifdef HB_PROF
             ++pn;
@@ -1985,42 +2035,11 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
             o[8] = pa; o[9] = pb; o[12] = pn;
         }
 #endif
-    } else if (warp == kComputeWarps + 1) {
-        // ---------------- locator warp (CSR only): claim tiles in order, load the record
-        // before each tile and locate its resources, kLoc tiles ahead of the producer.
-        // The producer pops exactly kStages end markers (see its loop), so emit as many.
-        if constexpr (CSR) {
-            csr_sample_fill(p.hseg, p.host_ids, c->csr[0], lane);
-            csr_sample_fill(p.dseg, p.dev_ids, c->csr[1], lane);
-            const int64_t total = p.host_tiles + p.dev_tiles;
-            int64_t pend = claim_issue(p, lane);
-            for (int k = 0, ends = 0; ends < kStages; ++k) {
-                const int slot = k % kLoc;
-                const Claim cl = claim_finish<true>(p, c->csr, pend, lane);
-                if (cl.t < total) pend = claim_issue(p, lane);   // the next claim is in flight meanwhile
-                if (k >= kLoc) mbar_wait(&c->loc_empty[slot], (uint32_t)(((k / kLoc) - 1) & 1));
-                LocSlot &x = c->loc[slot];
-                if (lane == 0) {
-                    x.t = cl.t;   // >= total: end marker
-                    x.prev_r = cl.prev_r;
-                    x.r0 = cl.r0;
-                    x.prev_s = cl.prev_s;
-                    x.prev_e = cl.prev_e;
-                }
-                x.w[lane] = cl.w;
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&c->loc_full[slot]);
-                if (cl.t >= total) {
-                    ++ends;
-                    pend = total;   // no more claims: the remaining markers are ends too
-                }
-            }
-        }
-    } else if (warp > kComputeWarps + 1) {
+    } else if (warp > kComputeWarps) {
         // ---------------- epilogue warps: look-back + carry fix-up of device tiles ----------------
         // descriptor k goes to epilogue warp k % kEpiWarps
         PROF_DECL(pc); PROF_DECL(pw);
-        for (int k = warp - kComputeWarps - 2;; k += kEpiWarps) {
+        for (int k = warp - kComputeWarps - 1;; k += kEpiWarps) {
             const int slot = k % kRing;
             long long t0 = PROF_NOW();
             mbar_wait(&c->info_full[slot], (uint32_t)((k / kRing) & 1));
@@ -2035,7 +2054,7 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
             (void)t0;
         }
 #ifdef HB_PROF
-        if (lane == 0 && warp == kComputeWarps + 2) {
+        if (lane == 0 && warp == kComputeWarps + 1) {
             unsigned long long *o = hb_prof_buf + blockIdx.x * kProfSlots;
             o[10] = pc; o[11] = pw;
         }
@@ -2339,7 +2358,7 @@ int analyze_grid(int device)
 
 cudaError_t launch_analyze(const Params &p, int grid, cudaStream_t s)
 {
-    // CSR offsets on either side: the instantiation with the locator warp
+    // CSR offsets on either side: the instantiation that reads them
     if (p.hseg || p.dseg) analyze_kernel<true><<<grid, kThreads, analyze_smem_bytes(), s>>>(p);
     else analyze_kernel<false><<<grid, kThreads, analyze_smem_bytes(), s>>>(p);
     return cudaGetLastError();

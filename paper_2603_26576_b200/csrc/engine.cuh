@@ -23,7 +23,7 @@ typedef unsigned long long u64;
 constexpr int kComputeWarps = HB_WARPS;
 constexpr int kComputeThreads = kComputeWarps * 32;
 constexpr int kEpiWarps = HB_EPI;                      // look-back / carry fix-up warps
-constexpr int kThreads = kComputeThreads + 32 * (2 + kEpiWarps);   // + TMA, locator, epilogue warps
+constexpr int kThreads = kComputeThreads + 32 * (1 + kEpiWarps);   // + TMA warp + epilogue warps
 constexpr int kItems = HB_ITEMS;                       // odd: conflict-free blocked smem reads
 constexpr int kTile = kComputeThreads * kItems;        // records per tile (multiple of 16)
 constexpr int kStages = HB_STAGES;

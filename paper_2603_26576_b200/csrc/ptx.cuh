@@ -61,6 +61,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
     }
 }
 
+// for warps far ahead of their consumer (locator, epilogue): sleep between polls so
+// the waiting warp fetches no instructions (its SM sub-partition's instruction cache
+// stays with the compute warps)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, unsigned ns)
+{
+    while (!mbar_try_wait(bar, parity)) __nanosleep(ns);
+}
+
 // generic-proxy smem accesses -> subsequent async-proxy (TMA) writes
 __device__ __forceinline__ void fence_proxy_async_smem()
 {

@@ -25,7 +25,7 @@ P = buf[: k].reshape(-1, 32)
 P = P[P[:, 2] > 0]
 names = {0: ("c.wait_full", 2), 1: ("c.compute", 2), 16: ("host.loop+devpub", 18), 17: ("host.emit+max", 18),
          3: ("dev.phaseA", 19), 20: ("dev.barrier", 19), 4: ("dev.E+view", 19), 5: ("dev.phaseB", 19), 6: ("dev.emit", 19),
-         8: ("tma.wait_empty", 12), 9: ("tma.produce", 12), 10: ("epi.work", 19), 11: ("epi.wait_info", 19)}
+         8: ("tma.wait_empty", 12), 9: ("tma.produce", 12), 13: ("tma.claim_done", 12), 14: ("tma.claim_start", 12), 10: ("epi.work", 19), 11: ("epi.wait_info", 19)}
 print(f"{cfg.name}: kernel {f.kernel_ms:.3f} ms, CTAs {P.shape[0]}, tiles/CTA {P[:, 2].mean():.1f}")
 print(f"  host tiles/CTA {P[:, 18].mean():.1f}, device tiles/CTA {P[:, 19].mean():.1f}")
 print(f"  single-segment device tiles run in one pass (warp 0): {P[:, 21].mean():.1f}/CTA, needing a carry fix: {P[:, 22].mean():.1f}/CTA")
