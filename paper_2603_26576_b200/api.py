@@ -91,9 +91,12 @@ def _run(trace: Trace, mode: int, elapsed: int = 0, want_lists: bool = True):
     return packed, f
 
 
-def _invalid(trace: Trace, f: Findings) -> bool:
+def _invalid(trace: Trace, packed: PackedTrace, f: Findings) -> bool:
+    """Errors the reference's validate() reports (model.py:160-230): declaration errors,
+    kernel findings, and records the packer quarantined (non-int / negative / beyond-u64
+    timestamps never reach the kernel, model.py:140-157)."""
     decl_errors, _ = declaration_messages(trace)
-    return bool(decl_errors) or f.status == N.INVALID_TRACE
+    return bool(decl_errors) or bool(packed.host_q) or bool(packed.dev_q) or f.status == N.INVALID_TRACE
 
 
 def _raise_invalid(trace: Trace, packed: PackedTrace, f: Findings, report: ValidationReport | None = None):
@@ -129,7 +132,7 @@ def validate(trace: Trace) -> ValidationReport:
 def summarize_host(trace: Trace) -> tuple[list[HostSummary], int]:
     """Per-rank totals and the elapsed time E; ``summarize.py:57-92``."""
     packed, f = _run(trace, N.MODE_SUMMARIZE_HOST, want_lists=False)
-    if _invalid(trace, f):
+    if _invalid(trace, packed, f):
         _, f = _run(trace, N.MODE_VALIDATE)
         _raise_invalid(trace, packed, f)
     return _host_summaries(trace, f), f.elapsed
@@ -140,7 +143,7 @@ def summarize_device(trace: Trace, elapsed: int) -> tuple[list[DeviceSummary], l
     if elapsed <= 0:
         raise ValueError(f"elapsed must be positive, got {elapsed}")
     packed, f = _run(trace, N.MODE_SUMMARIZE_DEVICE, min(elapsed, U64_MAX), want_lists=False)
-    if _invalid(trace, f):
+    if _invalid(trace, packed, f):
         _, f = _run(trace, N.MODE_VALIDATE)
         _raise_invalid(trace, packed, f)
     return _device_summaries(trace, f, elapsed), clamp_warnings(trace, f, elapsed)
@@ -153,12 +156,20 @@ def _u64_rows(rows) -> np.ndarray:
         raise OverflowError("summary durations must fit in 64 bits") from e
 
 
+def _u64_elapsed(elapsed: int) -> None:
+    """The metric kernels take E as a u64 (include/heteff_b200.h); a larger E is refused
+    loudly rather than truncated by the C call."""
+    if elapsed > U64_MAX:
+        raise OverflowError("elapsed must fit in 64 bits")
+
+
 def host_metrics(summaries: list[HostSummary], elapsed: int) -> HostMetrics:
     """Host tree from per-rank totals; ``metrics.py:66-93``."""
     if len(summaries) < 1:
         raise ValueError("host_metrics requires at least one rank")
     if elapsed <= 0:
         raise ValueError(f"elapsed must be positive, got {elapsed}")
+    _u64_elapsed(elapsed)
     rows = _u64_rows([(s.d_useful, s.d_offload, s.d_mpi, s.span_end) for s in summaries])
     return HostMetrics(*metrics_from_summaries(rows, elapsed, host_side=True))
 
@@ -169,6 +180,7 @@ def device_metrics(summaries: list[DeviceSummary], elapsed: int) -> DeviceMetric
         raise ValueError("device_metrics requires at least one device")
     if elapsed <= 0:
         raise ValueError(f"elapsed must be positive, got {elapsed}")
+    _u64_elapsed(elapsed)
     rows = _u64_rows([(s.d_kernel, s.d_memory, s.d_idle, 0) for s in summaries])
     return DeviceMetrics(*metrics_from_summaries(rows, elapsed, host_side=False))
 

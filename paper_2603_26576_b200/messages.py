@@ -42,10 +42,22 @@ def _canon(pos: np.ndarray, index: np.ndarray | None) -> list[int]:
     return [int(index[x]) for x in pos]
 
 
+def _after(end, host_elapsed) -> bool:
+    """``end > host_elapsed`` as the reference evaluates it (model.py:224); ends the
+    reference itself cannot compare are not late."""
+    try:
+        return bool(end > host_elapsed)
+    except TypeError:
+        return False
+
+
 def _record_events(records, label: str, res_label: str, res_of, declared: set, f: Findings, packed_cols,
                    quarantined, cls_malformed: int, cls_zero: int, cls_undecl: int, cls_late: int | None,
-                   host_elapsed: int):
-    """(errors, warnings) as lists of (canonical index, order, text)."""
+                   host_elapsed, late: list[int] | None = None):
+    """(errors, warnings) as lists of (canonical index, order, text).
+
+    ``late``: canonical indices of device records ending after ``host_elapsed``, when the
+    caller had to decide them itself (quarantined host records), else None."""
     errs: list[tuple[int, int, str]] = []
     warns: list[tuple[int, int, str]] = []
     index = packed_cols.index
@@ -61,7 +73,10 @@ def _record_events(records, label: str, res_label: str, res_of, declared: set, f
     for i in _canon(f.lists[cls_undecl], index):
         errs.append((i, 1, f"{where(i)}: {res_label if res_label == 'device' else 'rank'} not declared"))
     if cls_late is not None:
-        for i in _canon(f.lists[cls_late], index):
+        if late is None:   # the kernel's list (in-domain records) + quarantined records
+            late = _canon(f.lists[cls_late], index)
+            late += [q.index for q in quarantined if _after(records[q.index].interval.end, host_elapsed)]
+        for i in late:
             warns.append((i, 1, f"{where(i)}: ends at {records[i].interval.end}, after host elapsed time "
                                 f"{host_elapsed}; it will be clamped"))
     for q in quarantined:
@@ -101,9 +116,17 @@ def validation_report(trace: Trace, packed: PackedTrace, f: Findings) -> Validat
                 a, b = trace.host_records[c].interval, trace.host_records[i].interval
                 errors.append(f"rank {rank}: host records {c} and {i} overlap: "
                               f"[{a.start}, {a.end}) and [{b.start}, {b.end})")
+    # model.py:217-228: late device records, only when ranks are declared.  The kernel compares
+    # in-domain records against the max in-domain host end; a quarantined host record (its end
+    # outside u64 or not an int) moves the reference's host elapsed, so then the comparison is
+    # made here, on the unclipped values, for every device record.
+    host_elapsed, late = f.host_elapsed, None
+    if trace.n >= 1 and packed.host_q:
+        host_elapsed = max((r.interval.end for r in trace.host_records), default=0)
+        late = [i for i, r in enumerate(trace.device_records) if _after(r.interval.end, host_elapsed)]
     d_err, d_warn = _record_events(trace.device_records, "device", "device", lambda r: r.device_id, devs, f,
                                    packed.dev, packed.dev_q, N.DEV_MALFORMED, N.DEV_ZERO, N.DEV_UNDECLARED,
-                                   N.DEV_LATE, f.host_elapsed)
+                                   N.DEV_LATE if trace.n >= 1 else None, host_elapsed, late)
     errors += [t for _, _, t in d_err]
     warnings += [t for _, _, t in d_warn]
     return ValidationReport(errors, warnings)

@@ -221,6 +221,61 @@ def invalid_corpus() -> list:
     return out
 
 
+def _stage(fn):
+    try:
+        return {"ok": fn()}
+    except InvalidTraceError as e:
+        return {"raise": "InvalidTraceError", "msg": str(e)}
+    except (ValueError, AnalysisError) as e:
+        return {"raise": type(e).__name__, "msg": str(e)}
+
+
+def quarantine_corpus() -> list:
+    """Out-of-u64-domain timestamps (negative, beyond 2**64-1, non-int) on either side,
+    through compute_report / validate AND the stage functions summarize_host /
+    summarize_device (model.py:140-157, :217-228; summarize.py:57-138)."""
+    rng = random.Random(0x0A7A)
+    H, D = HostState, DeviceActivityKind
+    bad = [Interval(-5, 10), Interval(3, 2 ** 64 + 5), Interval(-1, 20), Interval(2 ** 64 + 5, 2 ** 64 + 1),
+           Interval(-5, -9), Interval(4, 20.5), Interval(2.5, 3), Interval(-7, 2 ** 64 + 9), Interval(30, 2 ** 70)]
+    traces = []
+    for iv in bad:
+        for side in ("host", "device"):
+            base_h = [HostRecord(0, H.USEFUL, Interval(0, 10)), HostRecord(1, H.MPI, Interval(2, 8))]
+            base_d = [DeviceRecord(0, D.KERNEL, Interval(1, 6)), DeviceRecord(1, D.MEMORY, Interval(3, 9))]
+            if side == "host":
+                base_h.append(HostRecord(rng.choice((0, 1)), H.OFFLOAD, iv))
+            else:
+                base_d.append(DeviceRecord(rng.choice((0, 1)), D.KERNEL, iv))
+            traces.append(Trace(host_processes=(0, 1), devices=(DeviceDecl(0, 0), DeviceDecl(1, 1)),
+                                host_records=tuple(base_h), device_records=tuple(base_d)))
+            # device-only twin: no late warnings (n == 0), E from the device side
+            if side == "device":
+                traces.append(Trace(devices=(DeviceDecl(0), DeviceDecl(1)), device_records=tuple(base_d)))
+    for i in range(120):
+        base = random_valid_trace(rng, max_ranks=3, max_devices=3, max_segments=6)
+        hrec, drec = list(base.host_records), list(base.device_records)
+        for _ in range(rng.randint(1, 3)):
+            iv = rng.choice(bad + [Interval(rng.randint(0, 300), rng.randint(300, 400))])
+            if base.host_processes and rng.random() < 0.5:
+                hrec.append(HostRecord(rng.choice(base.host_processes), rng.choice(list(H)), iv))
+            elif base.devices:
+                drec.append(DeviceRecord(rng.choice(base.devices).device_id, rng.choice(list(D)), iv))
+        traces.append(Trace(host_processes=base.host_processes, devices=base.devices, host_records=tuple(hrec),
+                            device_records=tuple(drec)))
+    out = []
+    for i, t in enumerate(traces):
+        c = case(t, f"quarantine/{i}")
+        c["summarize_host"] = _stage(lambda: [[s.rank, s.d_useful, s.d_offload, s.d_mpi, s.span_end]
+                                              for s in heteff.summarize_host(t)[0]] + [heteff.summarize_host(t)[1]])
+        c["summarize_device"] = {str(E): _stage(lambda E=E: [[[s.device_id, s.d_kernel, s.d_memory, s.d_idle]
+                                                                for s in heteff.summarize_device(t, E)[0]],
+                                                               heteff.summarize_device(t, E)[1]])
+                                 for E in (7, 50, 2 ** 64 + 3)}
+        out.append(c)
+    return out
+
+
 def summarize_device_corpus() -> list:
     rng = random.Random(0x5D5D)
     out = []
@@ -634,7 +689,7 @@ def render_corpus() -> list:
 
 def main() -> None:
     only = sys.argv[sys.argv.index("--only") + 1].split(",") if "--only" in sys.argv else None
-    jobs = {"presets": presets, "acceptance": acceptance_corpora, "invalid": invalid_corpus,
+    jobs = {"presets": presets, "acceptance": acceptance_corpora, "invalid": invalid_corpus, "quarantine": quarantine_corpus,
             "summarize_device": summarize_device_corpus, "metrics": metrics_corpus,
             "config_shards": config_shards, "regions": regions_corpus, "intervals": intervals_corpus,
             "trace_docs": trace_docs_corpus, "imports": import_corpus, "renders": render_corpus}

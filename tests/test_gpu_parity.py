@@ -298,3 +298,38 @@ def test_timestamps_at_the_top_of_u64_and_across_a_32_bit_boundary(offset):
     got, _ = _engine_vs_oracle(hs, ds, n, m)        # report mode compares the finding lists too
     assert got.elapsed == int(hs[1].max())
     _engine_vs_oracle(hs, ds, n, m, N.MODE_SUMMARIZE_DEVICE, int(hs[1].max()) - 1000)
+
+
+QUARANTINE = load("quarantine")
+
+
+def _expect(fn, want):
+    if "raise" in want:
+        exc = {"InvalidTraceError": hb.InvalidTraceError, "ValueError": ValueError,
+               "AnalysisError": hb.AnalysisError}[want["raise"]]
+        with pytest.raises(exc) as ei:
+            fn()
+        assert str(ei.value) == want["msg"]
+    else:
+        assert fn() == want["ok"]
+
+
+@pytest.mark.parametrize("case", QUARANTINE, ids=[c["tag"] for c in QUARANTINE])
+def test_out_of_domain_timestamps_match_reference(case):
+    """Records outside the u64 domain never reach the kernels (packing.py quarantine); the
+    reference still reports them -- validate() (incl. their late-device warnings,
+    model.py:217-228), compute_report, and the stage functions summarize_host /
+    summarize_device must raise exactly as the reference does (summarize.py:57-138)."""
+    test_compute_report_and_validate_match_reference(case)
+    t = to_trace(case["trace"])
+
+    def sh():
+        s, E = hb.summarize_host(t)
+        return [[x.rank, x.d_useful, x.d_offload, x.d_mpi, x.span_end] for x in s] + [E]
+
+    _expect(sh, case["summarize_host"])
+    for E, want in case["summarize_device"].items():
+        def sd(E=int(E)):
+            s, w = hb.summarize_device(t, E)
+            return [[[x.device_id, x.d_kernel, x.d_memory, x.d_idle] for x in s], w]
+        _expect(sd, want)

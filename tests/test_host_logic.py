@@ -132,3 +132,16 @@ def test_csr_offsets_are_checked_before_any_device_work(seg):
     dseg = np.zeros(1, dtype=np.int64)
     rc = lib.heteff_analyze_host_csr(None, C.byref(t), hseg.ctypes.data, dseg.ctypes.data, None, None, None, None)
     assert rc == N.BAD_ARG
+
+
+def test_metric_stage_functions_refuse_elapsed_beyond_u64():
+    """The metric kernels take E as u64; a larger E raises instead of being truncated
+    by the C call (no GPU needed: the check precedes the native call)."""
+    import paper_2603_26576_b200 as hb
+    big = 2 ** 64 + 5
+    with pytest.raises(OverflowError):
+        hb.host_metrics([hb.HostSummary(0, 1, 2, 3, 6)], big)
+    with pytest.raises(OverflowError):
+        hb.device_metrics([hb.DeviceSummary(0, 1, 2, 3)], big)
+    with pytest.raises(ValueError):   # the reference's own checks still come first
+        hb.host_metrics([], big)
