@@ -1,6 +1,7 @@
 """Config-shaped traces generated in HBM: generator bit-exactness vs the numpy
 twin, parity with the reference on rank shards, and full-scale parity with
-the C oracle (C2, 1e8 intervals) plus size-independent properties."""
+the C oracle: C2 (1e8) whole, C3 / C4 / C5 (5e8 / 1e9 / 2e9) through the
+oracle run rank-sharded with the global E, plus size-independent properties."""
 
 from __future__ import annotations
 
@@ -70,6 +71,51 @@ def test_c2_full_scale_matches_oracle():
     assert np.array_equal(f.host_sum, ref.host_sum)
     assert np.array_equal(f.dev_sum, ref.dev_sum)
     assert f.host_metrics == ref.host_metrics and f.device_metrics == ref.device_metrics
+
+
+def _fetch(dt, g):
+    """Rank block [r0, r1) of an HBM-resident generated trace as host numpy columns
+    (resource ids local to the block) -- one block at a time, for the sharded oracle."""
+    hseg = dt.h_seg.cpu().numpy()
+    dseg = dt.d_seg.cpu().numpy()
+
+    def fetch(r0, r1):
+        a, b = int(hseg[r0]), int(hseg[r1])
+        c, d = int(dseg[r0 * g]), int(dseg[r1 * g])
+        h = (_u64(dt.h_start[a:b]), _u64(dt.h_end[a:b]), _host(dt.h_res[a:b]) - np.int32(r0), _host(dt.h_kind[a:b]))
+        v = (_u64(dt.d_start[c:d]), _u64(dt.d_end[c:d]), _host(dt.d_res[c:d]) - np.int32(r0 * g),
+             _host(dt.d_kind[c:d]))
+        return h, v
+    return fetch
+
+
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+def test_full_scale_matches_sharded_oracle(name):
+    """C3 (5e8), C4 (1e9) and C5 (2e9 -- the north star's trace) IN FULL on one GPU,
+    bit-exact against the C oracle run rank-sharded in the reference's exact sharded form
+    (summarize_host per block, E = max, summarize_device(block, E_global), the metric
+    stage functions on the gathered summaries -- summarize.py:57-138, metrics.py:66-122):
+    E, every per-rank and per-device summary, every device's clamp count and all nine
+    metric floats ``==``.  Both input layouts (CSR offsets, res columns) are checked."""
+    from oracle import oracle as O
+    cfg = CONFIGS[name]
+    dt = generate(cfg)
+    f = analyze_device(dt)                   # resource ids as CSR offsets (17 B / interval)
+    g = analyze_device(dt.columns_only())    # res columns (21 B / interval)
+    assert f.status == N.OK and g.status == N.OK
+    per_rank = cfg.intervals / cfg.n_ranks
+    block = max(1, int(1.2e8 // per_rank))
+    ref = O.analyze_sharded(_fetch(dt, cfg.gpus_per_rank), cfg.n_ranks, cfg.gpus_per_rank, block)
+    for got in (f, g):
+        assert got.elapsed == ref.elapsed
+        assert np.array_equal(got.host_sum, ref.host_sum)
+        assert np.array_equal(got.dev_sum, ref.dev_sum)          # k, mem, idle, clamp count
+        assert tuple(got.host_metrics) == ref.host_metrics
+        assert tuple(got.device_metrics) == ref.device_metrics
+    # the workload really exercises the cross-rank coupling: devices clamp at the GLOBAL E
+    if name == "c5":
+        assert int(ref.dev_sum[:, 3].sum()) > 0
+    assert ref.blocks > 1
 
 
 @pytest.mark.parametrize("name", ["c3", "c5"])

@@ -52,7 +52,13 @@ def test_bench_under_torchrun(cfg, world, port, scaling):
     from paper_2603_26576_b200.configs import CONFIGS
     c = CONFIGS[cfg]
     if scaling == "weak":   # every rank a C-sized block of a world-times larger trace
-        assert d["config"]["intervals"] == world * d["roofline"]["per_gpu_intervals"] == world * c.intervals
+        import types
+        sys.path.insert(0, str(ROOT))
+        import bench
+        g = bench._global_config(types.SimpleNamespace(config=cfg, scaling=scaling), world)
+        assert d["config"]["intervals"] == world * c.intervals == g.intervals
+        # rank 0's block: its ranks hold the remainder records of the larger trace
+        assert d["roofline"]["per_gpu_intervals"] == g.block_intervals(0, g.n_ranks // world)
     else:                   # the one trace split by rank blocks (rank 0's block: the first n // world ranks)
         assert d["config"]["intervals"] == c.intervals
         assert d["roofline"]["per_gpu_intervals"] == c.block_intervals(0, c.n_ranks // world)
