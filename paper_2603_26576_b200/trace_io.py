@@ -28,8 +28,6 @@ from .model import DeviceActivityKind, DeviceDecl, DeviceRecord, HostRecord, Hos
 from .packing import PackedTrace, RecordColumns, pack_trace
 
 FORMAT_VERSION = 1
-_HOST_STATES = {s.value: s for s in HostState}
-_DEVICE_KINDS = {k.value: k for k in DeviceActivityKind}
 _HOST_CODE_STATE = (HostState.USEFUL, HostState.OFFLOAD, HostState.MPI)     # ingest codes 0, 1, 2
 _DEV_CODE_KIND = (DeviceActivityKind.KERNEL, DeviceActivityKind.MEMORY)
 
@@ -39,7 +37,12 @@ class TraceFormatError(Exception):
 
 
 # ---------------------------------------------------------------------------
-# strict pure-Python reader: the error path (and unusual legal documents)
+# strict pure-Python reader: the error path (and unusual legal documents).
+# The document schema (pkg/docs/formats.md:9-85) is data -- SCHEMA below -- and one
+# walker checks any value against a node of it, so each error text is produced in
+# exactly one place: objects (required / optional / unknown fields, checked in
+# schema order, unknown ones after the known ones), arrays, non-negative integers,
+# enumerations and constants.
 # ---------------------------------------------------------------------------
 def _load(data):
     if isinstance(data, bytes):
@@ -53,92 +56,160 @@ def _load(data):
         raise TraceFormatError(f"trace document is not valid JSON: {e}") from e
 
 
-def _expect_obj(v, path):
-    if not isinstance(v, dict):
-        raise TraceFormatError(f"{path}: expected object, got {type(v).__name__}")
-    return dict(v)
+class _Node:
+    def check(self, value, path: str):
+        raise NotImplementedError
 
 
-def _expect_list(v, path):
-    if not isinstance(v, list):
-        raise TraceFormatError(f"{path}: expected array, got {type(v).__name__}")
-    return v
+class _Pass(_Node):
+    def check(self, value, path):
+        return value
 
 
-def _pop(d, path, key, required=True):
-    if key not in d:
-        if required:
-            raise TraceFormatError(f"{path}: missing required field {key!r}")
-        return None
-    return d.pop(key)
+class _UInt(_Node):
+    def check(self, value, path):
+        if isinstance(value, bool) or not isinstance(value, int):
+            raise TraceFormatError(f"{path}: expected integer, got {value!r}")
+        if value < 0:
+            raise TraceFormatError(f"{path}: negative value {value}")
+        return value
 
 
-def _done(d, path):
-    if d:
-        raise TraceFormatError(f"{path}: unknown field {sorted(d)[0]!r}")
+class _Enum(_Node):
+    def __init__(self, members):
+        self.table = {m.value: m for m in members}
+
+    def check(self, value, path):
+        if isinstance(value, str) and value in self.table:
+            return self.table[value]
+        raise TraceFormatError(f"{path}: expected one of {', '.join(sorted(self.table))}; got {value!r}")
 
 
-def _uint(v, path):
-    if isinstance(v, bool) or not isinstance(v, int):
-        raise TraceFormatError(f"{path}: expected integer, got {v!r}")
-    if v < 0:
-        raise TraceFormatError(f"{path}: negative value {v}")
-    return v
+class _Const(_Node):
+    def __init__(self, want, message):
+        self.want, self.message = want, message
+
+    def check(self, value, path):
+        if value != self.want:
+            raise TraceFormatError(f"{path}: {self.message.format(got=value)}")
+        return value
 
 
-def _choice(v, table, path):
-    if not isinstance(v, str) or v not in table:
-        raise TraceFormatError(f"{path}: expected one of {', '.join(sorted(table))}; got {v!r}")
-    return table[v]
+class _Array(_Node):
+    def __init__(self, item):
+        self.item = item
+
+    def check(self, value, path):
+        if not isinstance(value, list):
+            raise TraceFormatError(f"{path}: expected array, got {type(value).__name__}")
+        return [self.item.check(v, f"{path}[{i}]") for i, v in enumerate(value)]
+
+
+class _Object(_Node):
+    """Fields as (name, node, required); an optional field given as null counts as absent."""
+
+    def __init__(self, *fields):
+        self.fields = fields
+
+    def check(self, value, path):
+        if not isinstance(value, dict):
+            raise TraceFormatError(f"{path}: expected object, got {type(value).__name__}")
+        out = {}
+        for name, node, required in self.fields:
+            if name not in value:
+                if required:
+                    raise TraceFormatError(f"{path}: missing required field {name!r}")
+                out[name] = None
+                continue
+            v = value[name]
+            out[name] = None if (v is None and not required) else node.check(v, f"{path}.{name}")
+        extra = sorted(k for k in value if k not in out)
+        if extra:
+            raise TraceFormatError(f"{path}: unknown field {extra[0]!r}")
+        return out
+
+
+class _Str(_Node):
+    def check(self, value, path):
+        if not isinstance(value, str):
+            raise TraceFormatError(f"{path}: expected string, got {value!r}")
+        return value
+
+
+class _OneOf(_Node):
+    """A value from a fixed set of literals."""
+
+    def __init__(self, allowed, message):
+        self.allowed, self.message = allowed, message
+
+    def check(self, value, path):
+        if value not in self.allowed:
+            raise TraceFormatError(f"{path}: {self.message.format(got=value)}")
+        return value
+
+
+class _NonEmpty(_Node):
+    def __init__(self, inner: "_Array", message: str):
+        self.inner, self.message = inner, message
+
+    def check(self, value, path):
+        items = self.inner.check(value, path)
+        if not items:
+            raise TraceFormatError(f"{path}: {self.message}")
+        return items
+
+
+class _Resource(_Node):
+    """A mapping rule's resource: a fixed non-negative id or the event field 'pid' / 'tid'."""
+
+    def check(self, value, path):
+        if isinstance(value, bool) or not (isinstance(value, int) or value in ("pid", "tid")):
+            raise TraceFormatError(f"{path}: expected non-negative integer, 'pid' or 'tid'; got {value!r}")
+        if isinstance(value, int) and value < 0:
+            raise TraceFormatError(f"{path}: negative value {value}")
+        return value
+
+
+class _Micros(_Node):
+    """Trace-event microseconds -> integer nanoseconds, exactly (integral floats accepted)."""
+
+    def check(self, value, path):
+        if isinstance(value, float) and not isinstance(value, bool):
+            if not value.is_integer():
+                raise TraceFormatError(f"{path}: fractional timestamp {value!r} (would require rounding)")
+            value = int(value)
+        if isinstance(value, bool) or not isinstance(value, int):
+            raise TraceFormatError(f"{path}: expected number, got {value!r}")
+        if value < 0:
+            raise TraceFormatError(f"{path}: negative value {value}")
+        return value * 1000
+
+
+SCHEMA = _Object(
+    ("version", _Const(FORMAT_VERSION, "unsupported version {got!r}"), True),
+    ("time_unit", _Const("ns", "expected 'ns', got {got!r}"), True),
+    ("hosts", _Array(_Object(
+        ("rank", _UInt(), True),
+        ("records", _Array(_Object(("state", _Enum(HostState), True), ("start", _UInt(), True),
+                                   ("end", _UInt(), True))), True))), True),
+    ("devices", _Array(_Object(
+        ("id", _UInt(), True),
+        ("owner_rank", _UInt(), False),
+        ("records", _Array(_Object(("kind", _Enum(DeviceActivityKind), True), ("stream", _UInt(), False),
+                                   ("start", _UInt(), True), ("end", _UInt(), True))), True))), True),
+)
 
 
 def _parse_py(data) -> Trace:
-    doc = _expect_obj(_load(data), "$")
-    version = _pop(doc, "$", "version")
-    if version != FORMAT_VERSION:
-        raise TraceFormatError(f"$.version: unsupported version {version!r}")
-    unit = _pop(doc, "$", "time_unit")
-    if unit != "ns":
-        raise TraceFormatError(f"$.time_unit: expected 'ns', got {unit!r}")
-    hp, hrecs = [], []
-    for i, entry in enumerate(_expect_list(_pop(doc, "$", "hosts"), "$.hosts")):
-        path = f"$.hosts[{i}]"
-        entry = _expect_obj(entry, path)
-        rank = _uint(_pop(entry, path, "rank"), f"{path}.rank")
-        hp.append(rank)
-        for j, rec in enumerate(_expect_list(_pop(entry, path, "records"), f"{path}.records")):
-            rp = f"{path}.records[{j}]"
-            rec = _expect_obj(rec, rp)
-            state = _choice(_pop(rec, rp, "state"), _HOST_STATES, f"{rp}.state")
-            s = _uint(_pop(rec, rp, "start"), f"{rp}.start")
-            e = _uint(_pop(rec, rp, "end"), f"{rp}.end")
-            _done(rec, rp)
-            hrecs.append(HostRecord(rank, state, Interval(s, e)))
-        _done(entry, path)
-    decls, drecs = [], []
-    for i, entry in enumerate(_expect_list(_pop(doc, "$", "devices"), "$.devices")):
-        path = f"$.devices[{i}]"
-        entry = _expect_obj(entry, path)
-        did = _uint(_pop(entry, path, "id"), f"{path}.id")
-        owner = _pop(entry, path, "owner_rank", required=False)
-        if owner is not None:
-            owner = _uint(owner, f"{path}.owner_rank")
-        decls.append(DeviceDecl(did, owner))
-        for j, rec in enumerate(_expect_list(_pop(entry, path, "records"), f"{path}.records")):
-            rp = f"{path}.records[{j}]"
-            rec = _expect_obj(rec, rp)
-            kind = _choice(_pop(rec, rp, "kind"), _DEVICE_KINDS, f"{rp}.kind")
-            stream = _pop(rec, rp, "stream", required=False)
-            if stream is not None:
-                stream = _uint(stream, f"{rp}.stream")
-            s = _uint(_pop(rec, rp, "start"), f"{rp}.start")
-            e = _uint(_pop(rec, rp, "end"), f"{rp}.end")
-            _done(rec, rp)
-            drecs.append(DeviceRecord(did, kind, Interval(s, e), stream))
-        _done(entry, path)
-    _done(doc, "$")
-    return Trace(host_processes=tuple(hp), devices=tuple(decls), host_records=tuple(hrecs),
-                 device_records=tuple(drecs))
+    doc = SCHEMA.check(_load(data), "$")
+    hosts, devices = doc["hosts"], doc["devices"]
+    return Trace(
+        host_processes=tuple(h["rank"] for h in hosts),
+        devices=tuple(DeviceDecl(d["id"], d["owner_rank"]) for d in devices),
+        host_records=tuple(HostRecord(h["rank"], r["state"], Interval(r["start"], r["end"]))
+                           for h in hosts for r in h["records"]),
+        device_records=tuple(DeviceRecord(d["id"], r["kind"], Interval(r["start"], r["end"]), r["stream"])
+                             for d in devices for r in d["records"]))
 
 
 # ---------------------------------------------------------------------------
@@ -314,8 +385,9 @@ def read_trace_packed(data, nthreads: int | None = None):
 # ---------------------------------------------------------------------------
 from dataclasses import dataclass  # noqa: E402
 
-_TARGETS = {**_HOST_STATES, **_DEVICE_KINDS}
 _MATCH_KEYS = ("name_contains", "name_equals", "category_contains", "category_equals")
+_MODES = {"contains": lambda subject, pattern: pattern in subject,
+          "equals": lambda subject, pattern: pattern == subject}
 _TARGET_CODE = {HostState.USEFUL: 0, HostState.OFFLOAD: 1, HostState.MPI: 2,
                 DeviceActivityKind.KERNEL: 3, DeviceActivityKind.MEMORY: 4}
 
@@ -335,8 +407,7 @@ class MappingRule:
     resource: object  # fixed id, or "pid" / "tid"
 
     def matches(self, name: str, category: str) -> bool:
-        subject = name if self.field == "name" else category
-        return self.pattern in subject if self.mode == "contains" else self.pattern == subject
+        return _MODES[self.mode]({"name": name, "category": category}[self.field], self.pattern)
 
 
 @dataclass(frozen=True)
@@ -357,53 +428,36 @@ def _load_named(data, what):
         raise TraceFormatError(f"{what} is not valid JSON: {e}") from e
 
 
+class _MatchRule(_Node):
+    """One mapping rule (docs/formats.md:87-132): exactly one match key, then its pattern,
+    the target state / kind and the resource, then no other field."""
+
+    TARGET = None   # set below (needs the enums)
+
+    def check(self, value, path):
+        if not isinstance(value, dict):
+            raise TraceFormatError(f"{path}: expected object, got {type(value).__name__}")
+        keys = [k for k in _MATCH_KEYS if k in value]
+        if len(keys) != 1:
+            raise TraceFormatError(f"{path}: exactly one of {', '.join(_MATCH_KEYS)} is required")
+        key = keys[0]
+        got = _Object((key, _Str(), True), ("target", self.TARGET, True),
+                      ("resource", _Resource(), True)).check(value, path)
+        subject, mode = key.rsplit("_", 1)
+        return MappingRule(subject, mode, got[key], got["target"], got["resource"])
+
+
+_MatchRule.TARGET = _Enum(list(HostState) + list(DeviceActivityKind))
+MAPPING_SCHEMA = _Object(
+    ("default_policy", _OneOf(("drop", "error"), "expected 'drop' or 'error', got {got!r}"), True),
+    ("rules", _NonEmpty(_Array(_MatchRule()), "at least one rule is required"), True),
+)
+
+
 def read_mapping(data) -> CategoryMapping:
     """Parse a mapping document (``trace_io.py:222-260``, ``docs/formats.md:87-132``)."""
-    doc = _expect_obj(_load_named(data, "mapping document"), "$")
-    policy = _pop(doc, "$", "default_policy")
-    if policy not in ("drop", "error"):
-        raise TraceFormatError(f"$.default_policy: expected 'drop' or 'error', got {policy!r}")
-    entries = _expect_list(_pop(doc, "$", "rules"), "$.rules")
-    if not entries:
-        raise TraceFormatError("$.rules: at least one rule is required")
-    rules = []
-    for i, entry in enumerate(entries):
-        path = f"$.rules[{i}]"
-        entry = _expect_obj(entry, path)
-        present = [k for k in _MATCH_KEYS if k in entry]
-        if len(present) != 1:
-            raise TraceFormatError(f"{path}: exactly one of {', '.join(_MATCH_KEYS)} is required")
-        key = present[0]
-        pattern = _pop(entry, path, key)
-        if not isinstance(pattern, str):
-            raise TraceFormatError(f"{path}.{key}: expected string, got {pattern!r}")
-        field, mode = key.rsplit("_", 1)
-        field = "category" if field == "category" else "name"
-        target = _choice(_pop(entry, path, "target"), _TARGETS, f"{path}.target")
-        resource = _pop(entry, path, "resource")
-        if isinstance(resource, bool) or not (isinstance(resource, int) or resource in ("pid", "tid")):
-            raise TraceFormatError(f"{path}.resource: expected non-negative integer, 'pid' or 'tid'; "
-                                   f"got {resource!r}")
-        if isinstance(resource, int) and resource < 0:
-            raise TraceFormatError(f"{path}.resource: negative value {resource}")
-        _done(entry, path)
-        rules.append(MappingRule(field, mode, pattern, target, resource))
-    _done(doc, "$")
-    return CategoryMapping(tuple(rules), policy)
-
-
-def _us_ns(v, path):
-    if isinstance(v, bool):
-        raise TraceFormatError(f"{path}: expected number, got {v!r}")
-    if isinstance(v, float):
-        if not v.is_integer():
-            raise TraceFormatError(f"{path}: fractional timestamp {v!r} (would require rounding)")
-        v = int(v)
-    if not isinstance(v, int):
-        raise TraceFormatError(f"{path}: expected number, got {v!r}")
-    if v < 0:
-        raise TraceFormatError(f"{path}: negative value {v}")
-    return v * 1000
+    doc = MAPPING_SCHEMA.check(_load_named(data, "mapping document"), "$")
+    return CategoryMapping(tuple(doc["rules"]), doc["default_policy"])
 
 
 def _assemble(hrecs, drecs, unmapped, mapping):
@@ -419,36 +473,40 @@ def _assemble(hrecs, drecs, unmapped, mapping):
     return trace, warnings
 
 
+_MICROS = _Micros()
+
+
 def _import_py(data, mapping):
+    """The strict event importer (error texts, unusual legal documents): complete spans
+    ("ph": "X") only, first matching rule wins, unmatched events reported by index."""
     doc = _load_named(data, "events document")
-    events = _expect_list(doc.get("traceEvents"), "$.traceEvents") if isinstance(doc, dict) else \
-        _expect_list(doc, "$")
+    if isinstance(doc, dict):
+        events = _Array(_Pass()).check(doc.get("traceEvents"), "$.traceEvents")
+    else:
+        events = _Array(_Pass()).check(doc, "$")
     hrecs, drecs, unmapped = [], [], []
     for i, ev in enumerate(events):
-        path = f"$[{i}]"
-        if not isinstance(ev, dict) or ev.get("ph") != "X":
+        if not (isinstance(ev, dict) and ev.get("ph") == "X"):
             continue
-        name = ev.get("name")
-        if not isinstance(name, str):
-            raise TraceFormatError(f"{path}.name: expected string, got {name!r}")
-        cat = ev.get("cat", "")
-        if not isinstance(cat, str):
-            raise TraceFormatError(f"{path}.cat: expected string, got {cat!r}")
-        for key in ("ts", "dur"):
-            if key not in ev:
-                raise TraceFormatError(f"{path}: missing required field {key!r}")
-        start = _us_ns(ev["ts"], f"{path}.ts")
-        end = start + _us_ns(ev["dur"], f"{path}.dur")
+        path = f"$[{i}]"
+        name = _Str().check(ev.get("name"), f"{path}.name")
+        cat = _Str().check(ev.get("cat", ""), f"{path}.cat")
+        missing = [k for k in ("ts", "dur") if k not in ev]
+        if missing:
+            raise TraceFormatError(f"{path}: missing required field {missing[0]!r}")
+        start = _MICROS.check(ev["ts"], f"{path}.ts")
+        end = start + _MICROS.check(ev["dur"], f"{path}.dur")
         rule = next((r for r in mapping.rules if r.matches(name, cat)), None)
         if rule is None:
             unmapped.append((i, name))
             continue
-        rid = rule.resource if isinstance(rule.resource, int) else \
-            _uint(ev.get(rule.resource), f"{path}.{rule.resource}")
+        res = rule.resource
+        if not isinstance(res, int):
+            res = _UInt().check(ev.get(res), f"{path}.{res}")
         if isinstance(rule.target, HostState):
-            hrecs.append(HostRecord(rid, rule.target, Interval(start, end)))
+            hrecs.append(HostRecord(res, rule.target, Interval(start, end)))
         else:
-            drecs.append(DeviceRecord(rid, rule.target, Interval(start, end)))
+            drecs.append(DeviceRecord(res, rule.target, Interval(start, end)))
     return _assemble(hrecs, drecs, unmapped, mapping)
 
 
@@ -504,31 +562,41 @@ def import_mapped(data, mapping: CategoryMapping, nthreads: int | None = None, c
     return _assemble(hrecs, drecs, unmapped, mapping)
 
 
+def _host_item(rec) -> dict:
+    return {"state": rec.state.value, "start": rec.interval.start, "end": rec.interval.end}
+
+
+def _device_item(rec) -> dict:
+    stream = {} if rec.stream is None else {"stream": rec.stream}
+    return {"kind": rec.kind.value, **stream, "start": rec.interval.start, "end": rec.interval.end}
+
+
+def _grouped(records, key, declared, what):
+    """Records grouped by resource in declaration order; a record of an undeclared
+    resource is a ValueError (the document could not be read back)."""
+    groups = {k: [] for k in declared}
+    for rec in records:
+        k = key(rec)
+        if k not in groups:
+            raise ValueError(f"{what} {k}")
+        groups[k].append(rec)
+    return groups
+
+
 def write_trace(trace: Trace) -> bytes:
-    """Deterministic native document (``trace_io.py:161-193``): equal traces, equal bytes."""
-    by_rank = {r: [] for r in trace.host_processes}
-    for rec in trace.host_records:
-        if rec.rank not in by_rank:
-            raise ValueError(f"host record references undeclared rank {rec.rank}")
-        by_rank[rec.rank].append({"state": rec.state.value, "start": rec.interval.start, "end": rec.interval.end})
-    by_dev = {d.device_id: [] for d in trace.devices}
-    for rec in trace.device_records:
-        if rec.device_id not in by_dev:
-            raise ValueError(f"device record references undeclared device {rec.device_id}")
-        item = {"kind": rec.kind.value}
-        if rec.stream is not None:
-            item["stream"] = rec.stream
-        item["start"], item["end"] = rec.interval.start, rec.interval.end
-        by_dev[rec.device_id].append(item)
-    devices = []
-    for d in trace.devices:
-        entry = {"id": d.device_id}
-        if d.owner_rank is not None:
-            entry["owner_rank"] = d.owner_rank
-        entry["records"] = by_dev[d.device_id]
-        devices.append(entry)
-    doc = {"version": FORMAT_VERSION, "time_unit": "ns",
-           "hosts": [{"rank": r, "records": by_rank[r]} for r in trace.host_processes], "devices": devices}
+    """Deterministic native document (``trace_io.py:161-193``, docs/formats.md:9-85): equal
+    traces give equal bytes -- keys in schema order, two-space indent, final newline."""
+    hosts = _grouped(trace.host_records, lambda r: r.rank, trace.host_processes,
+                     "host record references undeclared rank")
+    devs = _grouped(trace.device_records, lambda r: r.device_id, [d.device_id for d in trace.devices],
+                    "device record references undeclared device")
+    doc = {
+        "version": FORMAT_VERSION,
+        "time_unit": "ns",
+        "hosts": [{"rank": r, "records": [_host_item(x) for x in hosts[r]]} for r in trace.host_processes],
+        "devices": [{"id": d.device_id, **({} if d.owner_rank is None else {"owner_rank": d.owner_rank}),
+                     "records": [_device_item(x) for x in devs[d.device_id]]} for d in trace.devices],
+    }
     return (json.dumps(doc, indent=2) + "\n").encode("utf-8")
 
 
