@@ -178,7 +178,8 @@ def _config_dict(args, cfg, world: int) -> dict:
     if args.shuffle:
         d["device_order"] = "random permutation (K3 sort inside every step)"
     if args.config == "c4" or args.regions:
-        d["regions"] = args.regions if args.regions is not None else 16
+        d["regions"] = (f"{args.regions if args.regions is not None else 16} nested monitoring regions per rank "
+                        "(each rank its own windows over its own span; devices follow their owner)")
     return d
 
 
@@ -307,8 +308,16 @@ def run_engine(args, world, rank, local):
     windows, owner = None, None
     if n_regions:
         from paper_2603_26576_b200.engine import analyze_regions
-        E0 = analyze_device(dt, N.MODE_REPORT, stream=stream.cuda_stream, device=local).elapsed
-        windows = [(i * E0 // 40, E0 - i * E0 // 40) for i in range(n_regions)]   # nested, shrinking
+        # per-rank regions (TALP annotates regions per process): region i of rank p is
+        # [i * S_p / 40 + (p % 13), S_p - i * S_p / 40) over the rank's own span S_p --
+        # nested per rank, different on every rank (tests/test_gpu_regions.py, same shape)
+        f0 = analyze_device(dt, N.MODE_REPORT, stream=stream.cuda_stream, device=local)
+        S = f0.host_sum[:, 3].astype(np.uint64)
+        pr = np.arange(S.size, dtype=np.uint64)
+        windows = np.zeros((n_regions, S.size, 2), dtype=np.uint64)
+        for i in range(n_regions):
+            lo = np.uint64(i) * S // np.uint64(40) + pr % np.uint64(13)
+            windows[i, :, 0], windows[i, :, 1] = lo, np.maximum(lo, S - np.uint64(i) * S // np.uint64(40))
         owner = np.arange(dt.m, dtype=np.int32) // cfg.gpus_per_rank
     if args.shuffle:   # device records in random order: the step includes the K3 sort
         g = torch.Generator(device=f"cuda:{local}").manual_seed(1)
@@ -450,7 +459,7 @@ def run_engine(args, world, rank, local):
         "clocks": clk.summary(),
     }
     if windows is not None:
-        line["regions"] = {"windows": len(windows), "nested": True, "overlap_metric": True,
+        line["regions"] = {"windows": len(windows), "per_rank": True, "nested": True, "overlap_metric": True,
                            "ms_per_call": statistics.mean(region_ms),
                            "note": "value = compute_report + every region tree + offload/busy overlap per call; "
                                    "e2e covers the compute_report path"}

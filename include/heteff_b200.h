@@ -314,11 +314,20 @@ void heteff_imported_free(heteff_imported *imported);
  * canonical: the call runs the full analysis first and returns its status
  * (INVALID_TRACE / CONTRACT) without computing regions otherwise.  All
  * windows are evaluated in one pass over the records per 16 windows. */
+#define HETEFF_REGIONS_PER_RANK 1   /* heteff_regions.flags */
+
+/* Per-rank regions (HETEFF_REGIONS_PER_RANK; TALP annotates regions per process,
+ * PAPER.md:113): region j has one window per rank, start / end are [count][host_ids]
+ * (window of dense host id h in region j at [j * host_ids + h]).  A rank's records are
+ * clipped to its own window and shifted by its own start; a device's records to its
+ * owner rank's window (dev_owner), a device without an owner records nothing in the
+ * region.  E_j = the longest rank's region (max span, summarize.py:88-89), and every
+ * device clamps at its owner's start + E_j. */
 typedef struct {
-    const uint64_t *start;      /* [count] window starts (host memory) */
-    const uint64_t *end;        /* [count] window ends (exclusive; end <= start = empty window) */
+    const uint64_t *start;      /* [count] window starts (host memory); per-rank: [count][host_ids] */
+    const uint64_t *end;        /* [count] window ends (exclusive; end <= start = empty window); per-rank: [count][host_ids] */
     int32_t count;
-    int32_t reserved;
+    int32_t flags;              /* 0 (one window per region) or HETEFF_REGIONS_PER_RANK */
     const int32_t *dev_owner;   /* [dev_ids] dense host id owning each device, -1 none (host memory; NULL = none) */
 } heteff_regions;
 

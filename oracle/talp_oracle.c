@@ -525,6 +525,17 @@ typedef struct {
     const uint64_t *win_start, *win_end;
     int32_t count;
     const int32_t *dev_owner;            /* [d_ids] dense host id owning the device, -1 none */
+    /* per-rank regions (TALP regions are annotated per process): NULL, or
+     * [count][h_ids][2] window of each rank -- then win_start / win_end are unused, a
+     * rank's records are clipped to its own window, a device's records to its owner's
+     * window, and the records of a device without an owner to the empty window */
+    const uint64_t *host_win;
+    /* sharded use (tests, oracle.regions_sharded): 0 compute_report per region; 1 the
+     * host pass only (summarize_host per region: host rows + the block's E, devices
+     * skipped); 2 the device pass with the GLOBAL E of each region, elapsed_in[j]
+     * (summarize_device + overlap; metric trees left to the caller) */
+    int32_t pass;
+    const uint64_t *elapsed_in;
 } orc_regions_in;
 
 typedef struct {
@@ -538,12 +549,21 @@ typedef struct {
     double *busy_frac; uint32_t *busy_mask; /* [R], [R] */
 } orc_regions_out;
 
-/* clip one record set to [a, b), shifted; returns the kept count */
+/* clip one record set to [a, b) (or, with `win`, record i to win[2 * rank_of(r[i])],
+ * rank_of = identity for host records, the owner table for device records, an
+ * empty window when rank_of < 0), shifted; returns the kept count */
 static int64_t clip_records(const uint64_t *s, const uint64_t *e, const int32_t *r, const uint8_t *k, int64_t n,
-                            uint64_t a, uint64_t b, uint64_t *os, uint64_t *oe, int32_t *orr, uint8_t *ok)
+                            uint64_t a0, uint64_t b0, const uint64_t *win, const int32_t *owner, int32_t h_ids,
+                            uint64_t *os, uint64_t *oe, int32_t *orr, uint8_t *ok)
 {
     int64_t w = 0;
     for (int64_t i = 0; i < n; ++i) {
+        uint64_t a = a0, b = b0;
+        if (win) {
+            const int32_t q = owner ? (owner[r[i]]) : r[i];
+            if (q < 0 || q >= h_ids) continue;
+            a = win[2 * (size_t)q]; b = win[2 * (size_t)q + 1];
+        }
         uint64_t cs, ce;
         if (s[i] == e[i]) {
             if (!(s[i] >= a && s[i] < b)) continue;
@@ -580,26 +600,39 @@ int orc_regions(const orc_in *in, const orc_regions_in *rg, orc_regions_out *o)
     iv_t *D = malloc(sizeof(iv_t) * (size_t)(hn + dn + 1));
     if (!hs || !he || !hr || !hk || !ds || !de || !dr || !dk || !A || !B || !D) return ORC_NOMEM;
     for (int32_t j = 0; j < rg->count; ++j) {
-        const uint64_t a = rg->win_start[j], b = rg->win_end[j];
-        const int64_t kh = clip_records(in->h_start, in->h_end, in->h_res, in->h_kind, hn, a, b, hs, he, hr, hk);
-        const int64_t kd = clip_records(in->d_start, in->d_end, in->d_res, in->d_kind, dn, a, b, ds, de, dr, dk);
+        const uint64_t *win = rg->host_win ? rg->host_win + (size_t)j * (size_t)in->h_ids * 2 : NULL;
+        const uint64_t a = win ? 0 : rg->win_start[j], b = win ? 0 : rg->win_end[j];
+        static const int32_t no_owner = -1;
+        const int64_t kh = clip_records(in->h_start, in->h_end, in->h_res, in->h_kind, hn, a, b, win, NULL, in->h_ids,
+                                        hs, he, hr, hk);
+        /* device ids index the owner table (all -1 without one) */
+        int32_t *own = NULL;
+        if (win) {
+            own = malloc(4 * (size_t)(in->d_ids > 0 ? in->d_ids : 1));
+            for (int32_t q = 0; q < in->d_ids; ++q) own[q] = rg->dev_owner ? rg->dev_owner[q] : no_owner;
+        }
+        const int64_t kd = rg->pass == 1 ? 0 : clip_records(in->d_start, in->d_end, in->d_res, in->d_kind, dn, a, b,
+                                                            win, own, in->h_ids, ds, de, dr, dk);
+        free(own);
         orc_in ri = *in;
         ri.h_start = hs; ri.h_end = he; ri.h_res = hr; ri.h_kind = hk; ri.h_count = kh;
         ri.d_start = ds; ri.d_end = de; ri.d_res = dr; ri.d_kind = dk; ri.d_count = kd;
-        ri.mode = MODE_REPORT; ri.cap = 0; ri.host_elapsed_floor = 0;
+        ri.mode = rg->pass == 1 ? MODE_SUMMARIZE_HOST : rg->pass == 2 ? MODE_SUMMARIZE_DEVICE : MODE_REPORT;
+        ri.elapsed_arg = rg->pass == 2 ? rg->elapsed_in[j] : 0;
+        ri.cap = 0; ri.host_elapsed_floor = 0;
         orc_out ro; memset(&ro, 0, sizeof(ro));
         ro.host_sum = o->host_sum + (size_t)j * (size_t)(n > 0 ? n : 1) * 4;
         ro.dev_sum = o->dev_sum + (size_t)j * (size_t)(m > 0 ? m : 1) * 4;
-        o->status[j] = orc_analyze(&ri, &ro);
-        o->elapsed[j] = ro.elapsed;
+        o->status[j] = rg->pass == 2 && ri.elapsed_arg == 0 ? ORC_ANALYSIS : orc_analyze(&ri, &ro);
+        o->elapsed[j] = rg->pass == 2 ? ri.elapsed_arg : ro.elapsed;
         for (int q = 0; q < 5; ++q) o->host_m[5 * j + q] = ro.host_m[q];
         for (int q = 0; q < 4; ++q) o->dev_m[4 * j + q] = ro.dev_m[q];
         o->host_mask[j] = ro.host_mask; o->dev_mask[j] = ro.dev_mask;
         o->busy_mask[j] = 0; o->busy_frac[j] = 0.0;
         uint64_t *busy = o->busy + (size_t)j * (size_t)(m > 0 ? m : 1);
         for (int32_t q = 0; q < m; ++q) busy[q] = 0;
-        if (o->status[j] != ORC_OK) continue;
-        const uint64_t E = ro.elapsed;
+        if (o->status[j] != ORC_OK || rg->pass == 1) continue;
+        const uint64_t E = o->elapsed[j];
         u128 num = 0, den = 0;
         for (int32_t did = 0; did < in->d_ids; ++did) {
             const int32_t q = in->d_decl ? in->d_decl[did] : did;     /* declaration position */

@@ -72,7 +72,10 @@ class SortInfo(C.Structure):
 
 
 class RegionsABI(C.Structure):
-    _fields_ = [("start", _p), ("end", _p), ("count", C.c_int32), ("reserved", C.c_int32), ("dev_owner", _p)]
+    _fields_ = [("start", _p), ("end", _p), ("count", C.c_int32), ("flags", C.c_int32), ("dev_owner", _p)]
+
+
+REGIONS_PER_RANK = 1
 
 
 class RegionResult(C.Structure):

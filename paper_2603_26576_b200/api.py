@@ -18,6 +18,7 @@ the fused analysis kernel; there is no CPU compute path.
 
 from __future__ import annotations
 
+from collections.abc import Mapping
 from dataclasses import dataclass
 
 import numpy as np
@@ -217,23 +218,45 @@ class RegionReport:
     reference raises AnalysisError); ``offload_busy[g]`` is the owner's offload
     time during which device g was busy, inside the region."""
 
-    window: tuple[int, int]
+    window: object               # (start, end) or {rank: (start, end)}, as given
     report: MetricsReport | None
     offload_busy: tuple[int, ...]
     offload_busy_fraction: float | None
 
 
 def region_reports(trace: Trace, windows) -> list[RegionReport]:
-    """Region metric trees for ``windows`` = ``[(start, end), ...]`` (K5 + K6 kernels).
+    """Region metric trees (K5 + K6 kernels).  ``windows`` lists the regions; each is
+    ``(start, end)`` -- one window for every rank and device -- or a mapping
+    ``{rank: (start, end)}`` -- a per-rank region (TALP annotates regions per process,
+    PAPER.md:113): each rank's records are clipped to its own window and shifted by its
+    own start, devices follow their ``owner_rank``; ranks missing from the mapping and
+    devices without a declared owner record nothing in that region.  With any mapping
+    present every region is evaluated per rank (a plain window applies to all ranks).
 
     Raises InvalidTraceError for an invalid trace (validation runs first).
-    Region reports carry summaries and metrics; their ``warnings`` are empty."""
+    Region reports carry summaries and metrics; their ``warnings`` are empty.
+    ``RegionReport.window`` is the region as given."""
     import torch
 
     from .engine import DeviceTrace, analyze_regions
 
     packed = pack_trace(trace)
-    windows = [(int(a), int(b)) for a, b in windows]
+    windows = list(windows)
+    per_rank = any(isinstance(w, Mapping) for w in windows)
+    if per_rank:   # [R][host_ids][2] over the dense host ids
+        dense = {rank: i for i, rank in enumerate(packed.host_ids)}
+        table = np.zeros((len(windows), len(packed.host_ids), 2), dtype=np.uint64)
+        for j, w in enumerate(windows):
+            if isinstance(w, Mapping):
+                for rank, (a, b) in w.items():
+                    if rank in dense:
+                        table[j, dense[rank]] = (int(a), int(b))
+            else:
+                table[j, :] = (int(w[0]), int(w[1]))
+        given, windows = windows, table
+    else:
+        windows = [(int(a), int(b)) for a, b in windows]
+        given = windows
     dev = torch.device("cuda", int(__import__("os").environ.get("HETEFF_DEVICE", "0")))
 
     def up(a):
@@ -252,7 +275,7 @@ def region_reports(trace: Trace, windows) -> list[RegionReport]:
         _, f = _run(trace, N.MODE_VALIDATE)
         _raise_invalid(trace, packed, f)
     out = []
-    for w, r in zip(windows, run.regions):
+    for w, r in zip(given, run.regions):
         if r.status != N.OK:
             out.append(RegionReport(w, None, tuple(int(x) for x in r.offload_busy), None))
             continue

@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <vector>
 #include <cstdlib>
 #include <string>
 
@@ -193,7 +194,7 @@ static int run_once(heteff_ctx *ctx, const heteff_trace *t, const heteff_options
     }
     const size_t ob_res = 256, ob_h = (size_t)(t->n > 0 ? t->n : 0) * 32, ob_d = (size_t)(t->m > 0 ? t->m : 0) * 32;
     const size_t ob_total = ob_res + ob_h + ob_d;
-    CK(ensure(ctx->out_blk, ob_total, false), "alloc result block");
+    CK(ensure(ctx->out_blk, ob_total, true), "alloc result block");   // zeroed once: every byte the D2H reads is defined
     if (ctx->out_pin_bytes < ob_total) {
         if (ctx->out_pin) cudaFreeHost(ctx->out_pin);
         ctx->out_pin = nullptr;
@@ -452,7 +453,11 @@ int heteff_analyze_regions(heteff_ctx *ctx, const heteff_trace *t, const heteff_
                            heteff_region_outputs *out, void *stream)
 {
     if (!ctx || !t || !rg || !out || rg->count < 0) return fail(ctx, HETEFF_BAD_ARG, "bad argument");
-    if (rg->count > 0 && (!rg->start || !rg->end || !out->results)) return fail(ctx, HETEFF_BAD_ARG, "null argument");
+    if (rg->flags & ~HETEFF_REGIONS_PER_RANK) return fail(ctx, HETEFF_BAD_ARG, "unknown region flags");
+    const bool per_rank = (rg->flags & HETEFF_REGIONS_PER_RANK) != 0;
+    const bool no_table = per_rank && t->host_ids == 0;   // per-rank regions without ranks: empty tables
+    if (rg->count > 0 && (!out->results || (!no_table && (!rg->start || !rg->end))))
+        return fail(ctx, HETEFF_BAD_ARG, "null argument");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CK(cudaSetDevice(ctx->device), "cudaSetDevice");
     // the whole trace first: validity and canonical order are preconditions
@@ -485,12 +490,13 @@ int heteff_analyze_regions(heteff_ctx *ctx, const heteff_trace *t, const heteff_
     const size_t b_dsub = up((size_t)(tiles + 1) * hb::region_subs() * 64);
     const size_t b_hacc = up((size_t)W * hid * 24), b_dacc = up((size_t)W * did * 32);
     const size_t b_E = up(W * 8), b_dmax = up(W * 8), b_own = up((size_t)did * 4);
+    const size_t b_hwin = per_rank ? up((size_t)W * hid * 16) : 0;
     CK(ensure(ctx->reg_ws, b_hseg + b_dseg + b_hagg + b_hck + b_dagg + b_drun + b_dsum + b_dck + b_scan + b_tst + b_dsub + b_hacc +
-                               b_dacc + b_E + b_dmax + b_own, false),
+                               b_dacc + b_E + b_dmax + b_own + b_hwin, false),
        "alloc regions");
     const size_t b_ho = up((size_t)W * nn * 32), b_do = up((size_t)W * mm * 32), b_bo = up((size_t)W * mm * 8);
     const size_t b_res = up(W * sizeof(hb::RegionResultDev));
-    CK(ensure(ctx->reg_out, b_ho + b_do + b_bo + b_res, false), "alloc region outputs");
+    CK(ensure(ctx->reg_out, b_ho + b_do + b_bo + b_res, true), "alloc region outputs");   // zeroed once (initcheck)
     uint8_t *w = static_cast<uint8_t *>(ctx->reg_ws.p);
     hb::RegParams p;
     memset(&p, 0, sizeof(p));
@@ -519,6 +525,8 @@ int heteff_analyze_regions(heteff_ctx *ctx, const heteff_trace *t, const heteff_
     p.E = static_cast<u64 *>(take(b_E));
     p.dmax = static_cast<u64 *>(take(b_dmax));
     int32_t *own = static_cast<int32_t *>(take(b_own));
+    u64 *hwin = per_rank ? static_cast<u64 *>(take(b_hwin)) : nullptr;
+    std::vector<u64> hwin_h(per_rank ? (size_t)W * hid * 2 : 0);
     p.tiles = tiles;
     p.hchunks = hch;
     if (rg->dev_owner && t->dev_ids > 0) {
@@ -545,21 +553,28 @@ int heteff_analyze_regions(heteff_ctx *ctx, const heteff_trace *t, const heteff_
     for (int32_t j0 = 0; j0 < rg->count; j0 += W) {
         const int R = rg->count - j0 < W ? rg->count - j0 : W;
         p.R = R;
+        if (per_rank) {   // [R][host_ids][2] of this pass, one H2D (start / end are [count][host_ids])
+            for (int j = 0; j < R; ++j)
+                for (int64_t id = 0; id < t->host_ids; ++id) {
+                    const size_t src = (size_t)(j0 + j) * (size_t)t->host_ids + (size_t)id;
+                    hwin_h[((size_t)j * t->host_ids + id) * 2] = rg->start[src];
+                    hwin_h[((size_t)j * t->host_ids + id) * 2 + 1] = rg->end[src];
+                }
+            if (t->host_ids > 0)
+                CK(cudaMemcpyAsync(hwin, hwin_h.data(), (size_t)R * t->host_ids * 16, cudaMemcpyHostToDevice, s),
+                   "h2d windows");
+            p.hwin = hwin;
+        }
         for (int j = 0; j < W; ++j) {
-            const bool live = j < R;
+            const bool live = j < R && !per_rank;
             const uint64_t a = live ? rg->start[j0 + j] : 0, b = live ? rg->end[j0 + j] : 0;
             p.wlo[j] = a;
             p.whi[j] = b > a ? b : a;
-            p.wtop[j] = a;
         }
         CK(cudaMemsetAsync(p.E, 0, b_E + b_dmax, s), "memset");
         CK(cudaEventRecord(ctx->ev0, s), "event");
         CK(hb::launch_regions_phase1(p, s), "launch regions phase 1");
-        u64 Eh[hb::kMaxWindows];
-        CK(cudaMemcpyAsync(Eh, p.E, sizeof(Eh), cudaMemcpyDeviceToHost, s), "d2h E");
-        CK(cudaStreamSynchronize(s), "regions phase 1");
-        for (int j = 0; j < R; ++j) p.wtop[j] = p.wlo[j] + Eh[j];
-        CK(hb::launch_regions_phase2(p, s), "launch regions phase 2");
+        CK(hb::launch_regions_phase2(p, s), "launch regions phase 2");   // reads E_j from device memory
         CK(cudaEventRecord(ctx->ev1, s), "event");
         CK(cudaMemcpyAsync(rh, p.res, sizeof(hb::RegionResultDev) * R, cudaMemcpyDeviceToHost, s), "d2h results");
         if (out->host_summaries && t->n > 0)

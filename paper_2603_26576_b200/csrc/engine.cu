@@ -123,35 +123,44 @@ struct TileInfo {
     u64 t0, t1;
 };
 
+// Per-tile header and compute scratch live in kHdr slots indexed by the tile's
+// sequence number in the CTA, not by its data stage, so the header of tile i+2
+// never overwrites tile i's while any warp still reads it, whenever the warps
+// release the stage.  (Releasing a stage early -- as soon as a warp holds its
+// records in registers -- was measured: 0.4-2.6 % slower on C2 / C3 / C5, so
+// warps release at the end of the tile.)  Warps drift at most two tiles apart
+// (tile i+3 needs every warp's release of tile i+1): 4 slots never alias.
+constexpr int kHdr = 4;
+
 struct Ctrl {
     uint64_t full[kStages];    // TMA warp -> compute: tile data landed
     uint64_t empty[kStages];   // compute -> TMA warp: stage consumed
     uint64_t info_full[kRing];  // compute -> epilogue warp: device tile published
     uint64_t info_empty[kRing]; // epilogue warp -> compute: descriptor slot free
     TileInfo info[kRing];
-    int64_t tile[kStages];
+    int64_t tile[kStages];     // read right after the full wait (before any release)
     int32_t cnt[kStages];
-    int32_t has_prev[kStages];
-    int32_t prev_res[kStages];
+    int32_t has_prev[kHdr];
+    int32_t prev_res[kHdr];
     int32_t is_last;
-    int32_t r0[kStages];       // CSR: first resource of the tile, leading records of it
-    int32_t r0cnt[kStages];
-    int32_t uni[kStages];      // CSR tile of ONE resource: its id (the stage's res column is not written), else -1
-    u64 prev_start[kStages];
-    u64 prev_end[kStages];
-    // host tiles: per-stage max end and finished-warp count (smem atomics)
-    u64 h_max[kStages];
-    unsigned int h_cnt[kStages];
+    int32_t r0[kHdr];          // CSR: first resource of the tile, leading records of it
+    int32_t r0cnt[kHdr];
+    int32_t uni[kHdr];         // CSR tile of ONE resource: its id (the stage's res column is not written), else -1
+    u64 prev_start[kHdr];
+    u64 prev_end[kHdr];
+    // host tiles: per-tile max end and finished-warp count (smem atomics)
+    u64 h_max[kHdr];
+    unsigned int h_cnt[kHdr];
     // single-segment device tiles: per-warp 32-bit aggregates relative to the tile base
-    uint32_t f_k[kStages][kComputeWarps];
-    uint32_t f_km[kStages][kComputeWarps];
-    int32_t f_fit[kStages][kComputeWarps];
-    // per-stage warp aggregates of the tile (written by compute warps)
-    int32_t w_flag[kStages][kComputeWarps];
-    u64 w_v0[kStages][kComputeWarps];
-    u64 w_v1[kStages][kComputeWarps];
-    u64 w_mn[kStages][kComputeWarps];
-    u64 w_mx[kStages][kComputeWarps];
+    uint32_t f_k[kHdr][kComputeWarps];
+    uint32_t f_km[kHdr][kComputeWarps];
+    int32_t f_fit[kHdr][kComputeWarps];
+    // per-tile warp aggregates (written by compute warps)
+    int32_t w_flag[kHdr][kComputeWarps];
+    u64 w_v0[kHdr][kComputeWarps];
+    u64 w_v1[kHdr][kComputeWarps];
+    u64 w_mn[kHdr][kComputeWarps];
+    u64 w_mx[kHdr][kComputeWarps];
     CsrSample csr[2];          // host, device (producer warp only)
     ClaimStage claim;          // the CSR claim in flight (producer warp only)
 };
@@ -187,10 +196,13 @@ __device__ __noinline__ void contract(const Params &p, unsigned flag, int64_t gi
     atomicMin(&p.g->contract_index, (long long)gi);
 }
 
-// named barrier over the compute warps only
+// named barrier over the compute warps only.  Non-.aligned (`bar.sync` is
+// barrier.sync.aligned): the per-warp schedule choice (dev_single<true/false>) and
+// lane-predicated stores mean the compiler cannot prove a warp converged here, and
+// compute-sanitizer synccheck flagged the aligned form ("divergent thread(s)").
 __device__ __forceinline__ void bar_compute()
 {
-    asm volatile("bar.sync 1, %0;" ::"n"(kComputeThreads) : "memory");
+    asm volatile("barrier.sync 1, %0;" ::"n"(kComputeThreads) : "memory");
 }
 
 __device__ __forceinline__ u64 warp_max(u64 v)
@@ -536,7 +548,8 @@ __device__ __noinline__ int csr_fill(const int64_t *seg, int32_t ids, int64_t ba
 }
 
 template <bool CSR>
-__device__ void produce(const Params &p, StageSmem *stages, Ctrl *c, int st, const Claim &cl, int lane, uint64_t pol)
+__device__ void produce(const Params &p, StageSmem *stages, Ctrl *c, int st, int hs, const Claim &cl, int lane,
+                        uint64_t pol)
 {
     const int64_t t = cl.t;
     const int64_t total = p.host_tiles + p.dev_tiles;
@@ -566,13 +579,13 @@ __device__ void produce(const Params &p, StageSmem *stages, Ctrl *c, int st, con
         if (lane == 0) {
             c->tile[st] = t;
             c->cnt[st] = cnt;
-            c->has_prev[st] = base > 0;
-            c->prev_res[st] = cl.prev_r;
-            c->prev_start[st] = cl.prev_s;
-            c->prev_end[st] = cl.prev_e;
-            c->r0cnt[st] = -1;
-            c->r0[st] = 0;
-            c->uni[st] = -1;
+            c->has_prev[hs] = base > 0;
+            c->prev_res[hs] = cl.prev_r;
+            c->prev_start[hs] = cl.prev_s;
+            c->prev_end[hs] = cl.prev_e;
+            c->r0cnt[hs] = -1;
+            c->r0[hs] = 0;
+            c->uni[hs] = -1;
         }
         __syncwarp();
         if (lane == 0) {
@@ -633,13 +646,13 @@ __device__ void produce(const Params &p, StageSmem *stages, Ctrl *c, int st, con
         if (lane == 0) {
             c->tile[st] = t;
             c->cnt[st] = cnt;
-            c->has_prev[st] = base > 0;
-            c->prev_res[st] = cl.prev_r;
-            c->prev_start[st] = cl.prev_s;
-            c->prev_end[st] = cl.prev_e;
-            c->r0cnt[st] = r0cnt;
-            c->r0[st] = cl.r0;
-            c->uni[st] = uni;
+            c->has_prev[hs] = base > 0;
+            c->prev_res[hs] = cl.prev_r;
+            c->prev_start[hs] = cl.prev_s;
+            c->prev_end[hs] = cl.prev_e;
+            c->r0cnt[hs] = r0cnt;
+            c->r0[hs] = cl.r0;
+            c->uni[hs] = uni;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&c->full[st]);
@@ -740,8 +753,20 @@ struct TileCtx {
     int64_t lt;        // tile index within its side
     int64_t gbase;     // global record index of item 0 of this tile
     int cnt;
-    int st;            // stage holding this tile
+    int st;            // header / scratch slot of this tile (kHdr ring; the data stage is separate)
+    uint64_t *empty;   // the data stage's empty barrier
+    bool released;     // this warp has released the data stage
 };
+
+// The warp no longer reads the tile's stage: the producer may refill it.
+// Warp-uniform; once per tile.
+__device__ __forceinline__ void release(TileCtx &tc, int lane)
+{
+    if (tc.released) return;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(tc.empty);
+    tc.released = true;
+}
 
 // combine two segmented-max scan elements, a earlier than b
 __device__ __forceinline__ void seg_combine(bool af, u64 a0, u64 a1, bool &bf, u64 &b0, u64 &b1)
@@ -961,11 +986,13 @@ __device__ __forceinline__ void phase_a(const StageSmem &sm, const Ctrl *c, int 
         pr = rid(sm, uni, b - 1);
     }
     mn = sm.s[b];
+    u64 ms = 0;   // max START: a (malformed) start above every end must still leave the 2^32 window
 #pragma unroll kUnrollG
     for (int j = 0; j < kItems; ++j) {
         if (j < nv) {
             const int32_t r = rid(sm, uni, b + j);
             const u64 e = sm.e[b + j];
+            ms = umax(ms, sm.s[b + j]);
             if ((j == 0 && !hp) || r != pr) {
                 sfm |= 1u << j;
                 mx = umax(mx, DEV ? v1 : v0);
@@ -982,7 +1009,7 @@ __device__ __forceinline__ void phase_a(const StageSmem &sm, const Ctrl *c, int 
             pr = r;
         }
     }
-    mx = umax(mx, DEV ? v1 : v0);
+    mx = umax(umax(mx, DEV ? v1 : v0), ms);
 }
 
 // record values in the arithmetic domain of phase B: 32-bit tile-relative
@@ -1182,16 +1209,20 @@ __device__ __noinline__ u64 host_rare(const Params &p, const StageSmem &sm, cons
 // Fast path for a thread whose records all belong to one rank and lie in one
 // aligned 2^32 ns window: every check and sum in 32 bits relative to the
 // window.  Returns false (results unused) if a record leaves the window.
+template <bool FULL>
 __device__ __forceinline__ bool host_fast32(const StageSmem &sm, int b, int nv, bool cont, u64 ps64, u64 pe64,
                                             bool &rare, bool &ovl, u64 &off, u64 &mpi, u64 &last)
 {
-    const u64 base = sm.s[b];
-    const uint32_t bh = (uint32_t)(base >> 32), bl = (uint32_t)base;
-    // the previous record of the same rank (cont): relative start / usable end, clamped into the window
+    if (FULL) nv = kItems;   // full tiles: the guard below folds away
+    // the ALIGNED 2^32 window holding the thread's first start: relative values are the
+    // low words and the window test is one compare of the high word per value
+    const u64 first = sm.s[b];
+    const u64 base = first & 0xffffffff00000000ull;
+    const uint32_t bh = (uint32_t)(base >> 32), bl = (uint32_t)base;   // bl == 0
+    // the previous record of the same rank (cont): order (64-bit), usable end clamped into the window
     uint32_t ps = 0, pe = 0;
     if (cont) {
-        ps = ps64 >= base ? (uint32_t)(ps64 - base) : 0u;
-        rare = rare || ps64 > base;                                     // order
+        rare = rare || ps64 > first;                                    // order
         pe = pe64 <= base ? 0u : (pe64 - base > 0xffffffffull ? 0xffffffffu : (uint32_t)(pe64 - base));
     }
     bool out = false;
@@ -1203,7 +1234,7 @@ __device__ __forceinline__ bool host_fast32(const StageSmem &sm, int b, int nv, 
             const u64 s64 = sm.s[i], e64 = sm.e[i];   // conflict-free LDS.64 at the odd record stride
             const uint32_t sl = (uint32_t)s64, sh = (uint32_t)(s64 >> 32), el = (uint32_t)e64, eh = (uint32_t)(e64 >> 32);
             const uint8_t k = sm.k[i];
-            out = out || sh != bh || eh != bh || sl < bl || el < bl;   // outside [base, base + 2^32)
+            out = out || sh != bh || eh != bh;   // outside [base, base + 2^32)
             const uint32_t s = sl - bl, e = el - bl;
             rare = rare || (j > 0 && s < ps) || s >= e;   // order / zero-length / malformed
             const bool usable = s < e;
@@ -1227,14 +1258,14 @@ __device__ __forceinline__ bool host_fast32(const StageSmem &sm, int b, int nv, 
 // 32-bit sums leave through REDUX (two 16-bit limbs) and one RED per field per warp.
 // Per warp: returns false (nothing emitted) if some lane leaves its 2^32 window --
 // that warp then runs the general path (host tiles need no CTA barrier).
-__device__ __forceinline__ bool host_single(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc,
+__device__ __forceinline__ bool host_single(const Params &p, const StageSmem &sm, Ctrl *c, TileCtx &tc,
                                             int tid, Phases &ph)
 {
     const int32_t uni = c->uni[tc.st];   // CSR tile of one resource: its id (sm.r not filled)
     ph.mark();
     const int lane = tid & 31;
     const int b = tid * kItems;
-    const int nv = max(0, min(kItems, tc.cnt - b));
+    constexpr int nv = kItems;   // full tiles only (host_compute)
     const int64_t gi0 = tc.gbase + (int64_t)b;
     const int32_t r0 = rid(sm, uni, 0);
     const bool has_prev = c->has_prev[tc.st] != 0;
@@ -1258,7 +1289,7 @@ __device__ __forceinline__ bool host_single(const Params &p, const StageSmem &sm
         rare = rare || !declared(p.host_decl, p.host_ids, p.n, r0);
     }
     u64 off = 0, mpi = 0, last = 0;
-    const bool ok = nv == 0 || host_fast32(sm, b, nv, cont, ps, pe, rare, ovl, off, mpi, last);
+    const bool ok = host_fast32<true>(sm, b, nv, cont, ps, pe, rare, ovl, off, mpi, last);
     if (!__all_sync(0xffffffffu, ok)) return false;
     u64 tmax = last;
     if (ovl && !*(volatile unsigned *)&p.g->ovl_suspect) atomicOr(&p.g->ovl_suspect, 1u);
@@ -1286,12 +1317,13 @@ __device__ __forceinline__ bool host_single(const Params &p, const StageSmem &sm
     return true;
 }
 
-__device__ __forceinline__ void host_compute(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc,
+__device__ __forceinline__ void host_compute(const Params &p, const StageSmem &sm, Ctrl *c, TileCtx &tc,
                                              int tid, Phases &ph)
 {
     const int32_t uni = c->uni[tc.st];   // CSR tile of one resource: its id (sm.r not filled)
 #ifndef HB_NO_HOST_SINGLE
-    if (tc.cnt > 0 && rid(sm, uni, 0) == rid(sm, uni, tc.cnt - 1) && host_single(p, sm, c, tc, tid, ph)) return;
+    // full single-rank tiles (every tile but the last of the side): the unguarded fast path
+    if (tc.cnt == kTile && rid(sm, uni, 0) == rid(sm, uni, tc.cnt - 1) && host_single(p, sm, c, tc, tid, ph)) return;
 #endif
     ph.mark();
     const int warp = tid >> 5, lane = tid & 31;
@@ -1333,7 +1365,7 @@ __device__ __forceinline__ void host_compute(const Params &p, const StageSmem &s
         const bool cont = hp && pr == rid(sm, uni, b);
         bool r2 = rare, o2 = ovl;
         u64 of2, mp2, la2;
-        if (host_fast32(sm, b, nv, cont, ps, pe, r2, o2, of2, mp2, la2)) {
+        if (host_fast32<false>(sm, b, nv, cont, ps, pe, r2, o2, of2, mp2, la2)) {
             if (!cont) {
                 sfm = 1u;
                 P.head_open = false;
@@ -1503,7 +1535,7 @@ __device__ __forceinline__ u64 device_E(const Params &p, int tid, int lane, u64 
 // Returns false (nothing done) if some end leaves the window.
 // -------------------------------------------------------------------------
 template <bool MERGED>
-__device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
+__device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm, Ctrl *c, TileCtx &tc, int tid,
                                            u64 &E_cache, bool &E_known, int &hpend, int &kq, bool &one_pass,
                                            Phases &ph)
 {
@@ -1511,16 +1543,22 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
     ph.mark();
     const int warp = tid >> 5, lane = tid & 31;
     const int b = tid * kItems;
-    const int nv = max(0, min(kItems, tc.cnt - b));
+    constexpr int nv = kItems;   // full tiles only (dev_compute): the per-record guards fold away
     const int64_t gi0 = tc.gbase + (int64_t)b;
-    const u64 base = sm.s[0];
-    const uint32_t bl = (uint32_t)base, bh = (uint32_t)(base >> 32);
+    // the ALIGNED 2^32 ns window holding the tile's first start: relative values are the
+    // low words, one high-word compare per value tests the window
+    const u64 base = sm.s[0] & 0xffffffff00000000ull;
+    const uint32_t bl = (uint32_t)base, bh = (uint32_t)(base >> 32);   // bl == 0
     constexpr bool merged = MERGED;
     uint32_t runK = 0, runKM = 0, cK = 0, cKM = 0, ps = 0;
     uint32_t er[MERGED ? 1 : kItems], sr[MERGED ? 1 : kItems];
     uint32_t kmask = 0;             // bit j: record j is a kernel
     bool out = false, bad = false;  // bad: start outside the window / order / zero-length / malformed
-    if (b > 0) ps = (uint32_t)sm.s[b - 1] - bl;
+    if (b > 0) {   // the predecessor's start (order of the first record): exact only inside the window
+        const u64 p64 = sm.s[b - 1];
+        ps = (uint32_t)p64 - bl;
+        bad = (uint32_t)(p64 >> 32) != bh;
+    }
     if constexpr (merged) {
         er[0] = 0;
 #pragma unroll kUnrollB
@@ -1528,9 +1566,9 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
             if (j < nv) {
                 const u64 s64 = sm.s[b + j], e64 = sm.e[b + j];   // conflict-free LDS.64 at the odd record stride
                 const uint32_t sl = (uint32_t)s64, el = (uint32_t)e64;
-                out = out || (uint32_t)(e64 >> 32) != bh || el < bl;
+                out = out || (uint32_t)(e64 >> 32) != bh;
                 const uint32_t s0 = sl - bl, e = el - bl;
-                bad = bad || (uint32_t)(s64 >> 32) != bh || sl < bl || ((j > 0 || b > 0) && s0 < ps) || s0 >= e;
+                bad = bad || (uint32_t)(s64 >> 32) != bh || ((j > 0 || b > 0) && s0 < ps) || s0 >= e;
                 const uint32_t s = min(s0, e);
                 const uint32_t loKM = max(runKM, s);
                 runKM = max(runKM, e);
@@ -1552,11 +1590,12 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
             sr[j] = 0;
             if (j < nv) {
                 const u64 e64 = sm.e[b + j], s64 = sm.s[b + j];
-                const uint32_t e = (uint32_t)e64 - bl, sl = (uint32_t)s64;
-                out = out || (uint32_t)(e64 >> 32) != bh || (uint32_t)e64 < bl;
-                bad = bad || (uint32_t)(s64 >> 32) != bh || sl < bl;
+                const uint32_t e = (uint32_t)e64 - bl, sl = (uint32_t)s64, s0 = sl - bl;
+                out = out || (uint32_t)(e64 >> 32) != bh;
+                bad = bad || (uint32_t)(s64 >> 32) != bh || ((j > 0 || b > 0) && s0 < ps) || s0 >= e;
+                ps = s0;
                 er[MERGED ? 0 : j] = e;
-                sr[MERGED ? 0 : j] = sl - bl;
+                sr[MERGED ? 0 : j] = s0;
                 runKM = max(runKM, e);
                 if (sm.k[b + j] == 0) { runK = max(runK, e); kmask |= 1u << j; }
             }
@@ -1615,7 +1654,6 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
         for (int j = 0; j < kItems; ++j) {
             if (j < nv) {
                 const uint32_t s0 = sr[MERGED ? 0 : j], e0 = er[MERGED ? 0 : j];
-                bad = bad || ((j > 0 || b > 0) && s0 < ps) || s0 >= e0;
                 const uint32_t e = min(e0, Er), s = min(s0, e);
                 const uint32_t loKM = max(runKM, s);
                 runKM = max(runKM, e);
@@ -1625,7 +1663,6 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
                     runK = max(runK, e);
                     cK += runK - loK;
                 }
-                ps = s0;
             }
         }
     } else if (clamp) {
@@ -1680,12 +1717,13 @@ __device__ __forceinline__ bool dev_single(const Params &p, const StageSmem &sm,
 __device__ __forceinline__ void dev_general(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
                                   u64 &E_cache, bool &E_known, int &hpend, int &k, Phases &ph);
 
-__device__ __forceinline__ void dev_compute(const Params &p, const StageSmem &sm, Ctrl *c, const TileCtx &tc, int tid,
+__device__ __forceinline__ void dev_compute(const Params &p, const StageSmem &sm, Ctrl *c, TileCtx &tc, int tid,
                                             u64 &E_cache, bool &E_known, int &hpend, int &k, bool &one_pass,
                                             Phases &ph)
 {
     const int32_t uni = c->uni[tc.st];   // CSR tile of one resource: its id (sm.r not filled)
-    if (tc.cnt > 0 && rid(sm, uni, 0) == rid(sm, uni, tc.cnt - 1)) {
+    // full single-device tiles (every tile but the last of the side): the unguarded fast path
+    if (tc.cnt == kTile && rid(sm, uni, 0) == rid(sm, uni, tc.cnt - 1)) {
 #if HB_DEV_SCHED == 0
         const bool done = dev_single<false>(p, sm, c, tc, tid, E_cache, E_known, hpend, k, one_pass, ph);
 #elif HB_DEV_SCHED == 1
@@ -1947,6 +1985,8 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&c->full[s], 1);
             mbar_init(&c->empty[s], kComputeWarps);
+        }
+        for (int s = 0; s < kHdr; ++s) {
             c->h_max[s] = 0;
             c->h_cnt[s] = 0;
         }
@@ -1963,7 +2003,7 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
         // ---------------- TMA warp: keep every stage in flight ----------------
         const uint64_t pol = l2_policy_evict_first();
         for (int s = 0; s < kStages; ++s)
-            produce<false>(p, stages, c, s, claim_finish(p, claim_issue(p, lane)), lane, pol);
+            produce<false>(p, stages, c, s, s % kHdr, claim_finish(p, claim_issue(p, lane)), lane, pol);
         // claims run ahead of use: the atomic is issued one refill before its index is
         // needed and the previous-record loads one refill before the TMA issue
         Claim next = claim_finish(p, claim_issue(p, lane));
@@ -1977,7 +2017,7 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
             mbar_wait(&c->empty[st], ph);
             PROF_ADD(pa, t0);
             t0 = PROF_NOW();
-            produce<false>(p, stages, c, st, next, lane, pol);
+            produce<false>(p, stages, c, st, (it + kStages) % kHdr, next, lane, pol);
             next = claim_finish(p, pend);
             pend = claim_issue(p, lane);
             PROF_ADD(pb, t0);
@@ -2001,7 +2041,7 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
         csr_sample_fill(p.dseg, p.dev_ids, c->csr[1], lane);
         for (int s = 0; s < kStages; ++s) {
             const PendClaim pc = claim_start(p, c->csr, c->claim, claim_issue(p, lane), lane);
-            produce<true>(p, stages, c, s, claim_done(p, c->csr, pc, c->claim, lane), lane, pol);
+            produce<true>(p, stages, c, s, s % kHdr, claim_done(p, c->csr, pc, c->claim, lane), lane, pol);
         }
         Claim next;
         {
@@ -2019,7 +2059,7 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
             mbar_wait(&c->empty[st], ph);
             PROF_ADD(pa, t0);
             t0 = PROF_NOW();
-            produce<true>(p, stages, c, st, next, lane, pol);
+            produce<true>(p, stages, c, st, (it + kStages) % kHdr, next, lane, pol);
             next = claim_done(p, c->csr, mid, c->claim, lane);
             mid = claim_start(p, c->csr, c->claim, pend, lane);
             pend = claim_issue(p, lane);
@@ -2074,8 +2114,10 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
             const int64_t t = c->tile[st];
             if (t < 0) break;
             TileCtx tc;
-            tc.st = st;
+            tc.st = it % kHdr;
             tc.cnt = c->cnt[st];
+            tc.empty = &c->empty[st];
+            tc.released = false;
             const bool dev = t >= p.host_tiles;
             tc.lt = dev ? t - p.host_tiles : t;
             tc.gbase = tc.lt * kTile;
@@ -2088,8 +2130,7 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
 #ifdef HB_PROF
             if (dev) ++phs.dn; else ++phs.hn;
 #endif
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&c->empty[st]);
+            release(tc, lane);
             PROF_ADD(cb, t0);
 #ifdef HB_PROF
             ++cn;

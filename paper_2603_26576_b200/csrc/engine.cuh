@@ -144,7 +144,10 @@ struct RegParams {
     int32_t n, m;
     int32_t R;                              // windows of this pass (<= kMaxWindows)
     u64 wlo[kMaxWindows], whi[kMaxWindows]; // window bounds, padded with empty [0, 0)
-    u64 wtop[kMaxWindows];                  // phase 2: wlo + E (the region's clamp end)
+    // per-rank regions: [R][host_ids][2] window of every rank for this pass (device
+    // memory), devices take their owner's window, unowned devices an empty one;
+    // null = the global windows wlo / whi
+    const u64 *hwin;
     const int32_t *owner;                   // [dev_ids] dense host id or -1 (null = none)
     int64_t *hseg, *dseg;                   // [ids + 1] CSR offsets per dense id
     // window-independent checkpoints (prefix of the resource's segment at each chunk start)

@@ -80,6 +80,33 @@ __device__ __forceinline__ int32_t decl_pos(const int32_t *decl, int32_t r) { re
 
 __device__ __forceinline__ u64 sub0(u64 a, u64 b) { return a > b ? a - b : 0ull; }
 
+// window of region j for host rank `id`: its own (per-rank regions) or the global one
+__device__ __forceinline__ void host_window(const RegParams &p, int j, int32_t id, u64 &a, u64 &b)
+{
+    if (p.hwin) {
+        const u64 *w = p.hwin + ((size_t)j * p.host_ids + id) * 2;
+        a = w[0];
+        b = umax(w[1], a);
+    } else {
+        a = p.wlo[j];
+        b = p.whi[j];
+    }
+}
+
+// window of region j for device `id`: its owner rank's (per-rank regions; none without
+// an owner) or the global one
+__device__ __forceinline__ void dev_window(const RegParams &p, int j, int32_t id, u64 &a, u64 &b)
+{
+    if (p.hwin) {
+        const int32_t o = p.owner ? p.owner[id] : -1;
+        if (o < 0 || o >= p.host_ids) { a = b = 0; return; }
+        host_window(p, j, o, a, b);
+    } else {
+        a = p.wlo[j];
+        b = p.whi[j];
+    }
+}
+
 // first index in [lo, hi) with v[i] >= x  (lower) / > x (upper); v non-decreasing there
 __device__ __forceinline__ int64_t lower_idx(const u64 *v, int64_t lo, int64_t hi, u64 x)
 {
@@ -362,7 +389,8 @@ __global__ void __launch_bounds__(128) rh_query(const __grid_constant__ RegParam
     if (x >= (int64_t)p.R * p.host_ids) return;
     const int j = (int)(x / p.host_ids);
     const int32_t id = (int32_t)(x % p.host_ids);
-    const u64 a = p.wlo[j], b = p.whi[j];
+    u64 a, b;
+    host_window(p, j, id, a, b);
     u64 off = 0, mpi = 0, span = 0;
     if (a < b) {
         const HostQ qa = host_query(p, id, a), qb = host_query(p, id, b);
@@ -776,7 +804,12 @@ __global__ void __launch_bounds__(128) rd_query(const __grid_constant__ RegParam
     if (x >= (int64_t)p.R * p.dev_ids) return;
     const int j = (int)(x / p.dev_ids);
     const int32_t id = (int32_t)(x % p.dev_ids);
-    const u64 lo = p.wlo[j], top = p.wtop[j], b = p.whi[j];
+    u64 lo, b;
+    dev_window(p, j, id, lo, b);
+    // the region's clamp end in trace time: window start + E_j (E_j <= b - lo for global
+    // windows; a per-rank window may be shorter than the longest rank's region)
+    const u64 E = p.E[j];
+    const u64 top = E > b - lo ? b : lo + E;
     u64 K = 0, KM = 0, clamp = 0, busy = 0;
     if (top > lo) {
         const int64_t d0 = p.dseg[id], d1 = p.dseg[id + 1];
@@ -925,14 +958,15 @@ cudaError_t launch_regions_phase1(const RegParams &p, cudaStream_t s)
 {
     using namespace reg;
     const int sms = sm_count();
-    if (p.n == 0 && p.tiles > 0) rd_dmax<<<grid_cap((p.tiles + 7) / 8, sms, 8), 256, 0, s>>>(p);
+    // device-only traces: E from the devices (per-rank regions: no rank owns a device -> E = 0)
+    if (p.n == 0 && p.tiles > 0 && !p.hwin) rd_dmax<<<grid_cap((p.tiles + 7) / 8, sms, 8), 256, 0, s>>>(p);
     const int64_t hq = (int64_t)p.R * p.host_ids;
     if (hq > 0) rh_query<<<(unsigned)((hq + 127) / 128), 128, 0, s>>>(p);
     reg_E<<<p.R, 256, 0, s>>>(p);
     return cudaGetLastError();
 }
 
-// phase 2 (p.wtop = window start + E filled in by the caller): device queries, finalize
+// phase 2 (after phase 1 in stream order: E per window in p.E): device queries, finalize
 cudaError_t launch_regions_phase2(const RegParams &p, cudaStream_t s)
 {
     using namespace reg;

@@ -71,6 +71,7 @@ __global__ void range_init(Range *g)
     g->kind_wide = 0;
     g->dmax = 0;
     g->neg = 0;
+    g->pad = 0;   // every byte the D2H reads is defined (compute-sanitizer initcheck)
 }
 
 __global__ void __launch_bounds__(512) range_kernel(const u64 *__restrict__ S, const u64 *__restrict__ E,

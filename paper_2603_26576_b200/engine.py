@@ -340,8 +340,11 @@ class RegionsRun:
 def analyze_regions(dt: DeviceTrace, windows, dev_owner=None, stream: int | None = None,
                     device: int | None = None, host_decl=None, dev_decl=None, host_ids: int | None = None,
                     dev_ids: int | None = None) -> RegionsRun:
-    """Region reports for ``windows`` (``[(start, end), ...]``) of HBM-resident columns.
+    """Region reports for ``windows`` of HBM-resident columns.
 
+    ``windows``: ``[R][2]`` -- one window per region for every rank and device -- or
+    ``[R][host_ids][2]`` -- per-rank regions: each rank's own window (dense host ids),
+    devices follow their owner, unowned devices record nothing in the region.
     ``dev_owner``: int32 [dev_ids] dense host id owning each device (-1 none)."""
     ctx = N.context(device)
     lib = N.load()
@@ -349,16 +352,23 @@ def analyze_regions(dt: DeviceTrace, windows, dev_owner=None, stream: int | None
     if host_ids is not None:
         t.host_ids, t.dev_ids = host_ids, dev_ids
         t.host_decl, t.dev_decl = _dptr(host_decl), _dptr(dev_decl)
-    w = np.ascontiguousarray(np.asarray(windows, dtype=np.uint64).reshape(-1, 2))
-    ws, we = np.ascontiguousarray(w[:, 0]), np.ascontiguousarray(w[:, 1])
-    R = w.shape[0]
+    warr = np.asarray(windows, dtype=np.uint64)
+    per_rank = warr.ndim == 3
+    if per_rank:
+        if warr.shape[1:] != (t.host_ids, 2):
+            raise ValueError(f"per-rank windows must be [R][{t.host_ids}][2], got {list(warr.shape)}")
+        ws, we = np.ascontiguousarray(warr[:, :, 0]), np.ascontiguousarray(warr[:, :, 1])
+    else:
+        w = np.ascontiguousarray(warr.reshape(-1, 2))
+        ws, we = np.ascontiguousarray(w[:, 0]), np.ascontiguousarray(w[:, 1])
+    R = warr.shape[0]
     owner = None if dev_owner is None else np.ascontiguousarray(dev_owner, dtype=np.int32)
     n, m = t.n, t.m
     results = (N.RegionResult * max(R, 1))()
     hs = np.zeros((max(R, 1), max(n, 1), 4), dtype=np.uint64)
     ds = np.zeros((max(R, 1), max(m, 1), 4), dtype=np.uint64)
     busy = np.zeros((max(R, 1), max(m, 1)), dtype=np.uint64)
-    rg = N.RegionsABI(_ptr(ws), _ptr(we), R, 0, _ptr(owner))
+    rg = N.RegionsABI(_ptr(ws), _ptr(we), R, N.REGIONS_PER_RANK if per_rank else 0, _ptr(owner))
     out = N.RegionOutputs(C.cast(results, C.c_void_p), hs.ctypes.data, ds.ctypes.data, busy.ctypes.data, 0.0)
     rc = lib.heteff_analyze_regions(ctx, C.byref(t), C.byref(rg), C.byref(out), stream)
     _check(ctx, rc)

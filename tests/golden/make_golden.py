@@ -448,6 +448,80 @@ def regions_corpus() -> list:
     return out
 
 
+def region_trace_per_rank(t: Trace, wins: dict) -> Trace:
+    """Per-rank region: every rank's records clipped to ITS window, every
+    device's records to its owner's window; ranks without a window and devices without
+    a declared owner record nothing in the region."""
+    owner = {d.device_id: d.owner_rank for d in t.devices}
+    hr = [HostRecord(r.rank, r.state, c) for r in t.host_records
+          if r.rank in wins and (c := clip_interval(r.interval, *wins[r.rank]))]
+    dr = [DeviceRecord(r.device_id, r.kind, c, r.stream) for r in t.device_records
+          if owner.get(r.device_id) in wins and owner[r.device_id] in t.host_processes
+          and (c := clip_interval(r.interval, *wins[owner[r.device_id]]))]
+    return Trace(host_processes=t.host_processes, devices=t.devices, host_records=tuple(hr),
+                 device_records=tuple(dr), time_unit=t.time_unit)
+
+
+def region_case_per_rank(t: Trace, regions, tag: str) -> dict:
+    regs = []
+    for wins in regions:
+        rt = region_trace_per_rank(t, wins)
+        rep = enc_report(rt)
+        ov = region_overlap(rt, rep["E"]) if "E" in rep else None
+        regs.append({"report": rep, "busy": ov[0] if ov else None, "frac": ov[1] if ov else None})
+    return {"tag": tag, "trace": enc_trace(t), "windows": [[[r, a, b] for r, (a, b) in w.items()] for w in regions],
+            "regions": regs}
+
+
+def regions_per_rank_corpus() -> list:
+    """Per-rank monitoring regions: each region a window per rank (nested per rank, shifted
+    between ranks, some ranks absent, empty and past-the-end windows)."""
+    out = []
+    rng = random.Random(0x5EED41)
+    for i in range(250):
+        t = random_valid_trace(rng, max_ranks=4, max_devices=4, max_segments=12)
+        if rng.random() < 0.3 and t.devices:   # some devices without an owner
+            t = Trace(host_processes=t.host_processes,
+                      devices=tuple(DeviceDecl(d.device_id, None if rng.random() < 0.5 else d.owner_rank)
+                                    for d in t.devices),
+                      host_records=t.host_records, device_records=t.device_records)
+        span = {}
+        for r in t.host_records:
+            span[r.rank] = max(span.get(r.rank, 0), r.interval.end)
+        regions = []
+        k = rng.randint(1, 6)
+        for j in range(k):                  # nested per rank, each rank its own span
+            w = {}
+            for p in t.host_processes:
+                sp = span.get(p, 0) + rng.randint(0, 20)
+                if rng.random() < 0.1:
+                    continue                # rank without this region
+                lo = j * sp // (2 * k + 1) + rng.randint(0, 3)
+                w[p] = (lo, max(lo, sp - j * sp // (2 * k + 1)))
+            regions.append(w)
+        for _ in range(2):                  # arbitrary per-rank windows
+            w = {}
+            for p in t.host_processes:
+                a = rng.randint(0, span.get(p, 0) + 10)
+                w[p] = (a, a + rng.randint(0, span.get(p, 0) // 2 + 2))
+            regions.append(w)
+        regions.append({p: (span.get(p, 0) + 5, span.get(p, 0) + 50) for p in t.host_processes})   # past the end
+        out.append(region_case_per_rank(t, regions, f"prank{i}"))
+    for name, r0, r1 in (("c1", 0, 4), ("c4", 0, 2), ("c3", 0, 1)):
+        cfg = CONFIGS[name]
+        (hs, he, hr, hk), (ds, de, dr, dk) = ogen.generate(cfg, r0, r1)
+        t = config_trace(cfg, r0, r1)
+        spans = {r0 + p: int(he[hr == p].max()) for p in range(r1 - r0)}
+        nw = 4 if name == "c3" else 16
+        regions = [{p: (k * sp // 40 + 7 * (p - r0), sp - k * sp // 40) for p, sp in spans.items()} for k in range(nw)]
+        c = region_case_per_rank(t, regions, f"{name}[{r0}:{r1}]")
+        del c["trace"]
+        c.update({"config": name, "r0": r0, "r1": r1})
+        out.append(c)
+        print(f"  per-rank regions {name}[{r0}:{r1}] {len(t.host_records) + len(t.device_records)} records")
+    return out
+
+
 # ---------------------------------------------------------------------------
 # interval algebra (intervals.py:40-105), acceptance criterion 2 shapes
 # ---------------------------------------------------------------------------
@@ -691,7 +765,7 @@ def main() -> None:
     only = sys.argv[sys.argv.index("--only") + 1].split(",") if "--only" in sys.argv else None
     jobs = {"presets": presets, "acceptance": acceptance_corpora, "invalid": invalid_corpus, "quarantine": quarantine_corpus,
             "summarize_device": summarize_device_corpus, "metrics": metrics_corpus,
-            "config_shards": config_shards, "regions": regions_corpus, "intervals": intervals_corpus,
+            "config_shards": config_shards, "regions": regions_corpus, "regions_per_rank": regions_per_rank_corpus, "intervals": intervals_corpus,
             "trace_docs": trace_docs_corpus, "imports": import_corpus, "renders": render_corpus}
     for name, fn in jobs.items():
         if only is None or name in only:
