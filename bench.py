@@ -13,11 +13,15 @@ of the one 2e9-interval trace and the shards are combined with one all-reduce
 (E) and one all-gather (summary blocks) over NCCL.  Other configs default to
 weak scaling (every rank owns a C-sized block of an N-times larger trace).
 
-``value`` is whole-job intervals/s with the SoA (start, end, kind + CSR
-resource offsets, 17 B per interval) already resident in HBM, generated there
-by the engine's generator; ``e2e`` is the same metric through the C ABI from
-pinned HOST buffers (``heteff_analyze_host_csr``), H2D copies and the result
-D2H inside the timed region.
+``value`` is whole-job intervals/s with the SoA already resident in HBM,
+generated there by the engine's generator: ``--layout columns`` (default;
+start u64, end u64, res i32, kind u8: 21 B per interval) or ``--layout csr``
+(resource ids as CSR offsets: 17 B per interval -- fewer bytes, but at C5 the
+analysis kernel is bound by per-tile work and the column layout is the faster
+one); ``e2e`` is the same metric through the C ABI from
+pinned HOST buffers, H2D copies and the result D2H inside the timed region, on
+the CSR layout by default (``heteff_analyze_host_csr``: PCIe-bound, so the 17 B
+layout).
 
 ``--impl reference`` times the reference's CPU path on the host cores on the
 SAME config dict: the C oracle port of the reference algorithm
@@ -161,6 +165,18 @@ def _rank_block(cfg, world: int, rank: int) -> tuple[int, int]:
     return cfg.n_ranks * rank // world, cfg.n_ranks * (rank + 1) // world
 
 
+def _value_csr(args) -> bool:
+    """The device-resident layout `value` is measured on: resource ids as CSR offsets
+    (17 B / interval) or as a res column (21 B; the default: at C5 the kernel is bound by
+    per-tile work, not bytes, and the column layout is the faster of the two)."""
+    return args.layout == "csr" and not args.shuffle
+
+
+def _e2e_csr(args) -> bool:
+    """The host-buffer layout of `e2e` (PCIe-bound: the 17 B CSR layout by default)."""
+    return args.e2e_layout == "csr" and not args.shuffle
+
+
 def _flush_l2(cfg, world: int, bpi: int) -> bool:
     """Inputs of one GPU that fit in L2 are flushed between timed steps."""
     return cfg.intervals // world * bpi < 2 * L2_BYTES
@@ -168,7 +184,7 @@ def _flush_l2(cfg, world: int, bpi: int) -> bool:
 
 def _config_dict(args, cfg, world: int) -> dict:
     scaling = _scaling(args)
-    bpi = BYTES_COLUMNS if (args.res_columns or args.shuffle) else BYTES_CSR
+    bpi = BYTES_CSR if _value_csr(args) else BYTES_COLUMNS
     d = {"workload": args.config, "trace": cfg.name, "intervals": cfg.intervals, "ranks": cfg.n_ranks,
          "devices": cfg.n_devices, "parallelism": f"dp{world} (rank-sharded, {scaling} scaling)",
          "input": ("start u64 + end u64 + kind u8 + CSR offsets per rank / device (17 B/interval)" if bpi == BYTES_CSR
@@ -288,10 +304,10 @@ def run_engine(args, world, rank, local):
     cfg = _global_config(args, world)
     blocks = [_rank_block(cfg, world, r) for r in range(world)]
     r0, r1 = blocks[rank]
-    dt = generate(cfg, r0, r1, device=local)
-    csr = not (args.res_columns or args.shuffle)
-    if not csr:
-        dt = dt.columns_only()
+    dt_gen = generate(cfg, r0, r1, device=local)   # res columns + CSR offsets
+    csr = _value_csr(args)
+    e2e_csr = _e2e_csr(args)
+    dt = dt_gen if csr else dt_gen.columns_only()
     bpi = BYTES_CSR if csr else BYTES_COLUMNS
     intervals_local = dt.host_count + dt.dev_count
     intervals_total = cfg.intervals
@@ -400,10 +416,10 @@ def run_engine(args, world, rank, local):
     def pinned(x):
         return None if x is None else torch.empty(x.shape, dtype=x.dtype, pin_memory=True).copy_(x)
 
-    host_cols = [pinned(x) for x in (dt.h_start, dt.h_end)] + [None if csr else pinned(dt.h_res), pinned(dt.h_kind)] \
-        + [pinned(x) for x in (dt.d_start, dt.d_end)] + [None if csr else pinned(dt.d_res), pinned(dt.d_kind)]
+    host_cols = [pinned(x) for x in (dt.h_start, dt.h_end)] + [None if e2e_csr else pinned(dt.h_res), pinned(dt.h_kind)] \
+        + [pinned(x) for x in (dt.d_start, dt.d_end)] + [None if e2e_csr else pinned(dt.d_res), pinned(dt.d_kind)]
     host_dt = DeviceTrace(*host_cols, dt.n, dt.m)
-    seg = (dt.h_seg.cpu().numpy(), dt.d_seg.cpu().numpy()) if csr else None
+    seg = (dt_gen.h_seg.cpu().numpy(), dt_gen.d_seg.cpu().numpy()) if e2e_csr else None
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     f = analyze_host_columns(host_dt, stream=stream.cuda_stream, device=local, sort_if_needed=args.shuffle, csr=seg)
     if not kernel_ms:   # region / multi-GPU steps: the one-launch analysis kernel's time on this shard
@@ -446,8 +462,8 @@ def run_engine(args, world, rank, local):
         "config": _config_dict(args, cfg, world),
         "e2e": {"value": intervals_total / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-                "input": "pinned host SoA, resource ids as CSR offsets (heteff_analyze_host_csr)" if csr
-                else "pinned host SoA with res columns (heteff_analyze_host)"},
+                "input": "pinned host SoA, resource ids as CSR offsets (heteff_analyze_host_csr, 17 B/interval)"
+                if e2e_csr else "pinned host SoA with res columns (heteff_analyze_host, 21 B/interval)"},
         "gpu_launches": args.steps * launches_per_step,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_source": peak_kind,
@@ -532,7 +548,10 @@ def main():
     ap.add_argument("--ref-pkg-intervals", type=float, default=1e7,
                     help="reference arm: rank shard for the reference package itself (0: skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--res-columns", action="store_true", help="resource ids as a res column (21 B) instead of CSR")
+    ap.add_argument("--layout", choices=["columns", "csr"], default="columns",
+                    help="device-resident input of `value`: res column (21 B/interval) or CSR offsets (17 B)")
+    ap.add_argument("--e2e-layout", choices=["csr", "columns"], default="csr",
+                    help="host-buffer input of `e2e` (PCIe-bound): CSR offsets (17 B/interval) or res columns (21 B)")
     ap.add_argument("--regions", type=int, default=None, help="monitoring regions per step (default: 16 for c4)")
     ap.add_argument("--shuffle", action="store_true", help="device records in random order (step includes K3)")
     args = ap.parse_args()

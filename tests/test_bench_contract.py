@@ -72,7 +72,7 @@ def test_config_dicts_of_both_arms_are_identical():
 
 def _parse(b, argv):
     import argparse
-    ns = argparse.Namespace(config="c5", scaling=None, res_columns=False, shuffle=False, regions=None)
+    ns = argparse.Namespace(config="c5", scaling=None, layout="columns", e2e_layout="csr", shuffle=False, regions=None)
     i = 0
     while i < len(argv):
         setattr(ns, argv[i][2:], argv[i + 1])
