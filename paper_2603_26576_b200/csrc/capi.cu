@@ -5,12 +5,14 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <thread>
 #include <vector>
 #include <cstdlib>
 #include <string>
 
 #include "../../include/heteff_b200.h"
 #include "engine.cuh"
+#include "transfer.cuh"
 
 namespace hb {
 cudaError_t launch_generate(const heteff_gen_side &g, u64 *S, u64 *E, int32_t *R, uint8_t *K, cudaStream_t s);
@@ -59,6 +61,8 @@ struct heteff_ctx {
     size_t in_pin_bytes = 0;
     // CSR inputs on the paths that need res columns (error path, K3 sort, regions)
     DevBuf csr_res;
+    // large host-buffer calls: block-compressed column transfer (transfer.cu)
+    hb::TransferCtx xfer;
 };
 
 static int fail(heteff_ctx *ctx, int code, const std::string &msg)
@@ -148,6 +152,7 @@ void heteff_destroy(heteff_ctx *ctx)
     if (ctx->in_pin) cudaFreeHost(ctx->in_pin);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    hb::transfer_free(ctx->xfer);
     delete ctx;
 }
 
@@ -807,6 +812,12 @@ static int analyze_host_impl(heteff_ctx *ctx, const heteff_trace *trace, const i
         ctx->in_pin_bytes = total;
     }
     uint8_t *hpin = gather ? static_cast<uint8_t *>(ctx->in_pin) : nullptr;
+    // large calls: start / end / kind cross PCIe block-compressed (transfer.cu), encoded by
+    // host threads while earlier chunks copy and decode; HETEFF_RAW_TRANSFER=1 copies raw
+    const int64_t codec_min = getenv("HETEFF_CODEC_MIN") ? atoll(getenv("HETEFF_CODEC_MIN")) : ((int64_t)1 << 22);
+    const bool codec = !gather && !(getenv("HETEFF_RAW_TRANSFER") && atoi(getenv("HETEFF_RAW_TRANSFER")))
+                       && hn + dn >= codec_min && (hn == 0 || (trace->host.start && trace->host.end && trace->host.kind))
+                       && (dn == 0 || (trace->dev.start && trace->dev.end && trace->dev.kind));
     heteff_trace d = *trace;
     size_t o = 0;
     auto put = [&](const void *src, size_t bytes, size_t room) -> void * {
@@ -818,14 +829,29 @@ static int analyze_host_impl(heteff_ctx *ctx, const heteff_trace *trace, const i
         o += room;
         return dst;
     };
-    d.host.start = static_cast<const uint64_t *>(put(trace->host.start, (size_t)hn * 8, hb8));
-    d.host.end = static_cast<const uint64_t *>(put(trace->host.end, (size_t)hn * 8, hb8));
+    auto col = [&](const void *src, size_t bytes, size_t room) -> void * {   // the codec fills it
+        return codec ? put(nullptr, bytes, room) : put(src, bytes, room);
+    };
+    d.host.start = static_cast<const uint64_t *>(col(trace->host.start, (size_t)hn * 8, hb8));
+    d.host.end = static_cast<const uint64_t *>(col(trace->host.end, (size_t)hn * 8, hb8));
     d.host.res = static_cast<const int32_t *>(put(hseg ? nullptr : trace->host.res, (size_t)hn * 4, hseg ? 0 : hb4));
-    d.host.kind = static_cast<const uint8_t *>(put(trace->host.kind, (size_t)hn, hb1));
-    d.dev.start = static_cast<const uint64_t *>(put(trace->dev.start, (size_t)dn * 8, db8));
-    d.dev.end = static_cast<const uint64_t *>(put(trace->dev.end, (size_t)dn * 8, db8));
+    d.host.kind = static_cast<const uint8_t *>(col(trace->host.kind, (size_t)hn, hb1));
+    d.dev.start = static_cast<const uint64_t *>(col(trace->dev.start, (size_t)dn * 8, db8));
+    d.dev.end = static_cast<const uint64_t *>(col(trace->dev.end, (size_t)dn * 8, db8));
     d.dev.res = static_cast<const int32_t *>(put(dseg ? nullptr : trace->dev.res, (size_t)dn * 4, dseg ? 0 : db4));
-    d.dev.kind = static_cast<const uint8_t *>(put(trace->dev.kind, (size_t)dn, db1));
+    d.dev.kind = static_cast<const uint8_t *>(col(trace->dev.kind, (size_t)dn, db1));
+    if (codec) {
+        hb::TransferSide sides[2] = {
+            {trace->host.start, trace->host.end, trace->host.kind, hn, (uint64_t *)d.host.start, (uint64_t *)d.host.end,
+             (uint8_t *)d.host.kind},
+            {trace->dev.start, trace->dev.end, trace->dev.kind, dn, (uint64_t *)d.dev.start, (uint64_t *)d.dev.end,
+             (uint8_t *)d.dev.kind}};
+        int nt = getenv("HETEFF_CODEC_THREADS") ? atoi(getenv("HETEFF_CODEC_THREADS"))
+                                                 : (int)std::thread::hardware_concurrency() - 1;
+        nt = nt < 1 ? 1 : (nt > 63 ? 63 : nt);
+        std::string why;
+        if (hb::transfer_columns(ctx->xfer, sides, 2, nt, s, why) != 0) return fail(ctx, HETEFF_CUDA_ERROR, "transfer: " + why);
+    }
     d.host_decl = trace->host_decl
                       ? static_cast<const int32_t *>(put(trace->host_decl, (size_t)trace->host_ids * 4, hd))
                       : nullptr;
