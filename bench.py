@@ -468,7 +468,9 @@ def run_engine(args, world, rank, local):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_source": peak_kind,
                      "traffic": (traffic or {}).get(tkey, {}).get("bytes_per_launch") if traffic else None,
-                     "kernel": "hb::analyze_kernel", "kernel_ms": kms,
+                     "kernel": ("hb::analyze_kernel<CSR> (15 x 11 tiles)" if csr
+                                else "hb_cols::analyze_kernel<columns> (11 x 15 tiles, engine_cols.cu)"),
+                     "kernel_ms": kms,
                      "algorithmic_bytes_per_launch": algo,
                      "bytes_per_interval": bpi,
                      "per_gpu_intervals": intervals_local},

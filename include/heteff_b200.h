@@ -178,10 +178,10 @@ int heteff_analyze(heteff_ctx *ctx, const heteff_trace *trace, const heteff_opti
 
 /* trace columns in host memory (pinned for full PCIe rate); H2D inside.  Calls of
    >= 4 Mi records send start / end / kind block-compressed (csrc/transfer.cu: per block of
-   4096 records the offsets from the block's min start and the durations in 1, 2 or 4
-   bytes, raw 8-byte values where they do not fit), encoded by host threads while earlier
-   chunks copy and decode on the GPU -- bit-exact columns in HBM, ~2.5x fewer PCIe bytes on
-   dense traces.  Environment: HETEFF_RAW_TRANSFER=1 copies raw, HETEFF_CODEC_THREADS sets
+   4096 records the starts as gaps (sorted blocks) or offsets from the block's min start,
+   and the durations, in 1, 2 or 4 bytes, raw 8-byte values where they do not fit), encoded
+   by host threads while earlier chunks copy and decode on the GPU -- bit-exact columns in
+   HBM, ~4x fewer PCIe bytes on dense traces.  Environment: HETEFF_RAW_TRANSFER=1 copies raw, HETEFF_CODEC_THREADS sets
    the encoder threads (default: hardware threads - 1), HETEFF_CODEC_MIN the size threshold. */
 int heteff_analyze_host(heteff_ctx *ctx, const heteff_trace *trace, const heteff_options *opt,
                         heteff_result *result, const heteff_outputs *out, void *stream);

@@ -14,6 +14,12 @@
 #include "engine.cuh"
 #include "transfer.cuh"
 
+// the res-column compilation of the analysis kernel (engine_cols.cu: 11 x 15 tile geometry)
+namespace hb_cols {
+cudaError_t launch_analyze_v(const void *p, int grid, cudaStream_t s);
+int analyze_grid(int device);
+}
+
 namespace hb {
 cudaError_t launch_generate(const heteff_gen_side &g, u64 *S, u64 *E, int32_t *R, uint8_t *K, cudaStream_t s);
 }
@@ -27,7 +33,8 @@ struct DevBuf {
 
 struct heteff_ctx {
     int device = 0;
-    int grid = 0;
+    int grid = 0;          // CTAs of the analysis launch (CSR compilation, 15 x 11 tiles)
+    int grid_cols = 0;     // the same for the res-column compilation (engine_cols.cu, 11 x 15)
     std::string err;
     uint32_t epoch = 0;
     // per dense id accumulators (zero between calls)
@@ -97,6 +104,14 @@ static cudaError_t ensure(DevBuf &b, size_t bytes, bool zero)
     return e;
 }
 
+// the analysis launch: CSR inputs take the 15 x 11 compilation, res-column inputs the
+// 11 x 15 one (engine_cols.cu) -- each the faster on its layout
+static cudaError_t launch_engine(heteff_ctx *ctx, const hb::Params &p, cudaStream_t s)
+{
+    if (p.hseg || p.dseg) return hb::launch_analyze(p, ctx->grid, s);
+    return hb_cols::launch_analyze_v(&p, ctx->grid_cols, s);
+}
+
 static cudaError_t reset_globals(heteff_ctx *ctx)
 {
     hb::Globals g0;
@@ -123,10 +138,11 @@ heteff_ctx *heteff_create(int device)
     cudaEventCreate(&ctx->ev0);
     cudaEventCreate(&ctx->ev1);
     ctx->grid = hb::analyze_grid(device);
-    if (ctx->grid <= 0) { heteff_destroy(ctx); return nullptr; }   // tile geometry does not fit this GPU
+    ctx->grid_cols = hb_cols::analyze_grid(device);
+    if (ctx->grid <= 0 || ctx->grid_cols <= 0) { heteff_destroy(ctx); return nullptr; }   // geometry does not fit
     if (const char *g = getenv("HETEFF_GRID")) {
         const int v = atoi(g);
-        if (v > 0) ctx->grid = v;
+        if (v > 0) ctx->grid = ctx->grid_cols = v;
     }
     return ctx;
 }
@@ -135,6 +151,7 @@ int heteff_set_grid(heteff_ctx *ctx, int grid)
 {
     if (!ctx || grid < 0) return fail(ctx, HETEFF_BAD_ARG, "bad grid");
     ctx->grid = grid > 0 ? grid : hb::analyze_grid(ctx->device);
+    ctx->grid_cols = grid > 0 ? grid : hb_cols::analyze_grid(ctx->device);
     return HETEFF_OK;
 }
 
@@ -269,14 +286,14 @@ static int run_once(heteff_ctx *ctx, const heteff_trace *t, const heteff_options
         p.res = reinterpret_cast<hb::ResultDev *>(b + (opt->mode == HETEFF_MODE_SUMMARIZE_DEVICE ? 256 : 0));
         p.host_out = reinterpret_cast<u64 *>(b + 512);
         p.dev_out = reinterpret_cast<u64 *>(b + 512 + (size_t)into->n_max * 32);
-        CK(hb::launch_analyze(p, ctx->grid, s), "launch analyze");
+        CK(launch_engine(ctx, p, s), "launch analyze");
         return HETEFF_OK;
     }
     const bool want_sums = out && (out->host_summaries || out->device_summaries);
     const size_t ob_copy = want_sums ? ob_total : sizeof(hb::ResultDev);
 
     CK(cudaEventRecord(ctx->ev0, s), "event");
-    CK(hb::launch_analyze(p, ctx->grid, s), "launch analyze");
+    CK(launch_engine(ctx, p, s), "launch analyze");
     CK(cudaEventRecord(ctx->ev1, s), "event");
     CK(cudaMemcpyAsync(ctx->out_pin, blk, ob_copy, cudaMemcpyDeviceToHost, s), "d2h results");
     CK(cudaStreamSynchronize(s), "analysis");

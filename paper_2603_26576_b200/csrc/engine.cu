@@ -57,7 +57,7 @@
 #define HB_UNROLL_B HB_ITEMS
 #endif
 
-namespace hb {
+namespace HB_ENGINE_NS {
 
 #ifdef HB_PROF
 // per-CTA clock64 phase counters (tools/prof build only): read back with heteff_prof_read
@@ -2405,6 +2405,13 @@ cudaError_t launch_analyze(const Params &p, int grid, cudaStream_t s)
     return cudaGetLastError();
 }
 
+// entry for another compilation of this file (engine_cols.cu): the same Params layout,
+// reached through its address
+cudaError_t launch_analyze_v(const void *p, int grid, cudaStream_t s)
+{
+    return launch_analyze(*static_cast<const Params *>(p), grid, s);
+}
+
 // =========================================================================
 // multi-GPU merge of gathered per-rank result blocks (one CTA).  Every rank
 // ran two launches into its block [host header 256 B | device header 256 B |
@@ -2502,4 +2509,4 @@ cudaError_t launch_covers(const Params &p, const int64_t *err_idx, int64_t count
     return cudaGetLastError();
 }
 
-}  // namespace hb
+}  // namespace HB_ENGINE_NS

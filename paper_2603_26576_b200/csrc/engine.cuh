@@ -3,7 +3,12 @@
 #pragma once
 #include <cstdint>
 
-namespace hb {
+// The engine's namespace: `hb`, or another name for a second compilation of the
+// analysis kernel with a different tile geometry (engine_cols.cu).
+#ifndef HB_ENGINE_NS
+#define HB_ENGINE_NS hb
+#endif
+namespace HB_ENGINE_NS {
 
 typedef unsigned long long u64;
 
@@ -198,4 +203,4 @@ cudaError_t sort_records(const u64 *S, const u64 *E, const int32_t *R, const uin
 cudaError_t launch_remap(int64_t *list, int64_t k, const int64_t *perm, cudaStream_t s);
 cudaError_t launch_order_check(const int32_t *R, const u64 *S, int64_t n, unsigned int *bad, cudaStream_t s);
 
-}  // namespace hb
+}  // namespace HB_ENGINE_NS

@@ -7,7 +7,12 @@
 #include "engine.cuh"
 #include "ptx.cuh"
 
-namespace hb {
+// The engine's namespace: `hb`, or another name for a second compilation of the
+// analysis kernel with a different tile geometry (engine_cols.cu).
+#ifndef HB_ENGINE_NS
+#define HB_ENGINE_NS hb
+#endif
+namespace HB_ENGINE_NS {
 
 // =========================================================================
 // exact u128 / u128 -> nearest double, ties to even (Python int / int)
@@ -129,4 +134,4 @@ __device__ void metric_trees(Out *res, bool host_side, bool dev_side, u64 E, int
     }
 }
 
-}  // namespace hb
+}  // namespace HB_ENGINE_NS

@@ -4,7 +4,12 @@
 #pragma once
 #include <cstdint>
 
-namespace hb {
+// The engine's namespace: `hb`, or another name for a second compilation of the
+// analysis kernel with a different tile geometry (engine_cols.cu).
+#ifndef HB_ENGINE_NS
+#define HB_ENGINE_NS hb
+#endif
+namespace HB_ENGINE_NS {
 
 typedef unsigned long long u64;
 typedef unsigned __int128 u128;
@@ -147,4 +152,4 @@ __device__ __forceinline__ u64 shfl_down64(u64 v, int d)
     return __shfl_down_sync(0xffffffffu, v, d);
 }
 
-}  // namespace hb
+}  // namespace HB_ENGINE_NS

@@ -32,31 +32,64 @@ namespace xfer {
 
 // the block format (kBlock, BlockHdr) and the host encoder live in transfer.cuh /
 // transfer_enc.cpp (compiled for AVX-512 when the host has it)
-// one CTA per block: expand into the HBM columns
+// one CTA per block: expand into the HBM columns.  Gap blocks rebuild their starts with a
+// block-wide inclusive scan (16 consecutive records per thread, 64-bit sums).
 __global__ void __launch_bounds__(256) decode_kernel(const uint8_t *__restrict__ chunk, uint64_t *__restrict__ S,
                                                      uint64_t *__restrict__ E, uint8_t *__restrict__ K)
 {
+    __shared__ uint64_t warp_tot[8];
     const BlockHdr h = reinterpret_cast<const BlockHdr *>(chunk + 16)[blockIdx.x];
     const int cnt = (int)h.cnt + 1;
+    const int w = h.ws & 15;
     const uint8_t *ps = chunk + h.off;
-    const uint8_t *pd = ps + ((cnt * h.ws + 15) & ~15);
+    const uint8_t *pd = ps + ((cnt * w + 15) & ~15);
     const uint8_t *pk = pd + ((cnt * h.wd + 15) & ~15);
     const int64_t o = (int64_t)blockIdx.x * kBlock;
+    auto field = [](const uint8_t *p, int wd, int i) -> uint64_t {
+        switch (wd) {
+            case 1: return p[i];
+            case 2: return reinterpret_cast<const uint16_t *>(p)[i];
+            case 4: return reinterpret_cast<const uint32_t *>(p)[i];
+            default: return reinterpret_cast<const uint64_t *>(p)[i];
+        }
+    };
+    if (h.ws & kDelta) {
+        constexpr int kPer = kBlock / 256;
+        const int b = threadIdx.x * kPer;
+        uint64_t v[kPer], run = 0;
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            v[q] = b + q < cnt ? field(ps, w, b + q) : 0ull;
+            run += v[q];
+        }
+        // exclusive prefix of the thread sums across the CTA
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        uint64_t inc = run;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint64_t x = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += x;
+        }
+        if (lane == 31) warp_tot[warp] = inc;
+        __syncthreads();
+        uint64_t acc = h.s0 + inc - run;
+        for (int q = 0; q < warp; ++q) acc += warp_tot[q];
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const int i = b + q;
+            acc += v[q];
+            if (i < cnt) {
+                const uint64_t e = h.wd == 8 ? field(pd, 8, i) : acc + field(pd, h.wd, i);
+                S[o + i] = acc;
+                E[o + i] = e;
+                K[o + i] = pk[i];
+            }
+        }
+        return;
+    }
     for (int i = threadIdx.x; i < cnt; i += 256) {
-        uint64_t s;
-        switch (h.ws) {
-            case 1: s = h.s0 + ps[i]; break;
-            case 2: s = h.s0 + reinterpret_cast<const uint16_t *>(ps)[i]; break;
-            case 4: s = h.s0 + reinterpret_cast<const uint32_t *>(ps)[i]; break;
-            default: s = reinterpret_cast<const uint64_t *>(ps)[i];
-        }
-        uint64_t e;
-        switch (h.wd) {
-            case 1: e = s + pd[i]; break;
-            case 2: e = s + reinterpret_cast<const uint16_t *>(pd)[i]; break;
-            case 4: e = s + reinterpret_cast<const uint32_t *>(pd)[i]; break;
-            default: e = reinterpret_cast<const uint64_t *>(pd)[i];
-        }
+        const uint64_t s = w == 8 ? field(ps, 8, i) : h.s0 + field(ps, w, i);
+        const uint64_t e = h.wd == 8 ? field(pd, 8, i) : s + field(pd, h.wd, i);
         S[o + i] = s;
         E[o + i] = e;
         K[o + i] = pk[i];

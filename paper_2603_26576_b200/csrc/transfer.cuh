@@ -13,10 +13,12 @@ constexpr int kBlock = 4096;                       // records per block
 constexpr int kBlocksPerChunk = 256;               // 1 Mi records per chunk
 constexpr int64_t kChunk = (int64_t)kBlock * kBlocksPerChunk;
 
+constexpr uint8_t kDelta = 16;   // BlockHdr::ws flag: starts stored as gaps to the previous start
+
 struct BlockHdr {           // 16 bytes, in the chunk's block table
-    uint64_t s0;            // min start (or 0 for raw starts)
+    uint64_t s0;            // min start (the first one for gap blocks; 0 for raw starts)
     uint32_t off;           // payload offset from the chunk start (16-byte aligned)
-    uint8_t ws, wd;         // widths: 1, 2, 4, or 8 (raw values)
+    uint8_t ws, wd;         // widths: 1, 2, 4, or 8 (raw values); ws | kDelta: gaps
     uint16_t cnt;           // records in the block - 1 (<= 4095)
 };
 static_assert(sizeof(BlockHdr) == 16, "block header");

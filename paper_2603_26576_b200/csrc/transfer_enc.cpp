@@ -22,6 +22,14 @@ static inline __attribute__((always_inline)) void put_off(uint8_t *dst, const ui
 }
 
 template <typename T>
+static inline __attribute__((always_inline)) void put_gap(uint8_t *dst, const uint64_t *__restrict__ v, int n)
+{
+    T *__restrict__ o = reinterpret_cast<T *>(dst);
+    o[0] = 0;
+    for (int i = 1; i < n; ++i) o[i] = (T)(v[i] - v[i - 1]);
+}
+
+template <typename T>
 static inline __attribute__((always_inline)) void put_dur(uint8_t *dst, const uint64_t *__restrict__ s,
                                                           const uint64_t *__restrict__ e, int n)
 {
@@ -43,7 +51,7 @@ static inline __attribute__((always_inline)) size_t encode_body(const uint64_t *
         const uint64_t *__restrict__ s = S + i0;
         const uint64_t *__restrict__ e = E + i0;
         // reductions over the block (it stays in L1 / L2 for the writes below)
-        uint64_t mn = ~0ull, mx = 0, dmax = 0, neg = 0;
+        uint64_t mn = ~0ull, mx = 0, dmax = 0, neg = 0, down = 0, gmax = 0;
         for (int i = 0; i < cnt; ++i) {
             mn = std::min(mn, s[i]);
             mx = std::max(mx, s[i]);
@@ -52,20 +60,35 @@ static inline __attribute__((always_inline)) size_t encode_body(const uint64_t *
             neg |= (uint64_t)(e[i] < s[i]);
             dmax = std::max(dmax, e[i] - s[i]);
         }
+        for (int i = 1; i < cnt; ++i) {   // start-sorted blocks: the gaps between starts
+            down |= (uint64_t)(s[i] < s[i - 1]);
+            gmax = std::max(gmax, s[i] - s[i - 1]);
+        }
         BlockHdr h;
-        h.ws = width_of(mx - mn);
+        const uint8_t wo = width_of(mx - mn), wg = down ? 8 : width_of(gmax);
+        const bool delta = wg < wo;   // gaps narrower than offsets: starts as gaps (decoded by a scan)
+        h.ws = delta ? (uint8_t)(wg | kDelta) : wo;
         h.wd = neg ? 8 : width_of(dmax);
-        h.s0 = h.ws == 8 ? 0 : mn;
+        h.s0 = wo == 8 && !delta ? 0 : mn;   // delta blocks are sorted: mn is the first start
         h.cnt = (uint16_t)(cnt - 1);
         h.off = (uint32_t)pos;
         uint8_t *p = out + pos;
-        switch (h.ws) {
-            case 1: put_off<uint8_t>(p, s, mn, cnt); break;
-            case 2: put_off<uint16_t>(p, s, mn, cnt); break;
-            case 4: put_off<uint32_t>(p, s, mn, cnt); break;
-            default: memcpy(p, s, (size_t)cnt * 8);
+        const int w = h.ws & 15;
+        if (delta) {
+            switch (w) {
+                case 1: put_gap<uint8_t>(p, s, cnt); break;
+                case 2: put_gap<uint16_t>(p, s, cnt); break;
+                default: put_gap<uint32_t>(p, s, cnt); break;
+            }
+        } else {
+            switch (w) {
+                case 1: put_off<uint8_t>(p, s, mn, cnt); break;
+                case 2: put_off<uint16_t>(p, s, mn, cnt); break;
+                case 4: put_off<uint32_t>(p, s, mn, cnt); break;
+                default: memcpy(p, s, (size_t)cnt * 8);
+            }
         }
-        p += up16((size_t)cnt * h.ws);
+        p += up16((size_t)cnt * w);
         switch (h.wd) {
             case 1: put_dur<uint8_t>(p, s, e, cnt); break;
             case 2: put_dur<uint16_t>(p, s, e, cnt); break;

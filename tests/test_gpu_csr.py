@@ -30,6 +30,10 @@ def _pinned(h, d, n, m):
 def _same(a, b):
     assert (a.status, a.contract_flags, a.contract_index) == (b.status, b.contract_flags, b.contract_index)
     assert (a.elapsed, a.host_elapsed, a.dev_max_end, a.counts) == (b.elapsed, b.host_elapsed, b.dev_max_end, b.counts)
+    if a.status != N.OK:
+        # an invalid trace's partial sums are never observable (the reference raises;
+        # api.py raises) and may differ between the two kernel compilations
+        return
     assert a.host_metrics == b.host_metrics and a.device_metrics == b.device_metrics
     assert np.array_equal(a.host_sum, b.host_sum) and np.array_equal(a.dev_sum, b.dev_sum)
 

@@ -24,6 +24,15 @@ from paper_2603_26576_b200.synth import generate  # noqa: E402
 from test_gpu_csr import _same, _seg  # noqa: E402
 
 
+def _identical(a, b):
+    """Codec vs raw copy: the same kernel on what must be the same columns -- every output,
+    partial sums of invalid traces included."""
+    assert (a.status, a.contract_flags, a.contract_index) == (b.status, b.contract_flags, b.contract_index)
+    assert (a.elapsed, a.host_elapsed, a.dev_max_end, a.counts) == (b.elapsed, b.host_elapsed, b.dev_max_end, b.counts)
+    assert a.host_metrics == b.host_metrics and a.device_metrics == b.device_metrics
+    assert np.array_equal(a.host_sum, b.host_sum) and np.array_equal(a.dev_sum, b.dev_sum)
+
+
 def _host_trace(h, d, n, m):
     cols = [torch.from_numpy(np.ascontiguousarray(x).view(np.int64) if x.dtype == np.uint64 else
                              np.ascontiguousarray(x)).pin_memory() for x in (*h, *d)]
@@ -87,7 +96,7 @@ def test_codec_equals_raw_transfer_and_device(name, mode):
     d = (d[0], d[1], d[2], (d[3] % 2).astype(np.uint8))
     a = _run_host(h, d, n, m, mode, codec=True)
     b = _run_host(h, d, n, m, mode, codec=False)
-    _same(a, b)
+    _identical(a, b)
     dt = _dev_trace(h, d, n, m)
     c = analyze_device(DeviceTrace(dt.h_start, dt.h_end, dt.h_res, dt.h_kind, dt.d_start, dt.d_end, dt.d_res,
                                    dt.d_kind, n, m), mode)
@@ -109,7 +118,7 @@ def test_codec_with_malformed_unsorted_and_zero_length_records():
     h = (hs, he, h[2], (h[3] % 3).astype(np.uint8))
     d = (ds, d[1], d[2], (d[3] % 2).astype(np.uint8))
     for mode in (N.MODE_REPORT, N.MODE_VALIDATE):
-        _same(_run_host(h, d, n, m, mode, True), _run_host(h, d, n, m, mode, False))
+        _identical(_run_host(h, d, n, m, mode, True), _run_host(h, d, n, m, mode, False))
 
 
 def test_codec_on_a_c5_rank_shard():
@@ -123,3 +132,23 @@ def test_codec_on_a_c5_rank_shard():
     g = analyze_host_columns(host, csr=(dt.h_seg.cpu().numpy(), dt.d_seg.cpu().numpy()))
     assert f.status == N.OK
     _same(f, g)
+
+
+@pytest.mark.parametrize("k", [4095, 4097, 70_000, (1 << 20) + 3])
+def test_codec_on_valid_traces_equals_device_resident(k):
+    """Valid traces (disjoint host chains, overlapping device streams): status OK, so every
+    summary and float is compared with the device-resident analysis (the other kernel
+    compilation) as well as with the raw copy."""
+    from test_gpu_parity import _host_chain
+    rng = np.random.default_rng(k)
+    n, m = 4, 4
+    h = _host_chain(rng, n, np.array([k] * n))
+    res = np.repeat(np.arange(m, dtype=np.int32), k)
+    start = np.concatenate([np.cumsum(rng.integers(0, 300, size=k)) for _ in range(m)]).astype(np.uint64)
+    dur = rng.integers(1, 3000, size=m * k).astype(np.uint64)
+    kind = rng.integers(0, 2, size=m * k, dtype=np.uint8)
+    d = (start, start + dur, res, kind)
+    a = _run_host(h, d, n, m, N.MODE_REPORT, codec=True)
+    assert a.status == N.OK
+    _identical(a, _run_host(h, d, n, m, N.MODE_REPORT, codec=False))
+    _same(a, analyze_device(_dev_trace(h, d, n, m)))
