@@ -17,7 +17,9 @@
 // the res-column compilation of the analysis kernel (engine_cols.cu: 11 x 15 tile geometry)
 namespace hb_cols {
 cudaError_t launch_analyze_v(const void *p, int grid, cudaStream_t s);
+cudaError_t launch_overlap_pass_v(const void *p, unsigned long long *scratch, cudaStream_t s);
 int analyze_grid(int device);
+int tile_records();
 }
 
 namespace hb {
@@ -112,6 +114,19 @@ static cudaError_t launch_engine(heteff_ctx *ctx, const hb::Params &p, cudaStrea
     return hb_cols::launch_analyze_v(&p, ctx->grid_cols, s);
 }
 
+// the error-path overlap pass of the same compilation (its tiles)
+static cudaError_t launch_overlap(const hb::Params &p, bool csr, u64 *scratch, cudaStream_t s)
+{
+    if (csr) return hb::launch_overlap_pass(p, scratch, s);
+    return hb_cols::launch_overlap_pass_v(&p, scratch, s);
+}
+
+// records per tile of the compilation that analyses a trace (tile counts, look-back slots)
+static int64_t tile_of(const heteff_trace *t)
+{
+    return (t->host_seg || t->dev_seg) ? (int64_t)hb::kTile : (int64_t)hb_cols::tile_records();
+}
+
 static cudaError_t reset_globals(heteff_ctx *ctx)
 {
     hb::Globals g0;
@@ -192,8 +207,9 @@ static int run_once(heteff_ctx *ctx, const heteff_trace *t, const heteff_options
         return fail(ctx, HETEFF_BAD_ARG, "negative size");
     if (opt->mode < 0 || opt->mode > 3) return fail(ctx, HETEFF_BAD_ARG, "bad mode");
     CK(cudaSetDevice(ctx->device), "cudaSetDevice");
-    const int64_t ht = (t->host.count + hb::kTile - 1) / hb::kTile;
-    const int64_t dt = (t->dev.count + hb::kTile - 1) / hb::kTile;
+    const int64_t tile = tile_of(t);
+    const int64_t ht = (t->host.count + tile - 1) / tile;
+    const int64_t dt = (t->dev.count + tile - 1) / tile;
     const int64_t hid = t->host_ids > 0 ? t->host_ids : 1, did = t->dev_ids > 0 ? t->dev_ids : 1;
 
     // workspace (grow on demand; accumulators and tile flags start zeroed)
@@ -299,6 +315,7 @@ static int run_once(heteff_ctx *ctx, const heteff_trace *t, const heteff_options
     CK(cudaStreamSynchronize(s), "analysis");
     if (reinterpret_cast<const hb::ResultDev *>(ctx->out_pin)->status == -1) {
         // some host records overlap: exact overlap findings, then the finalize
+        const bool csr = p.hseg || p.dseg;   // which compilation analysed the call
         if (p.hseg) {   // the error-path kernels walk a res column: expand the offsets once
             CK(ensure(ctx->csr_res, (size_t)t->host.count * 4 + 256, false), "alloc res column");
             CK(hb::launch_expand_res(p.hseg, t->host_ids, t->host.count, static_cast<int32_t *>(ctx->csr_res.p), s),
@@ -306,7 +323,7 @@ static int run_once(heteff_ctx *ctx, const heteff_trace *t, const heteff_options
             p.hr = static_cast<const int32_t *>(ctx->csr_res.p);
         }
         CK(ensure(ctx->aux, (size_t)(ht + 1) * 3 * sizeof(u64), false), "alloc overlap scratch");
-        CK(hb::launch_overlap_pass(p, static_cast<u64 *>(ctx->aux.p), s), "launch overlap pass");
+        CK(launch_overlap(p, csr, static_cast<u64 *>(ctx->aux.p), s), "launch overlap pass");
         CK(cudaMemcpyAsync(ctx->out_pin, blk, ob_copy, cudaMemcpyDeviceToHost, s), "d2h results");
         CK(cudaStreamSynchronize(s), "overlap pass");
     }

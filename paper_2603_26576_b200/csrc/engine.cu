@@ -2405,12 +2405,19 @@ cudaError_t launch_analyze(const Params &p, int grid, cudaStream_t s)
     return cudaGetLastError();
 }
 
-// entry for another compilation of this file (engine_cols.cu): the same Params layout,
-// reached through its address
+// entries for another compilation of this file (engine_cols.cu): the same Params layout,
+// reached through its address; its tile size sets the tile counts of a call
 cudaError_t launch_analyze_v(const void *p, int grid, cudaStream_t s)
 {
     return launch_analyze(*static_cast<const Params *>(p), grid, s);
 }
+
+cudaError_t launch_overlap_pass_v(const void *p, u64 *scratch, cudaStream_t s)
+{
+    return launch_overlap_pass(*static_cast<const Params *>(p), scratch, s);
+}
+
+int tile_records() { return kTile; }
 
 // =========================================================================
 // multi-GPU merge of gathered per-rank result blocks (one CTA).  Every rank
