@@ -1,7 +1,8 @@
 """Randomized engine-vs-oracle stress run (test infrastructure): random trace shapes --
 counts around tile boundaries, time ranges crossing 2^32 or near U64_MAX, overlapping
 streams, zero-length / malformed records, empty resources -- through the engine's
-columnar path in REPORT / VALIDATE / SUMMARIZE_DEVICE mode against the C oracle.
+columnar path in REPORT / VALIDATE / SUMMARIZE_DEVICE mode against the C oracle -- both
+compilations of the analysis kernel (res columns, and CSR offsets when the ids allow).
 Usage: python tools/stress.py SECONDS [SEED]"""
 import sys
 import time
@@ -86,6 +87,27 @@ def one(rng):
             assert got.elapsed == ref.elapsed, (mode, got.elapsed, ref.elapsed)
             assert np.array_equal(got.host_sum, ref.host_sum) and np.array_equal(got.dev_sum, ref.dev_sum), mode
             assert got.host_metrics == ref.host_metrics and got.device_metrics == ref.device_metrics, mode
+    # the CSR compilation of the analysis kernel on the same columns (res ids as offsets),
+    # when every id is a declared dense id (offsets cannot express the others)
+    if (h[2].size == 0 or int(h[2].max()) < n) and (d[2].size == 0 or int(d[2].max()) < m):
+        import torch
+
+        from paper_2603_26576_b200.engine import DeviceTrace, analyze_device
+
+        def cu(x):
+            x = np.ascontiguousarray(x)
+            return torch.from_numpy(x.view(np.int64) if x.dtype == np.uint64 else x).cuda()
+        dt = DeviceTrace(*(cu(x) for x in (*h, *d)), n, m).with_csr()
+        for mode, el in modes:
+            got = analyze_device(dt, mode, el)
+            ref = O.analyze(h, d, n, m, mode=mode, elapsed=el, cap=1 << 18)
+            assert got.status == ref.status, ("csr", mode, got.status, ref.status)
+            lists = (0, 1, 2, 4, 5, 6, 7) if mode != N.MODE_SUMMARIZE_DEVICE else (0, 1, 2, 4, 5, 6)
+            assert [got.counts[c] for c in lists + (3,)] == [ref.counts[c] for c in lists + (3,)], ("csr", mode)
+            if ref.status == 0 and mode != N.MODE_VALIDATE:
+                assert got.elapsed == ref.elapsed, ("csr", mode)
+                assert np.array_equal(got.host_sum, ref.host_sum) and np.array_equal(got.dev_sum, ref.dev_sum)
+                assert got.host_metrics == ref.host_metrics and got.device_metrics == ref.device_metrics
     return h[0].size + d[0].size
 
 
