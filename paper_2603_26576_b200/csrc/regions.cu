@@ -678,11 +678,17 @@ __global__ void __launch_bounds__(kDT) rd_sums(const __grid_constant__ RegParams
         // (every lane together): the thread's first start is <= every piece start x of
         // the first device, and stage_overlap moves the cursor forward from there
         int sq = (S.count > 0 && nv > 0 && cur == S.dev) ? stage_locate(S, T.s[b]) : 0;
+        // contiguous pieces (a piece starting where the previous one ended: every record
+        // under overlapping streams) merge into one range before the staged walk -- the
+        // thread's sum of |offload ∩ piece| is |offload ∩ union|
+        u64 px = 0, py = 0;
+        bool pend = false;
         for (int q = 0; q < nv; ++q) {
             const int i = b + q;
             const int32_t pr = i > 0 ? T.r[i - 1] : prev_r;
             const int32_t r = T.r[i];
             if (r != pr) {
+                if (pend) { sa.v[2] += stage_overlap(S, sq, px, py); pend = false; }
                 sa = ident<3, 0>();
                 sa.f = true;
                 runK = runKM = 0;
@@ -696,7 +702,14 @@ __global__ void __launch_bounds__(kDT) rd_sums(const __grid_constant__ RegParams
             if (T.k[i] == 0) sa.v[0] += umax(runK, e) - umax(runK, s);
             if (x < y && owner >= 0 && owner < p.host_ids) {
                 if (S.count >= 0 && cur == S.dev) {
-                    sa.v[2] += stage_overlap(S, sq, x, y);
+                    if (pend && x == py) {
+                        py = y;
+                    } else {
+                        if (pend) sa.v[2] += stage_overlap(S, sq, px, py);
+                        px = x;
+                        py = y;
+                        pend = true;
+                    }
                 } else {
                     if (!wk.init) {
                         wk.h0 = p.hseg[owner];
@@ -710,6 +723,7 @@ __global__ void __launch_bounds__(kDT) rd_sums(const __grid_constant__ RegParams
             runKM = umax(runKM, e);
             if (T.k[i] == 0) runK = umax(runK, e);
         }
+        if (pend) sa.v[2] += stage_overlap(S, sq, px, py);
         SAgg<3, 0> tot3;
         const SAgg<3, 0> ex3 = block_seg_scan<3, 0>(sa, ws3, tot3);
         if (tid % kSub == 0) {   // in-tile prefix at this thread's first record: f, U_K, U_KM, busy, f, max K, max KM
