@@ -462,7 +462,8 @@ def run_engine(args, world, rank, local):
         "config": _config_dict(args, cfg, world),
         "e2e": {"value": intervals_total / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-                "input": "pinned host SoA, resource ids as CSR offsets (heteff_analyze_host_csr, 17 B/interval)"
+                "input": ("pinned host SoA, resource ids as CSR offsets (heteff_analyze_host_csr, 17 B/interval "
+                          "in host memory; the library moves them block-compressed, ~4 B/interval over PCIe)")
                 if e2e_csr else "pinned host SoA with res columns (heteff_analyze_host, 21 B/interval)"},
         "gpu_launches": args.steps * launches_per_step,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

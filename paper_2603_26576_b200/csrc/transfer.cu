@@ -213,6 +213,9 @@ int transfer_columns(TransferCtx &tc, const TransferSide *sides, int nsides, int
     }
     cv_free.notify_all();
     for (auto &t : pool) t.join();
+    // on failure nothing after this call waits for the copies already issued: drain them
+    // before the pinned slots can be reused (on success the caller's analysis syncs the stream)
+    if (rc != 0) cudaStreamSynchronize(s);
     cudaGetLastError();
     return rc;
 }
