@@ -142,7 +142,7 @@ typedef struct {
     int64_t contract_index;     /* first offending record (min over violations) */
     uint64_t host_elapsed;      /* max end over all host records (model.py:217) */
     uint64_t elapsed;           /* E (summarize.py:88-91) or the explicit window */
-    uint64_t dev_max_end;       /* max end over all device records */
+    uint64_t dev_max_end;       /* device-only traces (n == 0): max end over all device records (= E); else 0 */
     int32_t host_present;       /* n >= 1 */
     int32_t device_present;     /* m >= 1 */
     double host_metrics[5];     /* PE, MPI PE, MPI CE, MPI LB, device offload eff. */
@@ -171,6 +171,11 @@ const char *heteff_last_error(const heteff_ctx *ctx);
    progress without co-residency; a grid larger than one wave only runs slower.
    The environment variable HETEFF_GRID sets the same at heteff_create. */
 int heteff_set_grid(heteff_ctx *ctx, int grid);
+
+/* The tile geometry of the analysis kernel compilation the context's last analysis launch
+   used ("15x11" for CSR inputs; "11x15" or "8x19" for res columns, by device run length --
+   DESIGN.md section 5), or "" before the first one. */
+const char *heteff_kernel_name(const heteff_ctx *ctx);
 
 /* trace columns in device memory */
 int heteff_analyze(heteff_ctx *ctx, const heteff_trace *trace, const heteff_options *opt,

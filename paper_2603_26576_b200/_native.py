@@ -116,7 +116,7 @@ EXPORTED = (
     "heteff_flatten", "heteff_subtract", "heteff_intersect", "heteff_total_duration",
     "heteff_parse_trace", "heteff_parsed_info", "heteff_parsed_free",
     "heteff_import_events", "heteff_imported_info", "heteff_imported_free",
-    "heteff_analyze_into", "heteff_merge_shards", "heteff_set_grid",
+    "heteff_analyze_into", "heteff_merge_shards", "heteff_set_grid", "heteff_kernel_name",
 )
 
 _lib = None
@@ -185,6 +185,9 @@ def load() -> C.CDLL:
     lib.heteff_merge_shards.restype = C.c_int
     lib.heteff_merge_shards.argtypes = [_p, _p, C.c_int32, C.c_size_t, C.c_int32, C.c_int32, _p, _p, _p,
                                         C.POINTER(Result), C.POINTER(Outputs), _p]
+    if hasattr(lib, "heteff_kernel_name"):
+        lib.heteff_kernel_name.restype = C.c_char_p
+        lib.heteff_kernel_name.argtypes = [_p]
     if hasattr(lib, "heteff_set_grid"):   # (older builds loaded through HETEFF_LIB for A/B runs)
         lib.heteff_set_grid.restype = C.c_int
         lib.heteff_set_grid.argtypes = [_p, C.c_int]

@@ -14,13 +14,32 @@
 #include "engine.cuh"
 #include "transfer.cuh"
 
-// the res-column compilation of the analysis kernel (engine_cols.cu: 11 x 15 tile geometry)
-namespace hb_cols {
-cudaError_t launch_analyze_v(const void *p, int grid, cudaStream_t s);
-cudaError_t launch_overlap_pass_v(const void *p, unsigned long long *scratch, cudaStream_t s);
-int analyze_grid(int device);
-int tile_records();
-}
+// The analysis kernel is compiled once per tile geometry (engine.cu in namespaces hb,
+// hb_cols -- engine_cols.cu -- and hb_long -- engine_long.cu); each exports the same entries.
+#define HB_COMPILATION_ENTRIES                                                                   \
+    cudaError_t launch_analyze_v(const void *p, int grid, cudaStream_t s);                       \
+    cudaError_t launch_overlap_pass_v(const void *p, unsigned long long *scratch, cudaStream_t s); \
+    int analyze_grid(int device);                                                               \
+    int tile_records();
+namespace hb { HB_COMPILATION_ENTRIES }
+namespace hb_cols { HB_COMPILATION_ENTRIES }
+namespace hb_long { HB_COMPILATION_ENTRIES }
+
+struct Compilation {
+    const char *name;
+    cudaError_t (*launch)(const void *p, int grid, cudaStream_t s);
+    cudaError_t (*overlap)(const void *p, unsigned long long *scratch, cudaStream_t s);
+    int (*grid)(int device);
+    int (*tile)();
+};
+// measured per input: CSR offsets -> 15 x 11; res columns -> 11 x 15,
+// or 8 x 19 when devices hold long record runs
+static const Compilation kCompilations[3] = {
+    {"15x11", hb::launch_analyze_v, hb::launch_overlap_pass_v, hb::analyze_grid, hb::tile_records},
+    {"11x15", hb_cols::launch_analyze_v, hb_cols::launch_overlap_pass_v, hb_cols::analyze_grid, hb_cols::tile_records},
+    {"8x19", hb_long::launch_analyze_v, hb_long::launch_overlap_pass_v, hb_long::analyze_grid, hb_long::tile_records},
+};
+constexpr int64_t kLongRun = 200000;   // records per device (res-column inputs) for the 8 x 19 compilation
 
 namespace hb {
 cudaError_t launch_generate(const heteff_gen_side &g, u64 *S, u64 *E, int32_t *R, uint8_t *K, cudaStream_t s);
@@ -35,8 +54,8 @@ struct DevBuf {
 
 struct heteff_ctx {
     int device = 0;
-    int grid = 0;          // CTAs of the analysis launch (CSR compilation, 15 x 11 tiles)
-    int grid_cols = 0;     // the same for the res-column compilation (engine_cols.cu, 11 x 15)
+    int grid[3] = {0, 0, 0};   // CTAs of the analysis launch, per kernel compilation
+    const char *kernel = "";   // the compilation of the last analysis launch
     std::string err;
     uint32_t epoch = 0;
     // per dense id accumulators (zero between calls)
@@ -106,27 +125,19 @@ static cudaError_t ensure(DevBuf &b, size_t bytes, bool zero)
     return e;
 }
 
-// the analysis launch: CSR inputs take the 15 x 11 compilation, res-column inputs the
-// 11 x 15 one (engine_cols.cu) -- each the faster on its layout
-static cudaError_t launch_engine(heteff_ctx *ctx, const hb::Params &p, cudaStream_t s)
+// which compilation analyses a trace: CSR inputs the 15 x 11 one; res-column inputs by the
+// average device record run (the host side when there are no devices)
+static int pick_compilation(const heteff_trace *t)
 {
-    if (p.hseg || p.dseg) return hb::launch_analyze(p, ctx->grid, s);
-    return hb_cols::launch_analyze_v(&p, ctx->grid_cols, s);
+    if (t->host_seg || t->dev_seg) return 0;
+    const int64_t run = t->dev_ids > 0 ? t->dev.count / t->dev_ids
+                                       : (t->host_ids > 0 ? t->host.count / t->host_ids : 0);
+    if (const char *e = getenv("HETEFF_COMPILATION")) {   // tuning / test override of the choice below
+        const int c = atoi(e);
+        if (c == 1 || c == 2) return c;
+    }
+    return run >= kLongRun ? 2 : 1;
 }
-
-// the error-path overlap pass of the same compilation (its tiles)
-static cudaError_t launch_overlap(const hb::Params &p, bool csr, u64 *scratch, cudaStream_t s)
-{
-    if (csr) return hb::launch_overlap_pass(p, scratch, s);
-    return hb_cols::launch_overlap_pass_v(&p, scratch, s);
-}
-
-// records per tile of the compilation that analyses a trace (tile counts, look-back slots)
-static int64_t tile_of(const heteff_trace *t)
-{
-    return (t->host_seg || t->dev_seg) ? (int64_t)hb::kTile : (int64_t)hb_cols::tile_records();
-}
-
 static cudaError_t reset_globals(heteff_ctx *ctx)
 {
     hb::Globals g0;
@@ -152,21 +163,23 @@ heteff_ctx *heteff_create(int device)
     if (reset_globals(ctx) != cudaSuccess) { delete ctx; return nullptr; }
     cudaEventCreate(&ctx->ev0);
     cudaEventCreate(&ctx->ev1);
-    ctx->grid = hb::analyze_grid(device);
-    ctx->grid_cols = hb_cols::analyze_grid(device);
-    if (ctx->grid <= 0 || ctx->grid_cols <= 0) { heteff_destroy(ctx); return nullptr; }   // geometry does not fit
+    for (int c = 0; c < 3; ++c) {
+        ctx->grid[c] = kCompilations[c].grid(device);
+        if (ctx->grid[c] <= 0) { heteff_destroy(ctx); return nullptr; }   // a tile geometry does not fit this GPU
+    }
     if (const char *g = getenv("HETEFF_GRID")) {
         const int v = atoi(g);
-        if (v > 0) ctx->grid = ctx->grid_cols = v;
+        if (v > 0) ctx->grid[0] = ctx->grid[1] = ctx->grid[2] = v;
     }
     return ctx;
 }
 
+const char *heteff_kernel_name(const heteff_ctx *ctx) { return ctx ? ctx->kernel : ""; }
+
 int heteff_set_grid(heteff_ctx *ctx, int grid)
 {
     if (!ctx || grid < 0) return fail(ctx, HETEFF_BAD_ARG, "bad grid");
-    ctx->grid = grid > 0 ? grid : hb::analyze_grid(ctx->device);
-    ctx->grid_cols = grid > 0 ? grid : hb_cols::analyze_grid(ctx->device);
+    for (int c = 0; c < 3; ++c) ctx->grid[c] = grid > 0 ? grid : kCompilations[c].grid(ctx->device);
     return HETEFF_OK;
 }
 
@@ -207,7 +220,10 @@ static int run_once(heteff_ctx *ctx, const heteff_trace *t, const heteff_options
         return fail(ctx, HETEFF_BAD_ARG, "negative size");
     if (opt->mode < 0 || opt->mode > 3) return fail(ctx, HETEFF_BAD_ARG, "bad mode");
     CK(cudaSetDevice(ctx->device), "cudaSetDevice");
-    const int64_t tile = tile_of(t);
+    const int comp = pick_compilation(t);
+    const Compilation &K = kCompilations[comp];
+    ctx->kernel = K.name;
+    const int64_t tile = K.tile();
     const int64_t ht = (t->host.count + tile - 1) / tile;
     const int64_t dt = (t->dev.count + tile - 1) / tile;
     const int64_t hid = t->host_ids > 0 ? t->host_ids : 1, did = t->dev_ids > 0 ? t->dev_ids : 1;
@@ -302,20 +318,19 @@ static int run_once(heteff_ctx *ctx, const heteff_trace *t, const heteff_options
         p.res = reinterpret_cast<hb::ResultDev *>(b + (opt->mode == HETEFF_MODE_SUMMARIZE_DEVICE ? 256 : 0));
         p.host_out = reinterpret_cast<u64 *>(b + 512);
         p.dev_out = reinterpret_cast<u64 *>(b + 512 + (size_t)into->n_max * 32);
-        CK(launch_engine(ctx, p, s), "launch analyze");
+        CK(K.launch(&p, ctx->grid[comp], s), "launch analyze");
         return HETEFF_OK;
     }
     const bool want_sums = out && (out->host_summaries || out->device_summaries);
     const size_t ob_copy = want_sums ? ob_total : sizeof(hb::ResultDev);
 
     CK(cudaEventRecord(ctx->ev0, s), "event");
-    CK(launch_engine(ctx, p, s), "launch analyze");
+    CK(K.launch(&p, ctx->grid[comp], s), "launch analyze");
     CK(cudaEventRecord(ctx->ev1, s), "event");
     CK(cudaMemcpyAsync(ctx->out_pin, blk, ob_copy, cudaMemcpyDeviceToHost, s), "d2h results");
     CK(cudaStreamSynchronize(s), "analysis");
     if (reinterpret_cast<const hb::ResultDev *>(ctx->out_pin)->status == -1) {
         // some host records overlap: exact overlap findings, then the finalize
-        const bool csr = p.hseg || p.dseg;   // which compilation analysed the call
         if (p.hseg) {   // the error-path kernels walk a res column: expand the offsets once
             CK(ensure(ctx->csr_res, (size_t)t->host.count * 4 + 256, false), "alloc res column");
             CK(hb::launch_expand_res(p.hseg, t->host_ids, t->host.count, static_cast<int32_t *>(ctx->csr_res.p), s),
@@ -323,7 +338,7 @@ static int run_once(heteff_ctx *ctx, const heteff_trace *t, const heteff_options
             p.hr = static_cast<const int32_t *>(ctx->csr_res.p);
         }
         CK(ensure(ctx->aux, (size_t)(ht + 1) * 3 * sizeof(u64), false), "alloc overlap scratch");
-        CK(launch_overlap(p, csr, static_cast<u64 *>(ctx->aux.p), s), "launch overlap pass");
+        CK(K.overlap(&p, static_cast<u64 *>(ctx->aux.p), s), "launch overlap pass");   // same compilation
         CK(cudaMemcpyAsync(ctx->out_pin, blk, ob_copy, cudaMemcpyDeviceToHost, s), "d2h results");
         CK(cudaStreamSynchronize(s), "overlap pass");
     }

@@ -1903,7 +1903,9 @@ __device__ void finalize(const Params &p, u128 *scratch, int tid)
         res->contract_index = cf ? (int64_t)(*(volatile long long *)&g->contract_index) : -1;
         res->host_elapsed = host_elapsed;
         res->elapsed = E;
-        res->dev_max_end = dev_max_end;
+        // the device-only E (summarize.py:91); with ranks declared the per-device maxima are
+        // kept clamped at E by the union passes, so there is no trace-wide value to report
+        res->dev_max_end = p.n >= 1 ? 0ull : dev_max_end;
         res->host_present = p.n >= 1;
         res->device_present = p.m >= 1;
         res->host_mask = 0;

@@ -141,3 +141,32 @@ def test_full_scale_properties(name):
     assert abs(pe - mpe * oe) <= 1e-12 * pe and abs(mpe - ce * lb) <= 1e-12 * mpe
     dpe, dlb, dce, doe = f.device_metrics
     assert abs(dpe - dlb * dce * doe) <= 1e-12 * dpe
+
+
+@pytest.mark.parametrize("name,ranks", [("c3", 3), ("c5", 6), ("c2", 20)])
+def test_every_kernel_compilation_matches_the_oracle(name, ranks):
+    """The analysis kernel is compiled per tile geometry (15 x 11 for CSR inputs; 11 x 15 or
+    8 x 19 for res columns, chosen by device run length -- capi.cu pick_compilation): every
+    compilation, forced through HETEFF_COMPILATION, bit-exact against the oracle."""
+    import os
+    from oracle import oracle as O
+    cfg = CONFIGS[name]
+    dt = generate(cfg, 0, ranks)
+    h = (_u64(dt.h_start), _u64(dt.h_end), _host(dt.h_res), _host(dt.h_kind))
+    d = (_u64(dt.d_start), _u64(dt.d_end), _host(dt.d_res), _host(dt.d_kind))
+    ref = O.analyze(h, d, dt.n, dt.m)
+    runs = [analyze_device(dt)]                     # CSR offsets: the 15 x 11 compilation
+    old = os.environ.get("HETEFF_COMPILATION")
+    try:
+        for c in ("1", "2"):
+            os.environ["HETEFF_COMPILATION"] = c
+            runs.append(analyze_device(dt.columns_only()))
+    finally:
+        if old is None:
+            os.environ.pop("HETEFF_COMPILATION", None)
+        else:
+            os.environ["HETEFF_COMPILATION"] = old
+    for f in runs:
+        assert f.status == N.OK and f.elapsed == ref.elapsed
+        assert np.array_equal(f.host_sum, ref.host_sum) and np.array_equal(f.dev_sum, ref.dev_sum)
+        assert f.host_metrics == ref.host_metrics and f.device_metrics == ref.device_metrics

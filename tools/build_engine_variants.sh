@@ -12,7 +12,7 @@ for spec in "$@"; do
   cp csrc/* "$d"/p/csrc/; cp ../include/* "$d"/include/; cp "$src" "$d"/p/csrc/engine.cu
   c="$d"/p/csrc
   (nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -diag-suppress 550 $flags \
-    $c/engine.cu $c/engine_cols.cu $c/gen.cu $c/sort.cu $c/regions.cu $c/intervals.cu $c/transfer.cu $c/transfer_enc.cpp $c/capi.cu $c/ingest.cpp \
+    $c/engine.cu $c/engine_cols.cu $c/engine_long.cu $c/gen.cu $c/sort.cu $c/regions.cu $c/intervals.cu $c/transfer.cu $c/transfer_enc.cpp $c/capi.cu $c/ingest.cpp \
     -o variants/libheteff_b200_$tag.so && rm -rf "$d") &
 done
 wait
