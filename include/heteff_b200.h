@@ -187,7 +187,8 @@ int heteff_analyze(heteff_ctx *ctx, const heteff_trace *trace, const heteff_opti
    and the durations, in 1, 2 or 4 bytes, raw 8-byte values where they do not fit), encoded
    by host threads while earlier chunks copy and decode on the GPU -- bit-exact columns in
    HBM, ~4x fewer PCIe bytes on dense traces.  Environment: HETEFF_RAW_TRANSFER=1 copies raw, HETEFF_CODEC_THREADS sets
-   the encoder threads (default: hardware threads - 1), HETEFF_CODEC_MIN the size threshold. */
+   the encoder threads (default: hardware threads / LOCAL_WORLD_SIZE - 1), HETEFF_CODEC_MIN
+   the size threshold. */
 int heteff_analyze_host(heteff_ctx *ctx, const heteff_trace *trace, const heteff_options *opt,
                         heteff_result *result, const heteff_outputs *out, void *stream);
 

@@ -895,8 +895,12 @@ static int analyze_host_impl(heteff_ctx *ctx, const heteff_trace *trace, const i
              (uint8_t *)d.host.kind},
             {trace->dev.start, trace->dev.end, trace->dev.kind, dn, (uint64_t *)d.dev.start, (uint64_t *)d.dev.end,
              (uint8_t *)d.dev.kind}};
+        // default: the host's hardware threads, shared by the ranks of this node when launched
+        // one process per GPU (torchrun sets LOCAL_WORLD_SIZE), one left for the dispatcher
+        int share = getenv("LOCAL_WORLD_SIZE") ? atoi(getenv("LOCAL_WORLD_SIZE")) : 1;
+        share = share < 1 ? 1 : share;
         int nt = getenv("HETEFF_CODEC_THREADS") ? atoi(getenv("HETEFF_CODEC_THREADS"))
-                                                 : (int)std::thread::hardware_concurrency() - 1;
+                                                 : (int)std::thread::hardware_concurrency() / share - 1;
         nt = nt < 1 ? 1 : (nt > 63 ? 63 : nt);
         std::string why;
         if (hb::transfer_columns(ctx->xfer, sides, 2, nt, s, why) != 0) return fail(ctx, HETEFF_CUDA_ERROR, "transfer: " + why);
