@@ -210,6 +210,7 @@ __device__ __forceinline__ uint32_t block_excl_scan_bins(uint32_t x, uint32_t *w
 // Warp-private shared counters (atomics conflict only inside a warp); a
 // 256-thread CTA per tile keeps more tiles' loads in flight per SM.
 constexpr int kUT = 256, kUW = kUT / 32, kUI = kTileKeys / kUT;
+static_assert(kTileKeys % kUT == 0, "the upsweep covers a tile in whole 256-thread strides (HB_SORT_T x HB_SORT_I)");
 __global__ void __launch_bounds__(kUT) upsweep(const u64 *__restrict__ kin, int64_t n, int shift, int dbits,
                                                uint32_t *__restrict__ counts, int64_t tiles)
 {
