@@ -411,8 +411,11 @@ def run_engine(args, world, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = intervals_total / (ms / 1e3)
-    # the analysis kernel compilation the timed steps ran (before the e2e calls below)
+    # the analysis kernel compilation the timed steps ran (before the e2e calls below); a
+    # split analysis is three launches (host pass, device pass, merge)
     kernel_name = (N.load().heteff_kernel_name(N.context(local)) or b"?").decode()
+    if kernel_name.startswith("split") and merge is None and windows is None and not args.shuffle:
+        launches_per_step = 3
 
     # e2e: the same call from pinned host buffers (H2D + result D2H inside the timed region)
     def pinned(x):
@@ -471,7 +474,7 @@ def run_engine(args, world, rank, local):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_source": peak_kind,
                      "traffic": (traffic or {}).get(tkey, {}).get("bytes_per_launch") if traffic else None,
-                     "kernel": "analyze_kernel, %s tiles (compute warps x records per thread)" % kernel_name,
+                     "kernel": "analyze_kernel, %s (tiles: compute warps x records per thread)" % kernel_name,
                      "kernel_ms": kms,
                      "algorithmic_bytes_per_launch": algo,
                      "bytes_per_interval": bpi,

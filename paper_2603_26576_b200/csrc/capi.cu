@@ -55,7 +55,7 @@ struct DevBuf {
 struct heteff_ctx {
     int device = 0;
     int grid[3] = {0, 0, 0};   // CTAs of the analysis launch, per kernel compilation
-    const char *kernel = "";   // the compilation of the last analysis launch
+    std::string kernel;        // the compilation(s) of the last analysis
     std::string err;
     uint32_t epoch = 0;
     // per dense id accumulators (zero between calls)
@@ -73,6 +73,7 @@ struct heteff_ctx {
     // staging for heteff_analyze_host / metrics; scratch of the overlap error path
     DevBuf stage, aux;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev_split0 = nullptr, ev_split1 = nullptr;   // run_split's span (the merge uses ev0 / ev1)
     // K3 sort: workspace, sorted columns + permutations
     DevBuf sort_ws, sorted;
     // K5/K6 regions: accumulators, carries, outputs
@@ -91,6 +92,10 @@ struct heteff_ctx {
     DevBuf csr_res;
     // large host-buffer calls: block-compressed column transfer (transfer.cu)
     hb::TransferCtx xfer;
+    // split analysis (run_split): the shared result block + E, and its pinned mirror
+    DevBuf split;
+    void *split_pin = nullptr;
+    size_t split_pin_bytes = 0;
 };
 
 static int fail(heteff_ctx *ctx, int code, const std::string &msg)
@@ -163,6 +168,8 @@ heteff_ctx *heteff_create(int device)
     if (reset_globals(ctx) != cudaSuccess) { delete ctx; return nullptr; }
     cudaEventCreate(&ctx->ev0);
     cudaEventCreate(&ctx->ev1);
+    cudaEventCreate(&ctx->ev_split0);
+    cudaEventCreate(&ctx->ev_split1);
     for (int c = 0; c < 3; ++c) {
         ctx->grid[c] = kCompilations[c].grid(device);
         if (ctx->grid[c] <= 0) { heteff_destroy(ctx); return nullptr; }   // a tile geometry does not fit this GPU
@@ -174,7 +181,7 @@ heteff_ctx *heteff_create(int device)
     return ctx;
 }
 
-const char *heteff_kernel_name(const heteff_ctx *ctx) { return ctx ? ctx->kernel : ""; }
+const char *heteff_kernel_name(const heteff_ctx *ctx) { return ctx ? ctx->kernel.c_str() : ""; }
 
 int heteff_set_grid(heteff_ctx *ctx, int grid)
 {
@@ -187,7 +194,7 @@ void heteff_destroy(heteff_ctx *ctx)
 {
     if (!ctx) return;
     DevBuf *bufs[] = {&ctx->host_acc, &ctx->dev_acc, &ctx->host_tiles, &ctx->dev_tiles, &ctx->host_out,
-                      &ctx->dev_out, &ctx->lists, &ctx->stage, &ctx->aux, &ctx->sort_ws, &ctx->sorted, &ctx->reg_ws, &ctx->reg_out, &ctx->iv_ws, &ctx->out_blk, &ctx->csr_res};
+                      &ctx->dev_out, &ctx->lists, &ctx->stage, &ctx->aux, &ctx->sort_ws, &ctx->sorted, &ctx->reg_ws, &ctx->reg_out, &ctx->iv_ws, &ctx->out_blk, &ctx->csr_res, &ctx->split};
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->g) cudaFree(ctx->g);
@@ -195,8 +202,11 @@ void heteff_destroy(heteff_ctx *ctx)
     if (ctx->res_h) cudaFreeHost(ctx->res_h);
     if (ctx->out_pin) cudaFreeHost(ctx->out_pin);
     if (ctx->in_pin) cudaFreeHost(ctx->in_pin);
+    if (ctx->split_pin) cudaFreeHost(ctx->split_pin);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->ev_split0) cudaEventDestroy(ctx->ev_split0);
+    if (ctx->ev_split1) cudaEventDestroy(ctx->ev_split1);
     hb::transfer_free(ctx->xfer);
     delete ctx;
 }
@@ -435,9 +445,98 @@ static int materialize_res(heteff_ctx *ctx, const heteff_trace *t, heteff_trace 
     return HETEFF_OK;
 }
 
+// Split analysis: the host records and the device records as two launches, each with the
+// tile geometry best for its own record runs, E handed over in device memory, then the merge
+// kernel -- the multi-GPU protocol at world size 1 (include/heteff_b200.h "multi-GPU").
+// Taken for large REPORT calls without finding lists whose two sides prefer different
+// compilations (C5: host runs of 2.4e5 -> 8 x 19, device runs of 6.1e4 -> 11 x 15): C5
+// 7.05 -> 6.75 ms (tools/split_probe.py); identical results, the counts of the findings
+// included (the late-record count is the clamp count: E is the host elapsed).  Returns
+// HETEFF_PARSE_FALLBACK when the single launch must decide (a shard is not OK).
+static bool split_wanted(const heteff_trace *t, const heteff_options *opt)
+{
+    if (opt->mode != HETEFF_MODE_REPORT || opt->flags != 0 || opt->list_capacity != 0) return false;
+    if (t->n < 1 || t->m < 1 || getenv("HETEFF_NO_SPLIT")) return false;
+    const int64_t min = getenv("HETEFF_SPLIT_MIN") ? atoll(getenv("HETEFF_SPLIT_MIN")) : ((int64_t)1 << 26);
+    if (t->host.count < min || t->dev.count < min || 4 * t->host.count < t->host.count + t->dev.count) return false;
+    heteff_trace h = *t, d = *t;
+    h.dev.count = 0; h.dev_ids = 0; h.dev_seg = nullptr;
+    d.host.count = 0; d.host_ids = 0; d.host_seg = nullptr;
+    return pick_compilation(&h) != pick_compilation(&d);
+}
+
+static int run_split(heteff_ctx *ctx, const heteff_trace *t, heteff_result *result, const heteff_outputs *out,
+                     cudaStream_t s)
+{
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const int32_t n = t->n, m = t->m;
+    const size_t bytes = 512 + 32 * ((size_t)n + (size_t)m);
+    CK(ensure(ctx->split, bytes + 256, true), "alloc split block");
+    uint8_t *blk = static_cast<uint8_t *>(ctx->split.p);
+    u64 *e_dev = reinterpret_cast<u64 *>(blk + ((bytes + 127) & ~(size_t)127));
+    heteff_trace th = *t, td = *t;   // host records only / device records only
+    th.dev.count = 0; th.dev.start = th.dev.end = nullptr; th.dev.res = nullptr; th.dev.kind = nullptr;
+    th.dev_ids = 0; th.m = 0; th.dev_decl = nullptr; th.dev_seg = nullptr;
+    td.host.count = 0; td.host.start = td.host.end = nullptr; td.host.res = nullptr; td.host.kind = nullptr;
+    td.host_ids = 0; td.n = 0; td.host_decl = nullptr; td.host_seg = nullptr; td.host_elapsed_floor = 0;
+    heteff_options oh{}, od{};
+    oh.mode = HETEFF_MODE_SUMMARIZE_HOST;
+    od.mode = HETEFF_MODE_SUMMARIZE_DEVICE;
+    od.flags = HETEFF_FLAG_ELAPSED_DEVICE_PTR;
+    od.elapsed = (uint64_t)(uintptr_t)e_dev;
+    IntoBlock into{blk, n, m};
+    heteff_result r{};
+    CK(cudaEventRecord(ctx->ev_split0, s), "event");
+    int rc = run_once(ctx, &th, &oh, &r, nullptr, s, nullptr, &into);
+    if (rc != HETEFF_OK) return rc;
+    CK(cudaMemcpyAsync(e_dev, blk + 16, 8, cudaMemcpyDeviceToDevice, s), "E");   // the host header's elapsed
+    rc = run_once(ctx, &td, &od, &r, nullptr, s, nullptr, &into);
+    if (rc != HETEFF_OK) return rc;
+    // the block (both headers' finding counts, the device rows' clamp counts) comes back with
+    // the merged result: enqueued before the merge, whose sync covers it
+    if (ctx->split_pin_bytes < bytes) {
+        if (ctx->split_pin) cudaFreeHost(ctx->split_pin);
+        ctx->split_pin = nullptr;
+        ctx->split_pin_bytes = 0;
+        CK(cudaMallocHost(&ctx->split_pin, bytes), "alloc pinned split block");
+        ctx->split_pin_bytes = bytes;
+    }
+    CK(cudaMemcpyAsync(ctx->split_pin, blk, bytes, cudaMemcpyDeviceToHost, s), "d2h split block");
+    const int32_t n_of = n, m_of = m;
+    rc = heteff_merge_shards(ctx, blk, 1, bytes, n, m, &n_of, &m_of, reinterpret_cast<const uint64_t *>(e_dev), result,
+                             out, s);
+    if (rc != HETEFF_OK || result->status != HETEFF_OK) return HETEFF_PARSE_FALLBACK;
+    CK(cudaEventRecord(ctx->ev_split1, s), "event");
+    CK(cudaEventSynchronize(ctx->ev_split1), "split");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev_split0, ctx->ev_split1);   // both launches, the hand-over, the merge
+    const uint8_t *hb_ = static_cast<const uint8_t *>(ctx->split_pin);
+    const hb::ResultDev *hdr = reinterpret_cast<const hb::ResultDev *>(hb_);   // [0] host pass, at 256 the device pass
+    const hb::ResultDev &hdev = *reinterpret_cast<const hb::ResultDev *>(hb_ + 256);
+    const u64 *rows = reinterpret_cast<const u64 *>(hb_ + 512 + 32 * (size_t)n);
+    // the late-device count is the clamp count (E = host elapsed)
+    u64 late = 0;
+    for (int32_t q = 0; q < m; ++q) late += rows[4 * (size_t)q + 3];
+    for (int i = 0; i < 8; ++i) result->counts[i] = hdr[0].counts[i] + hdev.counts[i];
+    result->counts[7] = (int64_t)late;
+    result->host_elapsed = result->elapsed;
+    result->dev_max_end = 0;
+    result->contract_flags = 0;
+    result->contract_index = -1;
+    result->kernel_ms = ms;
+    ctx->kernel = std::string("split: host ") + kCompilations[pick_compilation(&th)].name + ", device " +
+                  kCompilations[pick_compilation(&td)].name;
+    ctx->err.clear();
+    return HETEFF_OK;
+}
+
 static int run_analysis(heteff_ctx *ctx, const heteff_trace *t0, const heteff_options *opt, heteff_result *result,
                         const heteff_outputs *out, cudaStream_t s)
 {
+    if (split_wanted(t0, opt)) {
+        const int rc = run_split(ctx, t0, result, out, s);
+        if (rc != HETEFF_PARSE_FALLBACK) return rc;
+    }
     if (!(opt->flags & HETEFF_FLAG_SORT_IF_NEEDED)) return run_once(ctx, t0, opt, result, out, s);
     heteff_trace tcol;   // the order check and K3 walk res columns
     {

@@ -170,3 +170,35 @@ def test_every_kernel_compilation_matches_the_oracle(name, ranks):
         assert f.status == N.OK and f.elapsed == ref.elapsed
         assert np.array_equal(f.host_sum, ref.host_sum) and np.array_equal(f.dev_sum, ref.dev_sum)
         assert f.host_metrics == ref.host_metrics and f.device_metrics == ref.device_metrics
+
+
+def test_split_analysis_equals_the_single_launch():
+    """Large REPORT calls whose host and device sides prefer different kernel compilations
+    run as two launches + the merge kernel (capi.cu run_split); forced here on a C5 shard
+    (HETEFF_SPLIT_MIN) and compared with the single launch (HETEFF_NO_SPLIT): E, every
+    summary (clamp counts included), the finding counts and the nine floats identical."""
+    import os
+    from paper_2603_26576_b200 import _native as Nn
+    cfg = CONFIGS["c5"]
+    dt = generate(cfg, 0, 40).columns_only()
+    keys = ("HETEFF_SPLIT_MIN", "HETEFF_NO_SPLIT")
+    old = {k: os.environ.get(k) for k in keys}
+    try:
+        os.environ["HETEFF_SPLIT_MIN"] = "1"
+        os.environ.pop("HETEFF_NO_SPLIT", None)
+        a = analyze_device(dt)
+        name = Nn.load().heteff_kernel_name(Nn.context(0)).decode()
+        os.environ["HETEFF_NO_SPLIT"] = "1"
+        b = analyze_device(dt)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    assert name.startswith("split"), name
+    assert a.status == b.status == N.OK
+    assert (a.elapsed, a.host_elapsed, a.dev_max_end, a.counts) == (b.elapsed, b.host_elapsed, b.dev_max_end, b.counts)
+    assert a.counts[7] > 0                       # late device records: the clamp-count hand-over is exercised
+    assert np.array_equal(a.host_sum, b.host_sum) and np.array_equal(a.dev_sum, b.dev_sum)
+    assert a.host_metrics == b.host_metrics and a.device_metrics == b.device_metrics
