@@ -30,4 +30,15 @@ st = [(k, float(v[i])) for i, k in enumerate(h)
 out.append("stall reasons (warps per issue, top 8):")
 for k, x in sorted(st, key=lambda t: -t[1])[:8]:
     out.append(f"   {k.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', ''):24s} {x:.3f}")
+# a capture of several launches (the split analysis: host pass, device pass, merge): one row each
+if len(rows) > 3 and "Kernel Name" in h:
+    out.append("per launch:")
+    tot = 0
+    for r in rows[2:]:
+        b = sum(float(r[h.index(k)]) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum") if k in h)
+        tot += b
+        d = r[h.index("gpu__time_duration.sum")] if "gpu__time_duration.sum" in h else "?"
+        out.append(f"   {r[h.index('Kernel Name')][:70]:70s} {d:>12s} {u[h.index('gpu__time_duration.sum')] if 'gpu__time_duration.sum' in h else ''}"
+                   f"  dram {b:.4g} {u[h.index('dram__bytes_read.sum')]}")
+    out.append(f"   total dram bytes {tot:.6g} {u[h.index('dram__bytes_read.sum')]}")
 print("\n".join(out))

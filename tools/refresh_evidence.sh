@@ -19,10 +19,13 @@ HETEFF_FORCE_DIST=1 timeout 900 python -m torch.distributed.run --nnodes=1 --npr
 timeout 900 python bench.py --impl reference > gpurun_out/r/bench_reference_c5.json 2>/dev/null
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 60 --csv \
     --log-file gpurun_out/r/launches_c5.csv timeout 600 python bench.py --steps 2 --warmup 3 --e2e-steps 1 --no-cpu-baseline > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:analyze_kernel -c 1 -f -o gpurun_out/r/prof_analyze_c5 \
+# one analysis call of the default line = the split: host pass, device pass, merge (3 launches)
+ncu --set full --clock-control none --import-source on -k regex:"analyze_kernel|merge_kernel" -c 3 -f -o gpurun_out/r/prof_analyze_c5 \
     timeout 900 python tools/one_launch.py c5 col 1 > gpurun_out/r/ncu.log 2>&1
-python tools/ncu_summary.py gpurun_out/r/prof_analyze_c5.ncu-rep "ncu --set full --clock-control none, analyze_kernel, c5 columns, one launch" \
+python tools/ncu_summary.py gpurun_out/r/prof_analyze_c5.ncu-rep "ncu --set full --clock-control none, c5 columns, one analysis call (split: host pass, device pass, merge)" \
     > gpurun_out/r/ncu_summary.txt 2>&1
+ncu -i gpurun_out/r/prof_analyze_c5.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/r/src_c5.csv 2>/dev/null
+python tools/ncu_lines.py gpurun_out/r/src_c5.csv 40 > gpurun_out/r/ncu_lines_c5.txt 2>&1
 timeout 300 python tools/bench_sort.py c2 > gpurun_out/r/sort_c2.txt 2>&1
 timeout 300 python tools/bench_regions.py c4 16 3 > gpurun_out/r/regions_c4.txt 2>&1
 timeout 600 python tools/bench_api.py > gpurun_out/r/api.txt 2>&1
