@@ -350,7 +350,10 @@ def run_engine(args, world, rank, local):
     elif args.shuffle:
         from paper_2603_26576_b200.engine import sort_records
         probe = sort_records(dt.d_start, dt.d_end, dt.d_res, dt.d_kind, device=local)
-        launches_per_step += 1 + 4 + 5 * probe.passes   # failed first pass, sort, re-run
+        # failed first pass + the narrow-key sort (range_init, range, build_keys with the first
+        # pass's counts; per pass three scans + downsweep, an upsweep from the second pass on;
+        # the last pass writes the columns) + the re-run counted above
+        launches_per_step += 1 + 2 + 5 * probe.passes
         del probe
 
     plan = AnalysisPlan(dt, N.MODE_REPORT, stream=stream.cuda_stream, device=local, sort_if_needed=args.shuffle)

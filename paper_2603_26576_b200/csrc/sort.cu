@@ -11,6 +11,10 @@
 // gathered through the permutation at the end.  Otherwise the sort runs in two
 // stable stages (by s', then by r').
 //
+// The first pass's digit counts come from the key-building kernel, and the last pass of
+// a narrow sort writes the output columns itself (start, res, end and kind from the key
+// and the index), so no pass re-reads the keys only to count or to unpack them.
+//
 // Each digit pass is reduce-then-scan: an upsweep kernel counts the digits of
 // every tile (digit-major count matrix), a three-kernel scan turns the matrix
 // into the global position of every (digit, tile) run, and the downsweep
@@ -37,6 +41,12 @@ namespace rsort {
 #endif
 #ifndef HB_SORT_I
 #define HB_SORT_I 11
+#endif
+#ifndef HB_SORT_VEARLY
+#define HB_SORT_VEARLY 1
+#endif
+#ifndef HB_SORT_MINB
+#define HB_SORT_MINB (HB_SORT_T <= 512 ? 1024 / HB_SORT_T : 1)   // resident CTAs per SM (64 registers)
 #endif
 constexpr int kT = HB_SORT_T;           // threads per CTA (512: 2 CTAs / SM)
 constexpr int kW = kT / 32;
@@ -74,22 +84,61 @@ __global__ void range_init(Range *g)
     g->pad = 0;   // every byte the D2H reads is defined (compute-sanitizer initcheck)
 }
 
+// VEC: each thread takes record pairs (16-byte start / end loads, 8-byte res loads); a
+// pair's predecessor start comes from the neighbouring lane
+template <bool VEC>
 __global__ void __launch_bounds__(512) range_kernel(const u64 *__restrict__ S, const u64 *__restrict__ E,
                                                     const int32_t *__restrict__ R, int64_t n, Range *g)
 {
     u64 smin = ~0ull, smax = 0, dmax = 0;
     unsigned int rmin = 0xffffffffu, rmax = 0;
     bool desc = false, neg = false;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const u64 s = __ldg(S + i), e = __ldcs(E + i);
-        if (i > 0) desc = desc || __ldg(S + i - 1) > s;
-        const unsigned int r = flip(__ldcs(R + i));
+    auto one = [&](u64 s, u64 e, int32_t rr) {
+        const unsigned int r = flip(rr);
         smin = umin(smin, s);
         smax = umax(smax, s);
         rmin = min(rmin, r);
         rmax = max(rmax, r);
         neg = neg || e < s;
         dmax = umax(dmax, e - s);
+    };
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (VEC) {
+        const int64_t pairs = n >> 1;
+        const int lane = threadIdx.x & 31;
+        // every lane of a warp runs the same trip count (the shuffle needs them all)
+        const int64_t trips = (pairs + stride - 1) / stride;
+        for (int64_t t = 0; t < trips; ++t) {
+            const int64_t p = t0 + t * stride;
+            const bool in = p < pairs;
+            ulonglong2 s2 = make_ulonglong2(0, 0), e2 = make_ulonglong2(0, 0);
+            int2 r2 = make_int2(0, 0);
+            if (in) {
+                s2 = __ldcs(reinterpret_cast<const ulonglong2 *>(S) + p);
+                e2 = __ldcs(reinterpret_cast<const ulonglong2 *>(E) + p);
+                r2 = __ldcs(reinterpret_cast<const int2 *>(R) + p);
+            }
+            u64 prev = __shfl_up_sync(0xffffffffu, s2.y, 1);
+            if (lane == 0 && in && p > 0) prev = __ldg(S + 2 * p - 1);
+            if (in) {
+                desc = desc || (p > 0 && prev > s2.x) || s2.x > s2.y;
+                one(s2.x, e2.x, r2.x);
+                one(s2.y, e2.y, r2.y);
+            }
+        }
+        if (t0 == 0 && (n & 1)) {   // the odd last record
+            const int64_t i = n - 1;
+            const u64 si = __ldg(S + i);
+            desc = desc || (i > 0 && __ldg(S + i - 1) > si);
+            one(si, __ldg(E + i), __ldg(R + i));
+        }
+    } else {
+        for (int64_t i = t0; i < n; i += stride) {
+            const u64 si = __ldg(S + i);
+            desc = desc || (i > 0 && __ldg(S + i - 1) > si);
+            one(si, __ldcs(E + i), __ldcs(R + i));
+        }
     }
     // 64-bit warp reductions by shuffles (the kernel is bandwidth-bound)
 #pragma unroll
@@ -145,24 +194,62 @@ __device__ __forceinline__ u64 make_key(const KeyPlan &kp, u64 s, int32_t r)
 // and the finish gathers them instead
 constexpr uint32_t kIdxMask = 0x3fffffffu;
 
-__global__ void __launch_bounds__(512) build_keys(const u64 *__restrict__ S, const u64 *__restrict__ E,
+// one CTA per sort tile: the keys and indices of the tile, and the tile's digit counts of
+// the first pass (the upsweep the first pass would otherwise run over the keys again)
+constexpr int kBT = 256;
+__global__ void __launch_bounds__(kBT) build_keys(const u64 *__restrict__ S, const u64 *__restrict__ E,
                                                   const int32_t *__restrict__ R,
                                                   const uint8_t *__restrict__ KD, int64_t n, KeyPlan kp,
                                                   u64 *__restrict__ K, uint32_t *__restrict__ V,
-                                                  unsigned int *__restrict__ kind_wide)
+                                                  unsigned int *__restrict__ kind_wide,
+                                                  uint32_t *__restrict__ counts, int64_t tiles)
 {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const u64 si = __ldcs(S + i);
-        u64 key = make_key(kp, si, __ldcs(R + i));
-        if (kp.dshift) key |= (__ldcs(E + i) - si) << kp.dshift;
+    __shared__ uint32_t h[kBT / 32][kBins];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t bins = 1u << kp.dbits;
+    const u64 mask = bins - 1;
+    for (int i = tid; i < (kBT / 32) * kBins; i += kBT) (&h[0][0])[i] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kTileKeys;
+    const int64_t end = n - base < kTileKeys ? n : base + kTileKeys;
+    bool wide = false;
+    auto one = [&](int64_t i, u64 si, int32_t ri, u64 ei, uint32_t ki) {
+        u64 key = make_key(kp, si, ri);
+        if (kp.dshift) key |= (ei - si) << kp.dshift;
         K[i] = key;
+        atomicAdd(&h[warp][(uint32_t)(key & mask)], 1u);
         uint32_t v = (uint32_t)i;
         if (kp.packk) {
-            const uint32_t k = __ldcs(KD + i);
-            if (k > 3u) atomicOr(kind_wide, 1u);
-            v |= (k & 3u) << 30;
+            wide = wide || ki > 3u;
+            v |= (ki & 3u) << 30;
         }
         V[i] = v;
+    };
+    constexpr int kU = 11;   // records in flight per thread (loads issued before the keys are built)
+    int64_t i = base + tid;
+    for (; i + (kU - 1) * kBT < end; i += kU * kBT) {
+        u64 s[kU], e[kU];
+        int32_t r[kU];
+        uint32_t k[kU];
+#pragma unroll
+        for (int q = 0; q < kU; ++q) {
+            const int64_t j = i + q * kBT;
+            s[q] = __ldcs(S + j);
+            r[q] = __ldcs(R + j);
+            e[q] = kp.dshift ? __ldcs(E + j) : 0ull;
+            k[q] = kp.packk ? __ldcs(KD + j) : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < kU; ++q) one(i + q * kBT, s[q], r[q], e[q], k[q]);
+    }
+    for (; i < end; i += kBT)
+        one(i, __ldcs(S + i), __ldcs(R + i), kp.dshift ? __ldcs(E + i) : 0ull, kp.packk ? __ldcs(KD + i) : 0u);
+    if (__syncthreads_or(wide) && tid == 0) atomicOr(kind_wide, 1u);
+    for (int d = tid; d < (int)bins; d += kBT) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int w = 0; w < kBT / 32; ++w) c += h[w][d];
+        counts[(int64_t)d * tiles + blockIdx.x] = c;
     }
 }
 
@@ -324,15 +411,14 @@ __global__ void __launch_bounds__(kScanT) scan_blocks(uint32_t *c, int64_t m, co
 
 // lanes holding the same digit as this lane, from dbits ballots (faster than
 // match.any on this part, measured: the upsweep went 348 -> 61 us without it)
-__device__ __forceinline__ uint32_t peers_of(uint32_t d, int dbits, uint32_t valid_mask)
+template <int DB>
+__device__ __forceinline__ uint32_t peers_of(uint32_t d, uint32_t valid_mask)
 {
     uint32_t m = valid_mask;
 #pragma unroll
-    for (int b = 0; b < kDMax; ++b) {
-        if (b < dbits) {
-            const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-            m &= ((d >> b) & 1u) ? bb : ~bb;
-        }
+    for (int b = 0; b < DB; ++b) {
+        const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        m &= ((d >> b) & 1u) ? bb : ~bb;
     }
     return m;
 }
@@ -348,17 +434,35 @@ struct Payload {
     uint8_t *k_out;
 };
 
-template <bool PL>
-__global__ void __launch_bounds__(kT, (kT <= 512 ? 2 : 1)) downsweep(const u64 *__restrict__ kin, const uint32_t *__restrict__ vin,
+// the last pass of a narrow sort writes the output columns itself (what finish_narrow
+// does after the passes otherwise): start and res from the key, end from the stashed
+// duration or a gather, kind from the index's top bits or a gather
+struct Finish {
+    KeyPlan kp;
+    const unsigned int *kind_wide;
+    const u64 *E;
+    const uint8_t *KD;
+    u64 *os, *oe;
+    int32_t *orr;
+    uint8_t *ok;
+    int64_t *perm;
+};
+
+enum { kPlain = 0, kCarry = 1, kFinish = 2 };
+
+// DB (bits per digit) is a template argument: the ballot ranking unrolls exactly DB bits
+template <int MODE, int DB>
+__global__ void __launch_bounds__(kT, HB_SORT_MINB) downsweep(const u64 *__restrict__ kin, const uint32_t *__restrict__ vin,
                                                    u64 *__restrict__ kout, uint32_t *__restrict__ vout, int64_t n,
-                                                   int shift, int dbits, const uint32_t *__restrict__ offs,
-                                                   int64_t tiles, Payload pl)
+                                                   int shift, const uint32_t *__restrict__ offs,
+                                                   int64_t tiles, Payload pl, Finish fin)
 {
+    constexpr bool PL = MODE == kCarry;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PassSmem &sm = *reinterpret_cast<PassSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t bins = 1u << dbits;
-    const u64 mask = bins - 1;
+    constexpr uint32_t bins = 1u << DB;
+    constexpr u64 mask = bins - 1;
     const int64_t tile = blockIdx.x;
     for (int i = tid; i < kW * kBins; i += kT) (&sm.whist[0][0])[i] = 0;
     for (int d = tid; d < (int)bins; d += kT) sm.gbase[d] = offs[(int64_t)d * tiles + tile];
@@ -385,7 +489,7 @@ __global__ void __launch_bounds__(kT, (kT <= 512 ? 2 : 1)) downsweep(const u64 *
     for (int j = 0; j < kI; ++j) {
         const bool valid = j * 32 + lane < wrem;
         const uint32_t dj = (uint32_t)((k[j] >> shift) & mask);
-        const uint32_t pm = peers_of(dj, dbits, __ballot_sync(0xffffffffu, valid));
+        const uint32_t pm = peers_of<DB>(dj, __ballot_sync(0xffffffffu, valid));
         const int leader = __ffs(pm) - 1;
         const uint32_t b = valid ? sm.whist[warp][dj] : 0u;
         __syncwarp();
@@ -393,6 +497,12 @@ __global__ void __launch_bounds__(kT, (kT <= 512 ? 2 : 1)) downsweep(const u64 *
         __syncwarp();
         rk[j >> 1] |= (b + __popc(pm & lt)) << (16 * (j & 1));
     }
+#if HB_SORT_VEARLY
+    // the index column's loads overlap the digit scan below
+    uint32_t vv[kI];
+#pragma unroll
+    for (int j = 0; j < kI; ++j) vv[j] = j * 32 + lane < wrem ? __ldcs(vin + wbase + j * 32 + lane) : 0u;
+#endif
     __syncthreads();
     // per digit: warp-exclusive offsets and the tile total
     uint32_t total = 0;
@@ -418,23 +528,47 @@ __global__ void __launch_bounds__(kT, (kT <= 512 ? 2 : 1)) downsweep(const u64 *
             const uint32_t dj = (uint32_t)((k[j] >> shift) & mask);
             const uint32_t pos = sm.bexcl[dj] + sm.whist[warp][dj] + ((rk[j >> 1] >> (16 * (j & 1))) & 0xffffu);
             sm.k[pos] = k[j];
+#if HB_SORT_VEARLY
+            sm.v[pos] = vv[j];
+#else
             sm.v[pos] = __ldcs(vin + wbase + o);
+#endif
             if (PL) sm.src[pos] = (uint16_t)(warp * 32 * kI + o);
         }
     }
     __syncthreads();
     const int cnt = (int)((n - base) < kTileKeys ? (n - base) : kTileKeys);
-    for (int i = tid; i < cnt; i += kT) {
-        const u64 key = sm.k[i];
-        const uint32_t dd = (uint32_t)((key >> shift) & mask);
-        const u64 dst = (u64)sm.gbase[dd] + (u64)(i - (int)sm.bexcl[dd]);
-        kout[dst] = key;
-        vout[dst] = sm.v[i];
-        if (PL) {   // tile-local gather (L2-resident), coalesced digit-run writes
-            const int64_t src = base + sm.src[i];
-            pl.s_out[dst] = __ldg(pl.s_in + src);
-            pl.e_out[dst] = __ldg(pl.e_in + src);
-            pl.k_out[dst] = __ldg(pl.k_in + src);
+    if constexpr (MODE == kFinish) {
+        const KeyPlan &kp = fin.kp;
+        const u64 tmask = kp.bt >= 64 ? ~0ull : ((1ull << kp.bt) - 1);
+        const bool gather_k = !kp.packk || *fin.kind_wide;
+        for (int i = tid; i < cnt; i += kT) {
+            const u64 key = sm.k[i];
+            const uint32_t pv = sm.v[i];
+            const uint32_t dd = (uint32_t)((key >> shift) & mask);
+            const u64 dst = (u64)sm.gbase[dd] + (u64)(i - (int)sm.bexcl[dd]);
+            const uint32_t v = kp.packk ? pv & kIdxMask : pv;
+            const u64 st = (key & tmask) + kp.smin;
+            fin.os[dst] = st;
+            const u64 rbits = kp.bt >= 64 ? 0ull : (key >> kp.bt) & ((1ull << kp.br) - 1);
+            fin.orr[dst] = unflip((unsigned int)rbits + kp.rmin);
+            fin.oe[dst] = kp.dshift ? st + (key >> kp.dshift) : __ldg(fin.E + v);
+            fin.ok[dst] = gather_k ? __ldg(fin.KD + v) : (uint8_t)(pv >> 30);
+            if (fin.perm) fin.perm[dst] = v;
+        }
+    } else {
+        for (int i = tid; i < cnt; i += kT) {
+            const u64 key = sm.k[i];
+            const uint32_t dd = (uint32_t)((key >> shift) & mask);
+            const u64 dst = (u64)sm.gbase[dd] + (u64)(i - (int)sm.bexcl[dd]);
+            kout[dst] = key;
+            vout[dst] = sm.v[i];
+            if (PL) {   // tile-local gather (L2-resident), coalesced digit-run writes
+                const int64_t src = base + sm.src[i];
+                pl.s_out[dst] = __ldg(pl.s_in + src);
+                pl.e_out[dst] = __ldg(pl.e_in + src);
+                pl.k_out[dst] = __ldg(pl.k_in + src);
+            }
         }
     }
 }
@@ -545,6 +679,19 @@ size_t sort_workspace_bytes(int64_t n)
 
 static int bits_of(u64 x) { return x ? 64 - __builtin_clzll(x) : 0; }
 
+using DownFn = void (*)(const u64 *, const uint32_t *, u64 *, uint32_t *, int64_t, int, const uint32_t *, int64_t,
+                        rsort::Payload, rsort::Finish);
+// downsweep instantiations by [mode][bits per digit]
+static DownFn down_table(int mode, int dbits)
+{
+    using namespace rsort;
+#define HB_DS_ROW(M) {nullptr, downsweep<M, 1>, downsweep<M, 2>, downsweep<M, 3>, downsweep<M, 4>, \
+                      downsweep<M, 5>, downsweep<M, 6>, downsweep<M, 7>, downsweep<M, 8>}
+    static const DownFn tbl[3][kDMax + 1] = {HB_DS_ROW(kPlain), HB_DS_ROW(kCarry), HB_DS_ROW(kFinish)};
+#undef HB_DS_ROW
+    return tbl[mode][dbits];
+}
+
 static int grid_for(int64_t n, int sms)
 {
     int64_t g = (n + 511) / 512;
@@ -566,12 +713,13 @@ cudaError_t sort_records(const u64 *S, const u64 *E, const int32_t *R, const uin
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     static bool attr_done = false;
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(downsweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)sizeof(PassSmem));
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(downsweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(PassSmem));
-        if (e != cudaSuccess) return e;
+        for (int mode = 0; mode < 3; ++mode)
+            for (int db = 1; db <= kDMax; ++db) {
+                const cudaError_t e = cudaFuncSetAttribute(down_table(mode, db),
+                                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                           (int)sizeof(PassSmem));
+                if (e != cudaSuccess) return e;
+            }
         attr_done = true;
     }
     const int64_t tiles = tiles_of(n);
@@ -594,7 +742,15 @@ cudaError_t sort_records(const u64 *S, const u64 *E, const int32_t *R, const uin
 
     // 1. key range (one D2H of 32 bytes decides the key layout)
     range_init<<<1, 1, 0, s>>>(range);
-    range_kernel<<<grid_for(n, sms), 512, 0, s>>>(S, E, R, n, range);
+    // one resident wave (4 CTAs of 512 per SM); 16-byte loads when the columns allow them
+    {
+        const bool vec = ((reinterpret_cast<uintptr_t>(S) | reinterpret_cast<uintptr_t>(E)) & 15) == 0 &&
+                         (reinterpret_cast<uintptr_t>(R) & 7) == 0;
+        int64_t g = ((n + 1) / 2 + 511) / 512;
+        g = g < 1 ? 1 : (g > (int64_t)sms * 4 ? (int64_t)sms * 4 : g);
+        if (vec) range_kernel<true><<<(unsigned)g, 512, 0, s>>>(S, E, R, n, range);
+        else range_kernel<false><<<grid_for(n, sms), 512, 0, s>>>(S, E, R, n, range);
+    }
     Range rg;
     if ((e = cudaMemcpyAsync(&rg, range, sizeof(Range), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
@@ -620,6 +776,9 @@ cudaError_t sort_records(const u64 *S, const u64 *E, const int32_t *R, const uin
     // the last pass writes them straight into the output columns
     const bool carry = kp.res_only && stage_bits[0] > 0;
     Payload pl{S, E, KD, nullptr, nullptr, nullptr};
+    // narrow keys: the last pass writes the output columns (no finish kernel)
+    const bool narrow = !kp.wide && !kp.res_only;
+    Finish fin{};
     for (int stage = 0; stage < 2; ++stage) {
         const int bits = stage_bits[stage];
         if (stage == 1 && !kp.wide) break;
@@ -631,30 +790,35 @@ cudaError_t sort_records(const u64 *S, const u64 *E, const int32_t *R, const uin
             kp.dshift = 0;
             const int cover = passes * kp.dbits;
             if (!kp.wide && !kp.res_only && !rg.neg && cover < 64 && bits_of(rg.dmax) <= 64 - cover) kp.dshift = cover;
-            build_keys<<<grid_for(n, sms), 512, 0, s>>>(S, E, R, KD, n, kp, kin, vin, &range->kind_wide);
+            build_keys<<<(unsigned)tiles, kBT, 0, s>>>(S, E, R, KD, n, kp, kin, vin, &range->kind_wide, counts, tiles);
         }
         else build_res_keys<<<grid_for(n, sms), 512, 0, s>>>(R, vin, n, kp, kin);
         for (int p = 0; p < passes; ++p) {
             const int shift = p * kp.dbits;
             const int64_t mm = ((int64_t)1 << kp.dbits) * tiles;   // this pass's matrix (digit-major)
             const int64_t nbb = (mm + kScanBlock - 1) / kScanBlock;
-            upsweep<<<(unsigned)tiles, kUT, 0, s>>>(kin, n, shift, kp.dbits, counts, tiles);
+            if (stage == 1 || p > 0)   // the first pass's counts come from build_keys
+                upsweep<<<(unsigned)tiles, kUT, 0, s>>>(kin, n, shift, kp.dbits, counts, tiles);
             scan_sums<<<(unsigned)nbb, kScanT, 0, s>>>(counts, mm, bsum);
             scan_top<<<1, kScanT, 0, s>>>(bsum, nbb);
             scan_blocks<<<(unsigned)nbb, kScanT, 0, s>>>(counts, mm, bsum);
+            int mode = kPlain;
             if (carry) {
                 const bool to_out = ((passes - 1 - p) & 1) == 0;
                 pl.s_out = to_out ? os : PS;
                 pl.e_out = to_out ? oe : PE;
                 pl.k_out = to_out ? ok : PK;
-                downsweep<true><<<(unsigned)tiles, kT, sizeof(PassSmem), s>>>(kin, vin, kout, vout, n, shift,
-                                                                              kp.dbits, counts, tiles, pl);
+                mode = kCarry;
+            } else if (narrow && p == passes - 1) {
+                fin = Finish{kp, &range->kind_wide, E, KD, os, oe, orr, ok, perm};
+                mode = kFinish;
+            }
+            down_table(mode, kp.dbits)<<<(unsigned)tiles, kT, sizeof(PassSmem), s>>>(kin, vin, kout, vout, n, shift,
+                                                                                   counts, tiles, pl, fin);
+            if (carry) {
                 pl.s_in = pl.s_out;
                 pl.e_in = pl.e_out;
                 pl.k_in = pl.k_out;
-            } else {
-                downsweep<false><<<(unsigned)tiles, kT, sizeof(PassSmem), s>>>(kin, vin, kout, vout, n, shift,
-                                                                               kp.dbits, counts, tiles, pl);
             }
             u64 *tk = kin; kin = kout; kout = tk;
             uint32_t *tv = vin; vin = vout; vout = tv;
@@ -663,7 +827,9 @@ cudaError_t sort_records(const u64 *S, const u64 *E, const int32_t *R, const uin
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     (void)nb;
-    if (!kp.wide && !kp.res_only) {
+    if (narrow && total_passes > 0) {
+        // written by the last pass
+    } else if (narrow) {
         finish_narrow<<<grid_for(n, sms), 512, 0, s>>>(kin, vin, n, kp, &range->kind_wide, E, KD, os, oe, orr, ok,
                                                        perm);
     } else if (carry) {
