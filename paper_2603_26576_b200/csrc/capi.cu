@@ -845,9 +845,11 @@ int heteff_merge_shards(heteff_ctx *ctx, const void *gathered, int32_t world, si
     int64_t ntot = 0, mtot = 0;
     for (int r = 0; r < world; ++r) { ntot += n_of[r]; mtot += m_of[r]; }
     const size_t need = 256 + 32 * (size_t)(ntot + mtot) + 8 * (size_t)world;
-    CK(ensure(ctx->aux, need + 256, false), "alloc merge output");
+    const size_t sizes_at = (256 + 32 * (size_t)(ntot + mtot) + 255) & ~(size_t)255;
+    const size_t scratch_at = (sizes_at + 8 * (size_t)world + 255) & ~(size_t)255;
+    CK(ensure(ctx->aux, scratch_at + hb::merge_scratch_bytes() + 256, false), "alloc merge output");
     uint8_t *dout = static_cast<uint8_t *>(ctx->aux.p);
-    int32_t *sizes_d = reinterpret_cast<int32_t *>(dout + ((256 + 32 * (size_t)(ntot + mtot) + 255) & ~(size_t)255));
+    int32_t *sizes_d = reinterpret_cast<int32_t *>(dout + sizes_at);
     if (ctx->out_pin_bytes < need) {
         if (ctx->out_pin) cudaFreeHost(ctx->out_pin);
         ctx->out_pin = nullptr;
@@ -860,7 +862,7 @@ int heteff_merge_shards(heteff_ctx *ctx, const void *gathered, int32_t world, si
     CK(cudaMemcpyAsync(sizes_d, sizes_h, 8 * (size_t)world, cudaMemcpyHostToDevice, s), "h2d sizes");
     CK(cudaEventRecord(ctx->ev0, s), "event");
     CK(hb::launch_merge(gathered, world, block_bytes, n_max, m_max, sizes_d, sizes_d + world, dout,
-                        (const u64 *)elapsed_dev, s),
+                        (const u64 *)elapsed_dev, dout + scratch_at, ntot + mtot, s),
        "launch merge");
     CK(cudaEventRecord(ctx->ev1, s), "event");
     const bool sums = out && (out->host_summaries || out->device_summaries);

@@ -2422,23 +2422,39 @@ cudaError_t launch_overlap_pass_v(const void *p, u64 *scratch, cudaStream_t s)
 int tile_records() { return kTile; }
 
 // =========================================================================
-// multi-GPU merge of gathered per-rank result blocks (one CTA).  Every rank
+// multi-GPU merge of gathered per-rank result blocks.  Every rank
 // ran two launches into its block [host header 256 B | device header 256 B |
 // host rows [n_max][4] | device rows [m_max][4]]: its host records
 // (SUMMARIZE_HOST) and, after the all-reduce of E, its device records
 // clamped at the GLOBAL E (SUMMARIZE_DEVICE, window read from device memory).
-// The merge concatenates the rows in rank order and evaluates both metric
-// trees; a non-OK shard makes it defer (status -2) to the host path.
+// The merge concatenates the rows in rank order (every CTA a strided share,
+// with partial sums / maxima) and the last CTA to finish reduces the partials
+// and evaluates both metric trees; a non-OK shard makes it defer (status -2)
+// to the host path.
 // =========================================================================
-__global__ void __launch_bounds__(1024) merge_kernel(const uint8_t *blocks, int32_t world, size_t block_bytes,
-                                                     int32_t n_max, int32_t m_max, const int32_t *n_of,
-                                                     const int32_t *m_of, uint8_t *out, const u64 *E_global)
+constexpr int kMergeT = 256;
+struct MergeScratch {
+    unsigned int done;   // CTAs finished (zeroed before every launch)
+    unsigned int pad[3];
+    u128 part[kMergeCTAs][6];   // per CTA: sum u, sum u+w, max u+w, sum k, max k, max k+m
+};
+
+__device__ __forceinline__ u128 ldcg128(const u128 *p)
+{
+    const u64 *q = reinterpret_cast<const u64 *>(p);
+    return ((u128)__ldcg(q + 1) << 64) | __ldcg(q);
+}
+
+__global__ void __launch_bounds__(kMergeT) merge_kernel(const uint8_t *blocks, int32_t world, size_t block_bytes,
+                                                        int32_t n_max, int32_t m_max, const int32_t *n_of,
+                                                        const int32_t *m_of, uint8_t *out, const u64 *E_global,
+                                                        MergeScratch *ms)
 {
     __shared__ u128 scratch[33];
+    __shared__ int s_defer, s_last;
     const int tid = threadIdx.x, nt = blockDim.x;
     ResultDev *res = reinterpret_cast<ResultDev *>(out);
     const u64 E = ld_relaxed(E_global);
-    __shared__ int s_defer;
     if (tid == 0) {
         int defer = 0;
         for (int r = 0; r < world; ++r) {
@@ -2448,58 +2464,91 @@ __global__ void __launch_bounds__(1024) merge_kernel(const uint8_t *blocks, int3
             if (h->status != 0 || d->status != 0) defer = 1;
         }
         s_defer = defer;
-        res->status = defer ? -2 : (E == 0 ? 2 : 0);
-        res->elapsed = E;
-        res->host_elapsed = E;
-        res->host_mask = res->device_mask = 0;
+        if (blockIdx.x == 0) {
+            res->status = defer ? -2 : (E == 0 ? 2 : 0);
+            res->elapsed = E;
+            res->host_elapsed = E;
+            res->host_mask = res->device_mask = 0;
+        }
     }
     __syncthreads();
     if (s_defer) return;
-    int32_t ntot = 0, mtot = 0;
+    int64_t ntot = 0, mtot = 0;
     for (int r = 0; r < world; ++r) { ntot += n_of[r]; mtot += m_of[r]; }
     u64 *hout = reinterpret_cast<u64 *>(out + 256);
     u64 *dout = hout + 4 * (size_t)ntot;
     u128 su = 0, suw = 0, muw = 0, sk = 0, mk = 0, mkm = 0;
-    int32_t hb = 0, db = 0;
-    for (int r = 0; r < world; ++r) {
+    for (int64_t g = (int64_t)blockIdx.x * nt + tid; g < ntot + mtot; g += (int64_t)gridDim.x * nt) {
+        const bool host = g < ntot;
+        int64_t i = host ? g : g - ntot;
+        int r = 0;
+        for (; r < world - 1; ++r) {   // the rank holding row i (rank order)
+            const int32_t k = host ? n_of[r] : m_of[r];
+            if (i < k) break;
+            i -= k;
+        }
         const u64 *hr = reinterpret_cast<const u64 *>(blocks + (size_t)r * block_bytes + 512);
-        const u64 *dr = hr + 4 * (size_t)n_max;
-        for (int32_t i = tid; i < n_of[r]; i += nt) {
-            const u64 *x = hr + 4 * (size_t)i;
-            u64 *o = hout + 4 * (size_t)(hb + i);
-            o[0] = x[0]; o[1] = x[1]; o[2] = x[2]; o[3] = x[3];
-            const u128 uw = (u128)x[0] + x[1];
-            su += x[0];
+        const u64 *x = (host ? hr : hr + 4 * (size_t)n_max) + 4 * (size_t)i;
+        const ulonglong2 x01 = *reinterpret_cast<const ulonglong2 *>(x);
+        const ulonglong2 x23 = *reinterpret_cast<const ulonglong2 *>(x + 2);
+        u64 *o = (host ? hout : dout) + 4 * (size_t)(host ? g : g - ntot);
+        *reinterpret_cast<ulonglong2 *>(o) = x01;
+        *reinterpret_cast<ulonglong2 *>(o + 2) = x23;
+        if (host) {
+            const u128 uw = (u128)x01.x + x01.y;
+            su += x01.x;
             suw += uw;
             if (uw > muw) muw = uw;
-        }
-        for (int32_t i = tid; i < m_of[r]; i += nt) {
-            const u64 *x = dr + 4 * (size_t)i;
-            u64 *o = dout + 4 * (size_t)(db + i);
-            o[0] = x[0]; o[1] = x[1]; o[2] = x[2]; o[3] = x[3];
-            sk += x[0];
-            if ((u128)x[0] > mk) mk = x[0];
-            const u128 km = (u128)x[0] + x[1];
+        } else {
+            sk += x01.x;
+            if ((u128)x01.x > mk) mk = x01.x;
+            const u128 km = (u128)x01.x + x01.y;
             if (km > mkm) mkm = km;
         }
-        hb += n_of[r];
-        db += m_of[r];
     }
-    su = block_reduce128<false>(su, scratch, tid, nt);
-    suw = block_reduce128<false>(suw, scratch, tid, nt);
-    muw = block_reduce128<true>(muw, scratch, tid, nt);
-    sk = block_reduce128<false>(sk, scratch, tid, nt);
-    mk = block_reduce128<true>(mk, scratch, tid, nt);
-    mkm = block_reduce128<true>(mkm, scratch, tid, nt);
+    u128 v[6] = {su, suw, muw, sk, mk, mkm};
+    constexpr bool kMax[6] = {false, false, true, false, true, true};
+#pragma unroll
+    for (int k = 0; k < 6; ++k)
+        v[k] = kMax[k] ? block_reduce128<true>(v[k], scratch, tid, nt) : block_reduce128<false>(v[k], scratch, tid, nt);
+    if (tid == 0) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) ms->part[blockIdx.x][k] = v[k];
+        __threadfence();
+        s_last = atomicAdd(&ms->done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // the last CTA: every CTA's partials
+    u128 a[6] = {0, 0, 0, 0, 0, 0};
+    for (int b = tid; b < (int)gridDim.x; b += nt) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            const u128 x = ldcg128(&ms->part[b][k]);
+            a[k] = kMax[k] ? (x > a[k] ? x : a[k]) : a[k] + x;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k)
+        a[k] = kMax[k] ? block_reduce128<true>(a[k], scratch, tid, nt) : block_reduce128<false>(a[k], scratch, tid, nt);
     if (E == 0) return;
-    metric_trees(res, ntot >= 1, mtot >= 1, E, ntot, mtot, su, suw, muw, sk, mk, mkm, tid);
+    metric_trees(res, ntot >= 1, mtot >= 1, E, (int32_t)ntot, (int32_t)mtot, a[0], a[1], a[2], a[3], a[4], a[5], tid);
 }
 
+size_t merge_scratch_bytes() { return sizeof(MergeScratch); }
+
 cudaError_t launch_merge(const void *blocks, int32_t world, size_t block_bytes, int32_t n_max, int32_t m_max,
-                         const int32_t *n_of, const int32_t *m_of, void *out, const u64 *E_global, cudaStream_t s)
+                         const int32_t *n_of, const int32_t *m_of, void *out, const u64 *E_global, void *scratch,
+                         int64_t rows, cudaStream_t s)
 {
-    merge_kernel<<<1, 1024, 0, s>>>(static_cast<const uint8_t *>(blocks), world, block_bytes, n_max, m_max, n_of,
-                                    m_of, static_cast<uint8_t *>(out), E_global);
+    MergeScratch *ms = static_cast<MergeScratch *>(scratch);
+    cudaError_t e = cudaMemsetAsync(&ms->done, 0, sizeof(unsigned int), s);
+    if (e != cudaSuccess) return e;
+    int64_t g = (rows + kMergeT - 1) / kMergeT;
+    g = g < 1 ? 1 : (g > kMergeCTAs ? kMergeCTAs : g);
+    merge_kernel<<<(unsigned)g, kMergeT, 0, s>>>(static_cast<const uint8_t *>(blocks), world, block_bytes, n_max, m_max,
+                                                 n_of, m_of, static_cast<uint8_t *>(out), E_global, ms);
     return cudaGetLastError();
 }
 

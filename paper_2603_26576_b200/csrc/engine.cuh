@@ -113,8 +113,13 @@ cudaError_t launch_metrics(const u64 *summaries, int32_t k, u64 elapsed, int hos
                            cudaStream_t s);
 // CSR offsets [ids + 1] -> res[n] (dense id of every record)
 cudaError_t launch_expand_res(const int64_t *seg, int32_t ids, int64_t n, int32_t *res, cudaStream_t s);
+// the merge runs on up to kMergeCTAs CTAs; the last one to finish reduces their partial
+// aggregates (scratch: merge_scratch_bytes() of device memory)
+constexpr int kMergeCTAs = 148;
+size_t merge_scratch_bytes();
 cudaError_t launch_merge(const void *blocks, int32_t world, size_t block_bytes, int32_t n_max, int32_t m_max,
-                         const int32_t *n_of, const int32_t *m_of, void *out, const u64 *E_global, cudaStream_t s);
+                         const int32_t *n_of, const int32_t *m_of, void *out, const u64 *E_global, void *scratch,
+                         int64_t rows, cudaStream_t s);
 // error path: exact host-overlap findings (only when ovl_suspect), then finalize
 cudaError_t launch_overlap_pass(const Params &p, u64 *scratch, cudaStream_t s);
 cudaError_t launch_covers(const Params &p, const int64_t *err_idx, int64_t count, int64_t *cover, cudaStream_t s);
