@@ -2,6 +2,7 @@
 // self-cleaning device workspace, host staging, result copy-back.
 #include <cuda_runtime.h>
 #include <climits>
+#include <cstddef>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -473,7 +474,9 @@ static int run_split(heteff_ctx *ctx, const heteff_trace *t, heteff_result *resu
     const size_t bytes = 512 + 32 * ((size_t)n + (size_t)m);
     CK(ensure(ctx->split, bytes + 256, true), "alloc split block");
     uint8_t *blk = static_cast<uint8_t *>(ctx->split.p);
-    u64 *e_dev = reinterpret_cast<u64 *>(blk + ((bytes + 127) & ~(size_t)127));
+    // the device pass and the merge read E where the host pass's finalize writes it: the
+    // host header's host_elapsed (the device pass's header goes to blk + 256)
+    u64 *e_dev = reinterpret_cast<u64 *>(blk + offsetof(hb::ResultDev, host_elapsed));
     heteff_trace th = *t, td = *t;   // host records only / device records only
     th.dev.count = 0; th.dev.start = th.dev.end = nullptr; th.dev.res = nullptr; th.dev.kind = nullptr;
     th.dev_ids = 0; th.m = 0; th.dev_decl = nullptr; th.dev_seg = nullptr;
@@ -489,7 +492,6 @@ static int run_split(heteff_ctx *ctx, const heteff_trace *t, heteff_result *resu
     CK(cudaEventRecord(ctx->ev_split0, s), "event");
     int rc = run_once(ctx, &th, &oh, &r, nullptr, s, nullptr, &into);
     if (rc != HETEFF_OK) return rc;
-    CK(cudaMemcpyAsync(e_dev, blk + 16, 8, cudaMemcpyDeviceToDevice, s), "E");   // the host header's elapsed
     rc = run_once(ctx, &td, &od, &r, nullptr, s, nullptr, &into);
     if (rc != HETEFF_OK) return rc;
     // the block (both headers' finding counts, the device rows' clamp counts) comes back with
