@@ -494,16 +494,17 @@ static int run_split(heteff_ctx *ctx, const heteff_trace *t, heteff_result *resu
     if (rc != HETEFF_OK) return rc;
     rc = run_once(ctx, &td, &od, &r, nullptr, s, nullptr, &into);
     if (rc != HETEFF_OK) return rc;
-    // the block (both headers' finding counts, the device rows' clamp counts) comes back with
-    // the merged result: enqueued before the merge, whose sync covers it
-    if (ctx->split_pin_bytes < bytes) {
+    // both passes' headers (finding counts) come back with the merged result: enqueued before
+    // the merge, whose sync covers them; the merge sums the device rows' clamp counts
+    constexpr size_t kHeads = 512;
+    if (ctx->split_pin_bytes < kHeads) {
         if (ctx->split_pin) cudaFreeHost(ctx->split_pin);
         ctx->split_pin = nullptr;
         ctx->split_pin_bytes = 0;
-        CK(cudaMallocHost(&ctx->split_pin, bytes), "alloc pinned split block");
-        ctx->split_pin_bytes = bytes;
+        CK(cudaMallocHost(&ctx->split_pin, kHeads), "alloc pinned split headers");
+        ctx->split_pin_bytes = kHeads;
     }
-    CK(cudaMemcpyAsync(ctx->split_pin, blk, bytes, cudaMemcpyDeviceToHost, s), "d2h split block");
+    CK(cudaMemcpyAsync(ctx->split_pin, blk, kHeads, cudaMemcpyDeviceToHost, s), "d2h split headers");
     const int32_t n_of = n, m_of = m;
     rc = heteff_merge_shards(ctx, blk, 1, bytes, n, m, &n_of, &m_of, reinterpret_cast<const uint64_t *>(e_dev), result,
                              out, s);
@@ -515,12 +516,10 @@ static int run_split(heteff_ctx *ctx, const heteff_trace *t, heteff_result *resu
     const uint8_t *hb_ = static_cast<const uint8_t *>(ctx->split_pin);
     const hb::ResultDev *hdr = reinterpret_cast<const hb::ResultDev *>(hb_);   // [0] host pass, at 256 the device pass
     const hb::ResultDev &hdev = *reinterpret_cast<const hb::ResultDev *>(hb_ + 256);
-    const u64 *rows = reinterpret_cast<const u64 *>(hb_ + 512 + 32 * (size_t)n);
-    // the late-device count is the clamp count (E = host elapsed)
-    u64 late = 0;
-    for (int32_t q = 0; q < m; ++q) late += rows[4 * (size_t)q + 3];
+    // the late-device count is the clamp count (E = host elapsed), summed by the merge
+    const hb::ResultDev &merged = *static_cast<const hb::ResultDev *>(ctx->out_pin);
     for (int i = 0; i < 8; ++i) result->counts[i] = hdr[0].counts[i] + hdev.counts[i];
-    result->counts[7] = (int64_t)late;
+    result->counts[7] = merged.counts[7];
     result->host_elapsed = result->elapsed;
     result->dev_max_end = 0;
     result->contract_flags = 0;

@@ -2436,7 +2436,7 @@ constexpr int kMergeT = 256;
 struct MergeScratch {
     unsigned int done;   // CTAs finished (zeroed before every launch)
     unsigned int pad[3];
-    u128 part[kMergeCTAs][6];   // per CTA: sum u, sum u+w, max u+w, sum k, max k, max k+m
+    u128 part[kMergeCTAs][7];   // per CTA: sum u, sum u+w, max u+w, sum k, max k, max k+m, sum clamp
 };
 
 __device__ __forceinline__ u128 ldcg128(const u128 *p)
@@ -2477,7 +2477,7 @@ __global__ void __launch_bounds__(kMergeT) merge_kernel(const uint8_t *blocks, i
     for (int r = 0; r < world; ++r) { ntot += n_of[r]; mtot += m_of[r]; }
     u64 *hout = reinterpret_cast<u64 *>(out + 256);
     u64 *dout = hout + 4 * (size_t)ntot;
-    u128 su = 0, suw = 0, muw = 0, sk = 0, mk = 0, mkm = 0;
+    u128 su = 0, suw = 0, muw = 0, sk = 0, mk = 0, mkm = 0, scl = 0;
     for (int64_t g = (int64_t)blockIdx.x * nt + tid; g < ntot + mtot; g += (int64_t)gridDim.x * nt) {
         const bool host = g < ntot;
         int64_t i = host ? g : g - ntot;
@@ -2504,16 +2504,17 @@ __global__ void __launch_bounds__(kMergeT) merge_kernel(const uint8_t *blocks, i
             if ((u128)x01.x > mk) mk = x01.x;
             const u128 km = (u128)x01.x + x01.y;
             if (km > mkm) mkm = km;
+            scl += x23.y;   // records clamped at E
         }
     }
-    u128 v[6] = {su, suw, muw, sk, mk, mkm};
-    constexpr bool kMax[6] = {false, false, true, false, true, true};
+    u128 v[7] = {su, suw, muw, sk, mk, mkm, scl};
+    constexpr bool kMax[7] = {false, false, true, false, true, true, false};
 #pragma unroll
-    for (int k = 0; k < 6; ++k)
+    for (int k = 0; k < 7; ++k)
         v[k] = kMax[k] ? block_reduce128<true>(v[k], scratch, tid, nt) : block_reduce128<false>(v[k], scratch, tid, nt);
     if (tid == 0) {
 #pragma unroll
-        for (int k = 0; k < 6; ++k) ms->part[blockIdx.x][k] = v[k];
+        for (int k = 0; k < 7; ++k) ms->part[blockIdx.x][k] = v[k];
         __threadfence();
         s_last = atomicAdd(&ms->done, 1u) == gridDim.x - 1;
     }
@@ -2521,17 +2522,18 @@ __global__ void __launch_bounds__(kMergeT) merge_kernel(const uint8_t *blocks, i
     if (!s_last) return;
     __threadfence();
     // the last CTA: every CTA's partials
-    u128 a[6] = {0, 0, 0, 0, 0, 0};
+    u128 a[7] = {0, 0, 0, 0, 0, 0, 0};
     for (int b = tid; b < (int)gridDim.x; b += nt) {
 #pragma unroll
-        for (int k = 0; k < 6; ++k) {
+        for (int k = 0; k < 7; ++k) {
             const u128 x = ldcg128(&ms->part[b][k]);
             a[k] = kMax[k] ? (x > a[k] ? x : a[k]) : a[k] + x;
         }
     }
 #pragma unroll
-    for (int k = 0; k < 6; ++k)
+    for (int k = 0; k < 7; ++k)
         a[k] = kMax[k] ? block_reduce128<true>(a[k], scratch, tid, nt) : block_reduce128<false>(a[k], scratch, tid, nt);
+    if (tid == 0) res->counts[7] = (int64_t)(u64)a[6];   // late device records (clamped at the global E)
     if (E == 0) return;
     metric_trees(res, ntot >= 1, mtot >= 1, E, (int32_t)ntot, (int32_t)mtot, a[0], a[1], a[2], a[3], a[4], a[5], tid);
 }
