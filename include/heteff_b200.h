@@ -377,8 +377,9 @@ int heteff_analyze_regions(heteff_ctx *ctx, const heteff_trace *trace, const het
  *   3. heteff_analyze_into(SUMMARIZE_DEVICE, HETEFF_FLAG_ELAPSED_DEVICE_PTR -> the
  *      all-reduced E) on its device records -> block device header + device rows,
  *      clamped at the GLOBAL E (summarize.py:88-89, :113);
- *   4. all-gather of the fixed-size blocks; 5. heteff_merge_shards: one kernel,
- *      concatenated summaries + both metric trees, one small D2H.
+ *   4. all-gather of the fixed-size blocks; 5. heteff_merge_shards: one kernel launch
+ *      (up to 148 CTAs; the last to finish reduces) -- concatenated summaries + both
+ *      metric trees, one small D2H.
  * Block: [host header 256 B | device header 256 B | host rows [n_max][4] |
  * device rows [m_max][4]], block_bytes >= 512 + 32 (n_max + m_max).  Every record
  * is read once, as in the single-GPU launch.  heteff_merge_shards returns
