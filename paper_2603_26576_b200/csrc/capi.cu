@@ -329,6 +329,7 @@ static int run_once(heteff_ctx *ctx, const heteff_trace *t, const heteff_options
         p.res = reinterpret_cast<hb::ResultDev *>(b + (opt->mode == HETEFF_MODE_SUMMARIZE_DEVICE ? 256 : 0));
         p.host_out = reinterpret_cast<u64 *>(b + 512);
         p.dev_out = reinterpret_cast<u64 *>(b + 512 + (size_t)into->n_max * 32);
+        p.settle = 1;   // no error-path kernels follow in block mode (status -1 defers)
         CK(K.launch(&p, ctx->grid[comp], s), "launch analyze");
         return HETEFF_OK;
     }
@@ -458,6 +459,7 @@ static bool split_wanted(const heteff_trace *t, const heteff_options *opt)
 {
     if (opt->mode != HETEFF_MODE_REPORT || opt->flags != 0 || opt->list_capacity != 0) return false;
     if (t->n < 1 || t->m < 1 || getenv("HETEFF_NO_SPLIT")) return false;
+    if (getenv("HETEFF_FORCE_SPLIT")) return true;   // tests / stress: every eligible call
     const int64_t min = getenv("HETEFF_SPLIT_MIN") ? atoll(getenv("HETEFF_SPLIT_MIN")) : ((int64_t)1 << 26);
     if (t->host.count < min || t->dev.count < min || 4 * t->host.count < t->host.count + t->dev.count) return false;
     heteff_trace h = *t, d = *t;

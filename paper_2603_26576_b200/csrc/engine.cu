@@ -2165,7 +2165,13 @@ __global__ void __launch_bounds__(kThreads, HB_MINB) analyze_kernel(const __grid
         __threadfence();
         if (*(volatile unsigned *)&p.g->ovl_suspect) {
             // host records overlap somewhere: the exact findings come from the
-            // error-path kernels (launch_overlap_pass), which then finalize
+            // error-path kernels (launch_overlap_pass), which then finalize -- or, in block
+            // mode, from the caller's fallback: finalize now (the context's accumulators and
+            // globals reset for the next call) and keep the status "pending"
+            if (p.settle) {
+                finalize(p, reinterpret_cast<u128 *>(smem_raw), tid);
+                __syncthreads();
+            }
             if (tid == 0) p.res->status = -1;
         } else {
             finalize(p, reinterpret_cast<u128 *>(smem_raw), tid);

@@ -85,6 +85,10 @@ struct Params {
     u64 host_elapsed_floor;
     int32_t mode;
     int32_t use_tma;
+    // 1: block mode (heteff_analyze_into): a trace with suspected host overlaps is
+    // finalized right away (context state reset) and reported as status -1, so the
+    // caller's fallback path re-runs it; 0: the error-path kernels finalize it
+    int32_t settle;
     u64 elapsed_arg;
     const u64 *elapsed_ptr;   // SUMMARIZE_DEVICE: the window read from device memory (multi-GPU: all-reduced E)
     int64_t cap;

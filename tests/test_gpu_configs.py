@@ -202,3 +202,44 @@ def test_split_analysis_equals_the_single_launch():
     assert a.counts[7] > 0                       # late device records: the clamp-count hand-over is exercised
     assert np.array_equal(a.host_sum, b.host_sum) and np.array_equal(a.dev_sum, b.dev_sum)
     assert a.host_metrics == b.host_metrics and a.device_metrics == b.device_metrics
+
+
+@pytest.mark.gpu
+def test_block_mode_overlap_leaves_the_context_clean():
+    """A block-mode launch (the split analysis, heteff_analyze_into) on a trace whose host
+    records overlap defers (status -1) without the error-path kernels; the kernel must still
+    reset the context's accumulators and globals, so the fallback answer and the NEXT call on
+    the same context equal the oracle's (found by tools/stress.py under HETEFF_FORCE_SPLIT)."""
+    import os
+
+    import torch
+
+    from oracle import oracle as O
+    from paper_2603_26576_b200.engine import DeviceTrace
+
+    def cols(s, e, r, k):
+        return (np.array(s, np.uint64), np.array(e, np.uint64), np.array(r, np.int32), np.array(k, np.uint8))
+
+    def cu(x):
+        return torch.from_numpy(x.view(np.int64) if x.dtype == np.uint64 else x).cuda()
+
+    bad_h = cols([0, 5, 0], [10, 15, 30], [0, 0, 1], [0, 0, 1])            # rank 0 overlaps itself
+    good_h = cols([0, 12, 0], [10, 20, 30], [0, 0, 1], [0, 1, 0])
+    d = cols([1, 4, 2], [3, 25, 9], [0, 0, 1], [0, 1, 0])
+    old = os.environ.get("HETEFF_FORCE_SPLIT")
+    os.environ["HETEFF_FORCE_SPLIT"] = "1"
+    try:
+        for h in (bad_h, good_h, bad_h, good_h):
+            dt = DeviceTrace(*(cu(x) for x in (*h, *d)), 2, 2)
+            got = analyze_device(dt)
+            ref = O.analyze(h, d, 2, 2, mode=N.MODE_REPORT, cap=0)
+            assert got.status == ref.status
+            if ref.status == N.OK:
+                assert got.elapsed == ref.elapsed
+                assert np.array_equal(got.host_sum, ref.host_sum) and np.array_equal(got.dev_sum, ref.dev_sum)
+                assert got.host_metrics == ref.host_metrics and got.device_metrics == ref.device_metrics
+    finally:
+        if old is None:
+            os.environ.pop("HETEFF_FORCE_SPLIT", None)
+        else:
+            os.environ["HETEFF_FORCE_SPLIT"] = old
