@@ -175,7 +175,9 @@ int heteff_set_grid(heteff_ctx *ctx, int grid);
 /* The tile geometry of the analysis kernel compilation the context's last analysis used
    ("15x11" for CSR inputs; "11x15" or "8x19" for res columns, by device run length;
    "split: host <g>, device <g>" when a large REPORT call ran its two sides as two launches --
-   DESIGN.md section 5), or "" before the first one.  Valid until the next call. */
+   DESIGN.md section 5), or "" before the first one.  Valid until the next call.
+   Environment: HETEFF_NO_SPLIT=1 never splits; HETEFF_FORCE_SPLIT=1 splits every eligible
+   REPORT call (tests). */
 const char *heteff_kernel_name(const heteff_ctx *ctx);
 
 /* trace columns in device memory */
